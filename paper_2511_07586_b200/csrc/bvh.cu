@@ -1,0 +1,335 @@
+// K1: LBVH builder on the GPU (replaces Scene::build_bvh, proj/src/geometry.cpp:68-144,
+// a single-threaded fp64 median split).
+//
+//   1. prim_kernel      per triangle: fp64 AABB padded by box_pad and rounded
+//                       outward to fp32; 63-bit Morton code of the centroid.
+//   2. cub radix sort   (morton, id) pairs.
+//   3. karras_kernel    Karras (HPG 2012) binary radix tree over the sorted codes
+//                       (ties broken by sort position), one thread per inner node.
+//   4. refit_kernel     bottom-up AABB union with one atomic flag per inner node.
+//   5. emit_kernel      64-B two-child nodes; any child subtree holding <= 4
+//                       triangles becomes a leaf reference to its contiguous
+//                       sorted range (the LBVH ranges are contiguous).
+//   6. tri_kernel       leaf-ordered fp64 triangle records (a, e1, e2, id).
+//
+// Exactness: the tree only culls.  Boxes are conservative (outward rounding
+// + padding), the triangle test that decides hits runs in fp64 with the
+// reference's arithmetic, so closest hits equal brute force
+// (Scene::intersect_brute_force, geometry.cpp:218-240) for ANY tree shape.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdio>
+
+#include "internal.h"
+
+namespace mcsbr_int {
+
+namespace {
+
+__device__ __forceinline__ uint64_t expand21(uint64_t v) {
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+struct Box {
+    float lo[3], hi[3];
+};
+
+__global__ void prim_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri, uint32_t n,
+                            double lox, double loy, double loz, double sx, double sy, double sz,
+                            double cx, double cy, double cz, double pad, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                            float4* __restrict__ box_lo, float4* __restrict__ box_hi) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4 t = tri[i];
+    const double* a = vtx + 3ull * t.x;
+    const double* b = vtx + 3ull * t.y;
+    const double* c = vtx + 3ull * t.z;
+    float lo[3], hi[3];
+    double cen[3];
+    const double ctr[3] = {cx, cy, cz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double mn = fmin(a[k], fmin(b[k], c[k]));
+        const double mx = fmax(a[k], fmax(b[k], c[k]));
+        lo[k] = __double2float_rd((mn - ctr[k]) - pad);
+        hi[k] = __double2float_ru((mx - ctr[k]) + pad);
+        cen[k] = (a[k] + b[k] + c[k]) * (1.0 / 3.0);
+    }
+    box_lo[i] = make_float4(lo[0], lo[1], lo[2], 0.f);
+    box_hi[i] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    const double qx = fmin(fmax((cen[0] - lox) * sx, 0.0), 2097151.0);
+    const double qy = fmin(fmax((cen[1] - loy) * sy, 0.0), 2097151.0);
+    const double qz = fmin(fmax((cen[2] - loz) * sz, 0.0), 2097151.0);
+    keys[i] = (expand21(static_cast<uint64_t>(qx)) << 2) | (expand21(static_cast<uint64_t>(qy)) << 1) |
+              expand21(static_cast<uint64_t>(qz));
+    ids[i] = i;
+}
+
+__device__ __forceinline__ int delta(const uint64_t* __restrict__ k, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    const uint64_t a = k[i], b = k[j];
+    if (a != b) return __clzll(static_cast<long long>(a ^ b));
+    return 64 + __clz(static_cast<int>(static_cast<uint32_t>(i) ^ static_cast<uint32_t>(j)));
+}
+
+// inner node i in [0, n-2]; child encoding: c >= 0 inner node c, c < 0 leaf ~c
+__global__ void karras_kernel(const uint64_t* __restrict__ k, int n, int2* __restrict__ child,
+                              int2* __restrict__ range, int* __restrict__ parent_inner,
+                              int* __restrict__ parent_leaf) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+    const int dmin = delta(k, n, i, i - d);
+    int lmax = 2;
+    while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int t = lmax >> 1; t >= 1; t >>= 1)
+        if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+    const int j = i + l * d;
+    const int dnode = delta(k, n, i, j);
+    int s = 0;
+    int t = l;
+    do {
+        t = (t + 1) >> 1;
+        if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    const int gamma = i + s * d + min(d, 0);
+    const int first = min(i, j), last = max(i, j);
+    const int left = (first == gamma) ? ~gamma : gamma;
+    const int right = (last == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+    child[i] = make_int2(left, right);
+    range[i] = make_int2(first, last);
+    if (left >= 0) parent_inner[left] = i; else parent_leaf[~left] = i;
+    if (right >= 0) parent_inner[right] = i; else parent_leaf[~right] = i;
+}
+
+__device__ __forceinline__ void load_box(int c, const float4* __restrict__ ilo,
+                                         const float4* __restrict__ ihi, const float4* __restrict__ llo,
+                                         const float4* __restrict__ lhi, float4& lo, float4& hi) {
+    if (c >= 0) {
+        lo = __ldcg(ilo + c);
+        hi = __ldcg(ihi + c);
+    } else {
+        lo = llo[~c];
+        hi = lhi[~c];
+    }
+}
+
+__global__ void refit_kernel(int n, const int2* __restrict__ child, const int* __restrict__ parent_inner,
+                             const int* __restrict__ parent_leaf, const float4* __restrict__ llo,
+                             const float4* __restrict__ lhi, float4* ilo, float4* ihi, int* flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int p = parent_leaf[i];
+    while (p >= 0) {
+        __threadfence();
+        if (atomicAdd(flags + p, 1) == 0) return;  // first arrival: sibling not done yet
+        __threadfence();
+        const int2 c = child[p];
+        float4 a0, a1, b0, b1;
+        load_box(c.x, ilo, ihi, llo, lhi, a0, a1);
+        load_box(c.y, ilo, ihi, llo, lhi, b0, b1);
+        __stcg(ilo + p, make_float4(fminf(a0.x, b0.x), fminf(a0.y, b0.y), fminf(a0.z, b0.z), 0.f));
+        __stcg(ihi + p, make_float4(fmaxf(a1.x, b1.x), fmaxf(a1.y, b1.y), fmaxf(a1.z, b1.z), 0.f));
+        p = parent_inner[p];
+    }
+}
+
+__device__ __forceinline__ int child_ref(int c, const int2* __restrict__ range) {
+    if (c < 0) return ~((~c) << 3 | 1);
+    const int2 r = range[c];
+    const int cnt = r.y - r.x + 1;
+    if (cnt <= kLeafMax) return ~(r.x << 3 | cnt);
+    return c;
+}
+
+__global__ void emit_kernel(int n, const int2* __restrict__ child, const int2* __restrict__ range,
+                            const float4* __restrict__ ilo, const float4* __restrict__ ihi,
+                            const float4* __restrict__ llo, const float4* __restrict__ lhi,
+                            float4* __restrict__ nodes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int2 c = child[i];
+    float4 a0, a1, b0, b1;
+    load_box(c.x, ilo, ihi, llo, lhi, a0, a1);
+    load_box(c.y, ilo, ihi, llo, lhi, b0, b1);
+    float4* o = nodes + 4ll * i;
+    o[0] = make_float4(a0.x, a1.x, a0.y, a1.y);
+    o[1] = make_float4(b0.x, b1.x, b0.y, b1.y);
+    o[2] = make_float4(a0.z, a1.z, b0.z, b1.z);
+    o[3] = make_float4(__int_as_float(child_ref(c.x, range)), __int_as_float(child_ref(c.y, range)),
+                       0.f, 0.f);
+}
+
+__global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri,
+                           const uint32_t* __restrict__ order, uint32_t n, double2* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t id = order[k];
+    const uint4 t = tri[id];
+    const double* a = vtx + 3ull * t.x;
+    const double* b = vtx + 3ull * t.y;
+    const double* c = vtx + 3ull * t.z;
+    double2* o = out + 5ull * k;
+    o[0] = make_double2(a[0], a[1]);
+    o[1] = make_double2(a[2], b[0] - a[0]);
+    o[2] = make_double2(b[1] - a[1], b[2] - a[2]);
+    o[3] = make_double2(c[0] - a[0], c[1] - a[1]);
+    o[4] = make_double2(c[2] - a[2], __longlong_as_double(static_cast<long long>(id)));
+}
+
+// sorted leaf boxes: lo_s[k] = lo[order[k]]
+__global__ void gather_boxes(const float4* __restrict__ lo, const float4* __restrict__ hi,
+                             const uint32_t* __restrict__ ord, int n, float4* __restrict__ lo_s,
+                             float4* __restrict__ hi_s) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    lo_s[k] = lo[ord[k]];
+    hi_s[k] = hi[ord[k]];
+}
+
+// depth of every Karras leaf (number of inner ancestors), for the stack bound
+__global__ void depth_kernel(int n, const int* __restrict__ parent_inner, const int* __restrict__ parent_leaf,
+                             unsigned int* max_depth) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = 0;
+    for (int p = parent_leaf[i]; p >= 0; p = parent_inner[p]) ++d;
+    atomicMax(max_depth, static_cast<unsigned int>(d));
+}
+
+}  // namespace
+
+#define BVH_CHECK(x)                          \
+    do {                                      \
+        cudaError_t e_ = (x);                 \
+        if (e_ != cudaSuccess) {              \
+            err = e_;                         \
+            goto done;                        \
+        }                                     \
+    } while (0)
+
+cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t n_tri,
+                      const double scene_lo[3], const double scene_hi[3], const double center[3],
+                      double box_pad, cudaStream_t stream, BvhBuildOut* out) {
+    cudaError_t err = cudaSuccess;
+    const int n = static_cast<int>(n_tri);
+    uint64_t *keys = nullptr, *keys_s = nullptr;
+    uint32_t *ids = nullptr, *ids_s = nullptr;
+    float4 *blo = nullptr, *bhi = nullptr, *blo_s = nullptr, *bhi_s = nullptr;
+    float4 *ilo = nullptr, *ihi = nullptr;
+    int2 *child = nullptr, *range = nullptr;
+    int *par_i = nullptr, *par_l = nullptr, *flags = nullptr;
+    unsigned int* dmax = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const int B = 256;
+    const int G = (n + B - 1) / B;
+    const int inner = n > 1 ? n - 1 : 1;
+    double s[3];
+    out->nodes = nullptr;
+    out->tri64 = nullptr;
+    for (int k = 0; k < 3; ++k) {
+        const double ext = scene_hi[k] - scene_lo[k];
+        s[k] = ext > 0.0 ? 2097152.0 / ext : 0.0;
+    }
+    BVH_CHECK(cudaEventCreate(&e0));
+    BVH_CHECK(cudaEventCreate(&e1));
+    BVH_CHECK(cudaEventRecord(e0, stream));
+    BVH_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * n));
+    BVH_CHECK(cudaMalloc(&keys_s, sizeof(uint64_t) * n));
+    BVH_CHECK(cudaMalloc(&ids, sizeof(uint32_t) * n));
+    BVH_CHECK(cudaMalloc(&ids_s, sizeof(uint32_t) * n));
+    BVH_CHECK(cudaMalloc(&blo, sizeof(float4) * n));
+    BVH_CHECK(cudaMalloc(&bhi, sizeof(float4) * n));
+    BVH_CHECK(cudaMalloc(&blo_s, sizeof(float4) * n));
+    BVH_CHECK(cudaMalloc(&bhi_s, sizeof(float4) * n));
+    BVH_CHECK(cudaMalloc(&ilo, sizeof(float4) * inner));
+    BVH_CHECK(cudaMalloc(&ihi, sizeof(float4) * inner));
+    BVH_CHECK(cudaMalloc(&child, sizeof(int2) * inner));
+    BVH_CHECK(cudaMalloc(&range, sizeof(int2) * inner));
+    BVH_CHECK(cudaMalloc(&par_i, sizeof(int) * inner));
+    BVH_CHECK(cudaMalloc(&par_l, sizeof(int) * n));
+    BVH_CHECK(cudaMalloc(&flags, sizeof(int) * inner));
+    BVH_CHECK(cudaMalloc(&dmax, sizeof(unsigned int)));
+    BVH_CHECK(cudaMalloc(&out->nodes, sizeof(float4) * 4 * inner));
+    BVH_CHECK(cudaMalloc(&out->tri64, sizeof(double2) * 5 * n));
+    BVH_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * inner, stream));
+    BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
+    BVH_CHECK(cudaMemsetAsync(par_i, 0xff, sizeof(int) * inner, stream));  // root parent = -1
+    BVH_CHECK(cudaMemsetAsync(par_l, 0xff, sizeof(int) * n, stream));
+
+    prim_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, n_tri, scene_lo[0], scene_lo[1], scene_lo[2],
+                                     s[0], s[1], s[2], center[0], center[1], center[2], box_pad, keys,
+                                     ids, blo, bhi);
+    BVH_CHECK(cudaGetLastError());
+    BVH_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
+                                              stream));
+    BVH_CHECK(cudaMalloc(&tmp, tmp_bytes));
+    BVH_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
+                                              stream));
+    tri_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, ids_s, n_tri, out->tri64);
+    BVH_CHECK(cudaGetLastError());
+    if (n > 1) {
+        gather_boxes<<<G, B, 0, stream>>>(blo, bhi, ids_s, n, blo_s, bhi_s);
+        BVH_CHECK(cudaGetLastError());
+        karras_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(keys_s, n, child, range, par_i, par_l);
+        BVH_CHECK(cudaGetLastError());
+        refit_kernel<<<G, B, 0, stream>>>(n, child, par_i, par_l, blo_s, bhi_s, ilo, ihi, flags);
+        BVH_CHECK(cudaGetLastError());
+        emit_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, ilo, ihi, blo_s, bhi_s,
+                                                           out->nodes);
+        BVH_CHECK(cudaGetLastError());
+        depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
+        BVH_CHECK(cudaGetLastError());
+    }
+    BVH_CHECK(cudaEventRecord(e1, stream));
+    {
+        unsigned int md = 0;
+        BVH_CHECK(cudaMemcpyAsync(&md, dmax, sizeof(md), cudaMemcpyDeviceToHost, stream));
+        BVH_CHECK(cudaStreamSynchronize(stream));
+        out->max_depth = md;
+        out->n_nodes = n > 1 ? static_cast<uint32_t>(n - 1) : 0;
+        out->root_ref = n <= kLeafMax ? ~(0 << 3 | n) : 0;
+        out->n_leaves = n_tri;
+        float ms = 0.f;
+        BVH_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        out->build_ms = ms;
+    }
+done:
+    cudaFree(keys);
+    cudaFree(keys_s);
+    cudaFree(ids);
+    cudaFree(ids_s);
+    cudaFree(blo);
+    cudaFree(bhi);
+    cudaFree(blo_s);
+    cudaFree(bhi_s);
+    cudaFree(ilo);
+    cudaFree(ihi);
+    cudaFree(child);
+    cudaFree(range);
+    cudaFree(par_i);
+    cudaFree(par_l);
+    cudaFree(flags);
+    cudaFree(dmax);
+    cudaFree(tmp);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (err != cudaSuccess) {
+        cudaFree(out->nodes);
+        cudaFree(out->tri64);
+        out->nodes = nullptr;
+        out->tri64 = nullptr;
+    }
+    return err;
+}
+
+}  // namespace mcsbr_int

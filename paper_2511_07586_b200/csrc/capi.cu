@@ -1,0 +1,727 @@
+// Host orchestration + the C ABI (include/mcsbr_gpu.h).
+//
+// Host-side planning is fp64 and restates the reference exactly (this file is
+// compiled with -ffp-contract=off and no -march, like the reference build):
+//   Scene::finalize bounding sphere   proj/src/geometry.cpp:146-162
+//   launch_rect                       proj/src/geometry.cpp:246-275
+//   build_strata                      proj/src/solver_mc.cpp:19-31
+//   McConfig::validate                proj/src/solver_mc.cpp:10-17
+//   SweepAccumulator::finalize        proj/src/farfield.cpp:154-167
+//   RunStats                          proj/include/mcsbr/solver_common.hpp:37-53
+// Everything per ray runs on the GPU (bvh.cu, trace.cu); there is no CPU
+// fallback: without a device every compute entry point returns MCSBR_ECUDA.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "mcsbr_gpu.h"
+
+using namespace mcsbr_int;
+
+namespace {
+
+constexpr double kC = 299792458.0;
+constexpr double kPi = 3.14159265358979323846;
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+    return set_err(MCSBR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x, what)                                  \
+    do {                                             \
+        cudaError_t e_ = (x);                        \
+        if (e_ != cudaSuccess) return cuda_err(e_, what); \
+    } while (0)
+
+struct V {
+    double x, y, z;
+};
+inline V operator+(V a, V b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline V operator-(V a, V b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline V operator*(V a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline double dot(V a, V b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V cross(V a, V b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+inline double norm(V v) { return std::sqrt(dot(v, v)); }
+inline V normalized(V v) {
+    const double n = norm(v);
+    return {v.x / n, v.y / n, v.z / n};
+}
+inline V ld(const double* p) { return {p[0], p[1], p[2]}; }
+inline void st(double* p, V v) {
+    p[0] = v.x;
+    p[1] = v.y;
+    p[2] = v.z;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t reserve(size_t want) {
+        if (want <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(want, 1));
+        if (e == cudaSuccess) n = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct mcsbr_scene {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<double> vtx;
+    uint32_t nv = 0, nt = 0, nm = 0;
+    double center[3] = {0, 0, 0};
+    double radius = 0.0, diameter = 0.0;
+    double ambient_n = 1.0;
+    double* d_vtx = nullptr;
+    uint4* d_tri = nullptr;
+    double2* d_info = nullptr;
+    double2* d_mat = nullptr;
+    BvhBuildOut bvh{};
+    // reusable work buffers
+    DevBuf<IncDev> inc;
+    DevBuf<RxDev> rx;
+    DevBuf<double> k0;
+    DevBuf<double> sums;
+    DevBuf<unsigned long long> counters;
+    DevBuf<unsigned long long> tile;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    SceneView view() const {
+        SceneView s{};
+        s.nodes = bvh.nodes;
+        s.tri64 = bvh.tri64;
+        s.tri_info = d_info;
+        s.mat = d_mat;
+        s.root_ref = bvh.root_ref;
+        s.n_tri = nt;
+        s.diameter = diameter;
+        s.t_eps = 1e-6 * diameter;
+        s.ambient_n = ambient_n;
+        s.center[0] = center[0];
+        s.center[1] = center[1];
+        s.center[2] = center[2];
+        s.skip_radius = radius * 1.01 + 1e-9;
+        return s;
+    }
+};
+
+namespace {
+
+// launch_rect (geometry.cpp:246-275) + build_strata (solver_mc.cpp:19-31)
+int plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw, double lambda_ref,
+         int32_t spp, mcsbr_launch_plan* out) {
+    const V k = normalized(ld(k_inc));
+    V seed{1.0, 0.0, 0.0};
+    if (std::abs(k.x) > 0.9) seed = V{0.0, 1.0, 0.0};
+    const V u = normalized(cross(k, seed));
+    const V v = cross(k, u);
+    double ulo = 1e300, uhi = -1e300, vlo = 1e300, vhi = -1e300;
+    for (uint32_t i = 0; i < s->nv; ++i) {
+        const V p = ld(&s->vtx[3ull * i]);
+        const double pu = dot(p, u);
+        const double pv = dot(p, v);
+        ulo = std::min(ulo, pu);
+        uhi = std::max(uhi, pu);
+        vlo = std::min(vlo, pv);
+        vhi = std::max(vhi, pv);
+    }
+    ulo -= padding;
+    uhi += padding;
+    vlo -= padding;
+    vhi += padding;
+    std::memset(out, 0, sizeof(*out));
+    st(out->u_axis, u);
+    st(out->v_axis, v);
+    out->half_u = 0.5 * (uhi - ulo);
+    out->half_v = 0.5 * (vhi - vlo);
+    const double standoff = dot(ld(s->center), k) - 1.05 * s->radius;
+    st(out->center, u * (0.5 * (ulo + uhi)) + v * (0.5 * (vlo + vhi)) + k * standoff);
+    if (!(lambda_ref > 0.0))
+        return set_err(MCSBR_EINVAL, "build_strata: reference wavelength must be > 0");
+    const double target = lambda_ref / spw;
+    out->nu = std::max(1, static_cast<int>(std::ceil(2.0 * out->half_u / target)));
+    out->nv = std::max(1, static_cast<int>(std::ceil(2.0 * out->half_v / target)));
+    const double area = 4.0 * out->half_u * out->half_v;
+    out->cell_area = area / (static_cast<double>(out->nu) * out->nv);
+    out->entries = static_cast<uint64_t>(out->nu * out->nv) * static_cast<uint64_t>(spp);
+    return MCSBR_OK;
+}
+
+int validate(const mcsbr_mc_config* c) {
+    if (!c) return set_err(MCSBR_EINVAL, "mc: null config");
+    if (!(c->strata_per_wavelength > 0.0)) return set_err(MCSBR_EINVAL, "mc: strata_per_wavelength must be > 0");
+    if (c->samples_per_stratum < 1) return set_err(MCSBR_EINVAL, "mc: samples_per_stratum must be >= 1");
+    if (!(c->roulette_q > 0.0 && c->roulette_q < 1.0)) return set_err(MCSBR_EINVAL, "mc: roulette q must be in (0,1)");
+    if (c->roulette_min_bounce < 1) return set_err(MCSBR_EINVAL, "mc: roulette min_bounce must be >= 1");
+    if (c->max_bounce < 2) return set_err(MCSBR_EINVAL, "mc: max_bounce must be >= 2");
+    if (c->block_size < 1) return set_err(MCSBR_EINVAL, "mc: block_size must be >= 1");
+    if (c->max_bounce > MCSBR_MAX_BOUNCE_LIMIT)
+        return set_err(MCSBR_EINVAL, "mc: max_bounce exceeds MCSBR_MAX_BOUNCE_LIMIT (64)");
+    if (c->rng_mode != MCSBR_RNG_REFERENCE && c->rng_mode != MCSBR_RNG_PHILOX)
+        return set_err(MCSBR_EINVAL, "mc: unknown rng_mode");
+    return MCSBR_OK;
+}
+
+struct Job {
+    std::vector<IncDev> inc;
+    std::vector<RxDev> rx;
+    std::vector<double> k0;
+    uint32_t n_rx = 1;
+    uint64_t total_tiles = 0;
+    uint32_t tile_entries = 0;
+    uint64_t total_entries = 0;
+};
+
+// Plan all incidences of a batch for one shard.
+int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
+             const mcsbr_receiver* rxs, uint32_t n_rx, const double* freqs, uint32_t nf,
+             const mcsbr_mc_config* cfg, uint32_t shard, uint32_t nshard, int warps_hint, Job* job) {
+    int rc = validate(cfg);
+    if (rc) return rc;
+    if (nf == 0 || !freqs) return set_err(MCSBR_EINVAL, "estimate: empty frequency list");
+    if (n_inc == 0) return set_err(MCSBR_EINVAL, "estimate: no incidences");
+    if (n_rx == 0 || !rxs) return set_err(MCSBR_EINVAL, "estimate: no receivers");
+    if (nshard == 0 || shard >= nshard) return set_err(MCSBR_EINVAL, "estimate: bad shard");
+    double lambda_ref = cfg->reference_wavelength;
+    if (lambda_ref <= 0.0) lambda_ref = kC / freqs[nf - 1];
+    job->inc.resize(n_inc);
+    job->rx.resize(static_cast<size_t>(n_inc) * n_rx);
+    job->n_rx = n_rx;
+    job->k0.resize(nf);
+    for (uint32_t f = 0; f < nf; ++f) job->k0[f] = 2.0 * kPi * freqs[f] / kC;
+    uint64_t total = 0;
+    for (uint32_t a = 0; a < n_inc; ++a) {
+        const mcsbr_incidence& in = incs[a];
+        const double spw = in.strata_per_wavelength > 0.0 ? in.strata_per_wavelength : cfg->strata_per_wavelength;
+        mcsbr_launch_plan lp;
+        rc = plan(s, in.k_inc, cfg->launch_padding, spw, lambda_ref, cfg->samples_per_stratum, &lp);
+        if (rc) return rc;
+        if (lp.entries == 0) return set_err(MCSBR_EINVAL, "estimate: empty strata grid");
+        IncDev& d = job->inc[a];
+        std::memset(&d, 0, sizeof(d));
+        std::memcpy(d.center, lp.center, sizeof(d.center));
+        std::memcpy(d.u, lp.u_axis, sizeof(d.u));
+        std::memcpy(d.v, lp.v_axis, sizeof(d.v));
+        d.half_u = lp.half_u;
+        d.half_v = lp.half_v;
+        std::memcpy(d.k_inc, in.k_inc, sizeof(d.k_inc));
+        std::memcpy(d.pol_v, in.pol_v, sizeof(d.pol_v));
+        std::memcpy(d.pol_h, in.pol_h, sizeof(d.pol_h));
+        d.area_weight = lp.cell_area / static_cast<double>(static_cast<uint64_t>(cfg->samples_per_stratum));
+        d.nu = lp.nu;
+        d.nv = lp.nv;
+        d.entry_begin = lp.entries * shard / nshard;
+        d.entry_end = lp.entries * (shard + 1) / nshard;
+        total += d.entry_end - d.entry_begin;
+        for (uint32_t r = 0; r < n_rx; ++r) {
+            RxDev& x = job->rx[static_cast<size_t>(a) * n_rx + r];
+            const mcsbr_receiver& y = rxs[static_cast<size_t>(a) * n_rx + r];
+            std::memcpy(x.k_s, y.k_scatter, sizeof(x.k_s));
+            std::memcpy(x.rx_v, y.rx_v, sizeof(x.rx_v));
+            std::memcpy(x.rx_h, y.rx_h, sizeof(x.rx_h));
+        }
+    }
+    job->total_entries = total;
+    // tile size: enough tiles for ~8 per warp, 64..4096 entries, multiple of 32
+    uint64_t t = total / (static_cast<uint64_t>(std::max(warps_hint, 1)) * 8);
+    t = (t + 31) / 32 * 32;
+    t = std::min<uint64_t>(std::max<uint64_t>(t, 64), 4096);
+    job->tile_entries = static_cast<uint32_t>(t);
+    uint64_t tiles = 0;
+    for (auto& d : job->inc) {
+        d.tile_begin = tiles;
+        tiles += (d.entry_end - d.entry_begin + t - 1) / t;
+    }
+    job->total_tiles = tiles;
+    return MCSBR_OK;
+}
+
+void fill_config(TraceParams& p, const mcsbr_mc_config* cfg) {
+    p.spp = static_cast<uint32_t>(cfg->samples_per_stratum);
+    p.seed = cfg->seed;
+    p.max_bounce = cfg->max_bounce;
+    p.fresnel_strategy = cfg->branch_strategy == MCSBR_BRANCH_FRESNEL;
+    p.p_min = cfg->p_min;
+    p.roulette_enabled = cfg->roulette_enabled != 0;
+    p.roulette_min_bounce = cfg->roulette_min_bounce;
+    p.roulette_q = cfg->roulette_q;
+    p.jitter = cfg->jitter != 0;
+    p.rng_mode = cfg->rng_mode;
+}
+
+// Upload a planned job and run the path kernel(s) on s->stream, adding into
+// d_sums / d_counters.  One launch per receiver index (receivers of one
+// incidence share nothing but the geometry).
+int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* cfg, int occlusion,
+            double* d_sums, unsigned long long* d_counters, cudaStream_t stream, TraceParams* extra,
+            float* kernel_ms) {
+    CK(s->inc.reserve(job.inc.size()), "cudaMalloc(incidences)");
+    CK(s->rx.reserve(job.rx.size()), "cudaMalloc(receivers)");
+    CK(s->k0.reserve(nf), "cudaMalloc(k0)");
+    CK(s->tile.reserve(1), "cudaMalloc(tile counter)");
+    CK(cudaMemcpyAsync(s->inc.p, job.inc.data(), sizeof(IncDev) * job.inc.size(), cudaMemcpyHostToDevice,
+                       stream), "upload incidences");
+    CK(cudaMemcpyAsync(s->rx.p, job.rx.data(), sizeof(RxDev) * job.rx.size(), cudaMemcpyHostToDevice, stream),
+       "upload receivers");
+    CK(cudaMemcpyAsync(s->k0.p, job.k0.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, stream),
+       "upload wavenumbers");
+    TraceParams p = extra ? *extra : TraceParams{};
+    p.scene = s->view();
+    p.inc = s->inc.p;
+    p.n_inc = static_cast<uint32_t>(job.inc.size());
+    p.n_rx = job.n_rx;
+    p.rx = s->rx.p;
+    p.k0 = s->k0.p;
+    p.nf = nf;
+    p.occlusion = occlusion;
+    p.sums = d_sums;
+    p.counters = d_counters;
+    p.tile_counter = s->tile.p;
+    p.total_tiles = job.total_tiles;
+    p.tile_entries = job.tile_entries;
+    fill_config(p, cfg);
+    if (kernel_ms && !s->ev0) {
+        CK(cudaEventCreate(&s->ev0), "cudaEventCreate");
+        CK(cudaEventCreate(&s->ev1), "cudaEventCreate");
+    }
+    if (kernel_ms) CK(cudaEventRecord(s->ev0, stream), "cudaEventRecord");
+    for (uint32_t r = 0; r < job.n_rx; ++r) {
+        p.rx_index = r;
+        CK(cudaMemsetAsync(s->tile.p, 0, sizeof(unsigned long long), stream), "reset tile counter");
+        CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
+    }
+    if (kernel_ms) {
+        CK(cudaEventRecord(s->ev1, stream), "cudaEventRecord");
+        CK(cudaEventSynchronize(s->ev1), "cudaEventSynchronize");
+        CK(cudaEventElapsedTime(kernel_ms, s->ev0, s->ev1), "cudaEventElapsedTime");
+    }
+    return MCSBR_OK;
+}
+
+void decode(const unsigned long long* c, mcsbr_stats* st) {
+    std::memset(st, 0, sizeof(*st));
+    st->rays_launched = c[kCntLaunched];
+    st->contributions = c[kCntContrib];
+    st->grazing_kills = c[kCntGrazing];
+    st->cap_kills = c[kCntCap];
+    st->occlusion_queries = c[kCntOcclusion];
+    uint32_t rounds = 0;
+    uint64_t seg = 0;
+    for (int i = 0; i < MCSBR_MAX_BOUNCE_LIMIT; ++i) {
+        st->rays_per_bounce[i] = c[kCntRaysPerBounce + i];
+        st->roulette_candidates[i] = c[kCntRouletteCand + i];
+        st->roulette_survivors[i] = c[kCntRouletteSurv + i];
+        seg += st->rays_per_bounce[i];
+        if (st->rays_per_bounce[i]) rounds = static_cast<uint32_t>(i + 1);
+    }
+    st->segments_traced = seg;
+    st->n_rounds = rounds;
+    st->state_bytes_per_ray = 208;  // registers of one in-flight path (Path + hit temporaries)
+}
+
+int fault_check(const unsigned long long* c) {
+    const unsigned long long f = c[kCntFault];
+    if (!f) return MCSBR_OK;
+    std::string m = "device fault:";
+    if (f & 1u) m += " fresnel: refractive indices / cos_theta_i out of domain;";
+    if (f & 2u) m += " interface_transform: field is not transverse to dir_in;";
+    if (f & 4u) m += " reflect_dir/refract_dir: grazing incidence;";
+    if (f & 8u) m += " BVH traversal stack overflow;";
+    return set_err(MCSBR_EDEVICE, m);
+}
+
+void finalize_values(const double* raw, uint32_t n, const double* freqs, uint32_t nf, double* values) {
+    for (uint32_t k = 0; k < n; ++k) {
+        for (int ch = 0; ch < 4; ++ch) {
+            for (uint32_t i = 0; i < nf; ++i) {
+                const double k0 = 2.0 * kPi * freqs[i] / kC;
+                const double pre_re = 0.0 * k0 / (2.0 * std::sqrt(kPi));
+                const double pre_im = 1.0 * k0 / (2.0 * std::sqrt(kPi));
+                const double* sv = raw + ((static_cast<size_t>(k) * nf + i) * 4 + ch) * 2;
+                double* o = values + ((static_cast<size_t>(k) * 4 + ch) * nf + i) * 2;
+                o[0] = pre_re * sv[0] - pre_im * sv[1];
+                o[1] = pre_re * sv[1] + pre_im * sv[0];
+            }
+        }
+    }
+}
+
+int use_device(const mcsbr_scene* s) {
+    CK(cudaSetDevice(s->device), "cudaSetDevice");
+    return MCSBR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mcsbr_gpu_last_error(void) { return g_err.c_str(); }
+int mcsbr_gpu_abi_version(void) { return MCSBR_GPU_ABI_VERSION; }
+uint64_t mcsbr_gpu_last_launch_count(void) { return g_launches; }
+
+void mcsbr_gpu_default_config(mcsbr_mc_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->strata_per_wavelength = 10.0;
+    c->samples_per_stratum = 16;
+    c->branch_strategy = MCSBR_BRANCH_FRESNEL;
+    c->roulette_enabled = 0;
+    c->roulette_min_bounce = 2;
+    c->roulette_q = 0.5;
+    c->max_bounce = 9;
+    c->jitter = 1;
+    c->seed = 1;
+    c->reference_wavelength = 0.0;
+    c->launch_padding = 0.0;
+    c->p_min = 0.05;
+    c->block_size = 8192;
+    c->rng_mode = MCSBR_RNG_REFERENCE;
+}
+
+int mcsbr_gpu_validate_config(const mcsbr_mc_config* cfg) { return validate(cfg); }
+
+int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle* tris, uint32_t nt,
+                           const mcsbr_material* mats, uint32_t nm, const double* eps_imag, int device,
+                           mcsbr_scene** out) {
+    if (!out) return set_err(MCSBR_EINVAL, "scene_create: null output");
+    *out = nullptr;
+    if (nt == 0 || !tris) return set_err(MCSBR_ESCENE, "scene has no triangles");
+    if (nm == 0 || !mats) return set_err(MCSBR_ESCENE, "material map: missing 'materials' object");
+    if (nv == 0 || !xyz) return set_err(MCSBR_ESCENE, "scene is degenerate (zero extent)");
+    if (mats[0].is_pec) return set_err(MCSBR_ESCENE, "material map: ambient material cannot be PEC");
+    for (uint32_t i = 0; i < nm; ++i) {
+        if (eps_imag && eps_imag[i] != 0.0)
+            return set_err(MCSBR_EINVAL,
+                           "lossy permittivity (Im eps != 0) is not supported by this build; pass eps_imag = NULL");
+        if (!mats[i].is_pec && (!(mats[i].eps_r > 0.0) || !(mats[i].mu_r > 0.0) ||
+                                !std::isfinite(mats[i].eps_r) || !std::isfinite(mats[i].mu_r)))
+            return set_err(MCSBR_ESCENE, "material: eps_r and mu_r must be positive");
+    }
+    for (uint32_t i = 0; i < nt; ++i) {
+        const mcsbr_triangle& t = tris[i];
+        if (t.v0 >= nv || t.v1 >= nv || t.v2 >= nv)
+            return set_err(MCSBR_ESCENE, "triangle " + std::to_string(i) + ": vertex index out of range");
+        if (t.front_material >= nm || t.back_material >= nm)
+            return set_err(MCSBR_ESCENE, "triangle " + std::to_string(i) + ": material index out of range");
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return set_err(MCSBR_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return set_err(MCSBR_EINVAL, "scene_create: bad device index");
+    CK(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+        return set_err(MCSBR_ECUDA, "this library is built for sm_100a (B200); device is sm_" +
+                                        std::to_string(prop.major) + std::to_string(prop.minor));
+
+    auto* s = new mcsbr_scene();
+    s->device = device;
+    s->sms = prop.multiProcessorCount;
+    s->nv = nv;
+    s->nt = nt;
+    s->nm = nm;
+    s->vtx.assign(xyz, xyz + 3ull * nv);
+    // Scene::finalize (geometry.cpp:146-162)
+    V lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
+    for (uint32_t i = 0; i < nv; ++i) {
+        const V v = ld(xyz + 3ull * i);
+        lo = {std::min(lo.x, v.x), std::min(lo.y, v.y), std::min(lo.z, v.z)};
+        hi = {std::max(hi.x, v.x), std::max(hi.y, v.y), std::max(hi.z, v.z)};
+    }
+    const V c = (lo + hi) * 0.5;
+    double r = 0.0;
+    for (uint32_t i = 0; i < nv; ++i) r = std::max(r, norm(ld(xyz + 3ull * i) - c));
+    st(s->center, c);
+    s->radius = r;
+    s->diameter = 2.0 * r;
+    if (!(s->diameter > 0.0)) {
+        delete s;
+        return set_err(MCSBR_ESCENE, "scene is degenerate (zero extent)");
+    }
+    s->ambient_n = mats[0].is_pec ? 0.0 : std::sqrt(mats[0].eps_r * mats[0].mu_r);
+
+    std::vector<uint4> tri_idx(nt);
+    std::vector<double2> info(2ull * nt);
+    for (uint32_t i = 0; i < nt; ++i) {
+        tri_idx[i] = make_uint4(tris[i].v0, tris[i].v1, tris[i].v2, 0);
+        uint64_t packed = static_cast<uint64_t>(tris[i].front_material) |
+                          (static_cast<uint64_t>(tris[i].back_material) << 16) |
+                          (static_cast<uint64_t>(tris[i].exterior_facing ? 1 : 0) << 32);
+        double pd;
+        std::memcpy(&pd, &packed, sizeof(pd));
+        info[2ull * i] = make_double2(tris[i].normal[0], tris[i].normal[1]);
+        info[2ull * i + 1] = make_double2(tris[i].normal[2], pd);
+    }
+    std::vector<double2> mat(nm);
+    for (uint32_t i = 0; i < nm; ++i)
+        mat[i] = make_double2(mats[i].is_pec ? 0.0 : std::sqrt(mats[i].eps_r * mats[i].mu_r),
+                              mats[i].is_pec ? 1.0 : 0.0);
+
+    auto fail = [&](cudaError_t e2, const char* what) {
+        mcsbr_gpu_scene_destroy(s);
+        return cuda_err(e2, what);
+    };
+    if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate");
+    if ((e = cudaMalloc(&s->d_vtx, sizeof(double) * 3 * nv)) != cudaSuccess) return fail(e, "cudaMalloc(vertices)");
+    if ((e = cudaMalloc(&s->d_tri, sizeof(uint4) * nt)) != cudaSuccess) return fail(e, "cudaMalloc(triangles)");
+    if ((e = cudaMalloc(&s->d_info, sizeof(double2) * 2 * nt)) != cudaSuccess) return fail(e, "cudaMalloc(tri info)");
+    if ((e = cudaMalloc(&s->d_mat, sizeof(double2) * nm)) != cudaSuccess) return fail(e, "cudaMalloc(materials)");
+    if ((e = cudaMemcpyAsync(s->d_vtx, xyz, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice, s->stream)) !=
+        cudaSuccess)
+        return fail(e, "upload vertices");
+    if ((e = cudaMemcpyAsync(s->d_tri, tri_idx.data(), sizeof(uint4) * nt, cudaMemcpyHostToDevice, s->stream)) !=
+        cudaSuccess)
+        return fail(e, "upload triangles");
+    if ((e = cudaMemcpyAsync(s->d_info, info.data(), sizeof(double2) * 2 * nt, cudaMemcpyHostToDevice, s->stream)) !=
+        cudaSuccess)
+        return fail(e, "upload tri info");
+    if ((e = cudaMemcpyAsync(s->d_mat, mat.data(), sizeof(double2) * nm, cudaMemcpyHostToDevice, s->stream)) !=
+        cudaSuccess)
+        return fail(e, "upload materials");
+    const double lo3[3] = {lo.x, lo.y, lo.z}, hi3[3] = {hi.x, hi.y, hi.z};
+    const double box_pad = 1e-5 * r + 1e-30;
+    if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
+        return fail(e, "BVH build");
+    g_launches += 7;
+    if (s->bvh.max_depth + 2 > static_cast<uint32_t>(kStackSize)) {
+        mcsbr_gpu_scene_destroy(s);
+        return set_err(MCSBR_ESCENE, "BVH depth exceeds the traversal stack (64)");
+    }
+    *out = s;
+    return MCSBR_OK;
+}
+
+void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    cudaFree(s->d_vtx);
+    cudaFree(s->d_tri);
+    cudaFree(s->d_info);
+    cudaFree(s->d_mat);
+    cudaFree(s->bvh.nodes);
+    cudaFree(s->bvh.tri64);
+    s->inc.release();
+    s->rx.release();
+    s->k0.release();
+    s->sums.release();
+    s->counters.release();
+    s->tile.release();
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+int mcsbr_gpu_scene_bounds(const mcsbr_scene* s, double center[3], double* radius, double* diameter) {
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    if (center) std::memcpy(center, s->center, sizeof(s->center));
+    if (radius) *radius = s->radius;
+    if (diameter) *diameter = s->diameter;
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_scene_bvh_info(const mcsbr_scene* s, uint32_t* n_nodes, uint32_t* max_depth, uint32_t* n_leaves,
+                             double* build_ms) {
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    if (n_nodes) *n_nodes = s->bvh.n_nodes;
+    if (max_depth) *max_depth = s->bvh.max_depth;
+    if (n_leaves) *n_leaves = s->bvh.n_leaves;
+    if (build_ms) *build_ms = s->bvh.build_ms;
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_launch_plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw,
+                          double lambda_ref, int32_t spp, mcsbr_launch_plan* out) {
+    if (!s || !k_inc || !out) return set_err(MCSBR_EINVAL, "launch_plan: null argument");
+    return plan(s, k_inc, padding, spw, lambda_ref, spp, out);
+}
+
+int mcsbr_gpu_intersect(const mcsbr_scene* s, const double* o, const double* d, const double* tmin, uint32_t n,
+                        int any_hit, double* t_out, uint32_t* id_out) {
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    if (n == 0) return MCSBR_OK;
+    int rc = use_device(s);
+    if (rc) return rc;
+    double *d_o = nullptr, *d_d = nullptr, *d_t = nullptr, *d_to = nullptr;
+    uint32_t* d_id = nullptr;
+    cudaError_t e = cudaSuccess;
+    const size_t v3 = sizeof(double) * 3 * n;
+    if ((e = cudaMalloc(&d_o, v3)) == cudaSuccess && (e = cudaMalloc(&d_d, v3)) == cudaSuccess &&
+        (e = cudaMalloc(&d_t, sizeof(double) * n)) == cudaSuccess &&
+        (e = cudaMalloc(&d_to, sizeof(double) * n)) == cudaSuccess &&
+        (e = cudaMalloc(&d_id, sizeof(uint32_t) * n)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(d_o, o, v3, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(d_d, d, v3, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(d_t, tmin, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
+        (e = launch_intersect(s->view(), d_o, d_d, d_t, n, any_hit, d_to, d_id, s->stream)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(t_out, d_to, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(id_out, d_id, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s->stream)) ==
+            cudaSuccess) {
+        ++g_launches;
+        e = cudaStreamSynchronize(s->stream);
+    }
+    cudaFree(d_o);
+    cudaFree(d_d);
+    cudaFree(d_t);
+    cudaFree(d_to);
+    cudaFree(d_id);
+    if (e != cudaSuccess) return cuda_err(e, "intersect");
+    return MCSBR_OK;
+}
+
+static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs,
+                           uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
+                           const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats,
+                           mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    int rc = use_device(s);
+    if (rc) return rc;
+    Job job;
+    rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, 0, 1, s->sms * 16, &job);
+    if (rc) return rc;
+    const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
+    CK(s->sums.reserve(nsum), "cudaMalloc(sums)");
+    CK(s->counters.reserve(kCntWords), "cudaMalloc(counters)");
+    CK(cudaMemsetAsync(s->sums.p, 0, sizeof(double) * nsum, s->stream), "memset sums");
+    CK(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kCntWords, s->stream), "memset counters");
+    TraceParams extra{};
+    mcsbr_contribution* d_out = nullptr;
+    mcsbr_contribution* d_scratch = nullptr;
+    unsigned long long* d_cnt = nullptr;
+    if (contribs) {
+        if (n_inc != 1 || n_rx != 1) return set_err(MCSBR_EINVAL, "contributions_out needs one incidence");
+        const size_t scratch_n = static_cast<size_t>(s->sms) * 32 * 128;  // >= resident threads
+        CK(cudaMalloc(&d_out, sizeof(mcsbr_contribution) * std::max<uint64_t>(capacity, 1)), "cudaMalloc(contribs)");
+        CK(cudaMalloc(&d_scratch, sizeof(mcsbr_contribution) * scratch_n), "cudaMalloc(scratch)");
+        CK(cudaMalloc(&d_cnt, sizeof(unsigned long long)), "cudaMalloc(count)");
+        CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s->stream), "memset count");
+        extra.contrib_out = d_out;
+        extra.contrib_cap = capacity;
+        extra.contrib_count = d_cnt;
+        extra.contrib_scratch = d_scratch;
+    }
+    float kms = 0.f;
+    rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms);
+    if (rc) {
+        cudaFree(d_out);
+        cudaFree(d_scratch);
+        cudaFree(d_cnt);
+        return rc;
+    }
+    std::vector<double> raw(nsum);
+    unsigned long long cnt[kCntWords];
+    cudaError_t e = cudaMemcpyAsync(raw.data(), s->sums.p, sizeof(double) * nsum, cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(cnt, s->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, s->stream);
+    unsigned long long ncol = 0;
+    if (e == cudaSuccess && contribs)
+        e = cudaMemcpyAsync(&ncol, d_cnt, sizeof(ncol), cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e == cudaSuccess && contribs) {
+        const uint64_t m = std::min<uint64_t>(ncol, capacity);
+        e = cudaMemcpy(contribs, d_out, sizeof(mcsbr_contribution) * m, cudaMemcpyDeviceToHost);
+        std::sort(contribs, contribs + m, [](const mcsbr_contribution& x, const mcsbr_contribution& y) {
+            return x.order_key < y.order_key;
+        });
+        if (n_contribs) *n_contribs = ncol;
+    }
+    cudaFree(d_out);
+    cudaFree(d_scratch);
+    cudaFree(d_cnt);
+    if (e != cudaSuccess) return cuda_err(e, "estimate readback");
+    rc = fault_check(cnt);
+    if (rc) return rc;
+    finalize_values(raw.data(), n_inc * n_rx, freqs, nf, values);
+    if (stats) {
+        decode(cnt, stats);
+        stats->block_size = static_cast<uint64_t>(cfg->block_size);
+        stats->peak_live_state_bytes = static_cast<uint64_t>(s->sms) * 2048 * stats->state_bytes_per_ray;
+        stats->kernel_ms = kms;
+        stats->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_estimate(mcsbr_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+                       const mcsbr_mc_config* cfg, int workers, double* values, mcsbr_stats* stats,
+                       mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+    (void)workers;
+    if (!exc) return set_err(MCSBR_EINVAL, "estimate: null excitation");
+    mcsbr_incidence inc;
+    std::memcpy(inc.k_inc, exc->k_inc, sizeof(inc.k_inc));
+    std::memcpy(inc.pol_v, exc->pol_v, sizeof(inc.pol_v));
+    std::memcpy(inc.pol_h, exc->pol_h, sizeof(inc.pol_h));
+    inc.strata_per_wavelength = 0.0;
+    mcsbr_receiver rx;
+    std::memcpy(rx.k_scatter, exc->k_scatter, sizeof(rx.k_scatter));
+    std::memcpy(rx.rx_v, exc->rx_v, sizeof(rx.rx_v));
+    std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
+    return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, cfg, values, stats, contribs,
+                           capacity, n_contribs);
+}
+
+int mcsbr_gpu_estimate_batch(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
+                             const mcsbr_receiver* rxs, uint32_t n_rx, int occlusion, const double* freqs,
+                             uint32_t nf, const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats) {
+    return estimate_common(s, incs, n_inc, rxs, n_rx, occlusion, freqs, nf, cfg, values, stats, nullptr, 0,
+                           nullptr);
+}
+
+int mcsbr_gpu_trace_device(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs,
+                           uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
+                           const mcsbr_mc_config* cfg, uint32_t shard, uint32_t nshard, double* d_sums,
+                           uint64_t* d_counters, void* stream) {
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    if (!d_sums || !d_counters) return set_err(MCSBR_EINVAL, "trace_device: null device buffer");
+    int rc = use_device(s);
+    if (rc) return rc;
+    Job job;
+    rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, shard, nshard, s->sms * 16, &job);
+    if (rc) return rc;
+    return run_job(s, job, nf, cfg, occlusion, d_sums, reinterpret_cast<unsigned long long*>(d_counters),
+                   static_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+int mcsbr_gpu_finalize(const double* raw, uint32_t n, const double* freqs, uint32_t nf, double* values) {
+    if (!raw || !freqs || !values) return set_err(MCSBR_EINVAL, "finalize: null argument");
+    finalize_values(raw, n, freqs, nf, values);
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_decode_counters(const uint64_t* counters, mcsbr_stats* stats) {
+    if (!counters || !stats) return set_err(MCSBR_EINVAL, "decode_counters: null argument");
+    decode(reinterpret_cast<const unsigned long long*>(counters), stats);
+    return fault_check(reinterpret_cast<const unsigned long long*>(counters));
+}
+
+}  // extern "C"

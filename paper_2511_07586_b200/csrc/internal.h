@@ -1,0 +1,143 @@
+// Internal (non-ABI) structures shared by the host orchestration (capi.cu),
+// the BVH builder (bvh.cu) and the path kernel (trace.cu).
+//
+// Device memory layout of a scene (all arrays 16-byte aligned, SoA-by-record):
+//   nodes      BVH2, 64 B per node = 4 x float4:
+//                [0] (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
+//                [1] (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
+//                [2] (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)
+//                [3] (ref0, ref1, -, -) as int bits; ref >= 0 inner node,
+//                    ref < 0 leaf: ~ref = (first << 3) | count (count <= 4)
+//              child boxes are fp32 in a frame centred on the scene's
+//              bounding sphere, rounded outward from fp64 and padded by
+//              box_pad so the fp32 slab test can only over-accept.
+//   tri64      per leaf-ordered triangle 5 x double2 = 80 B:
+//                (a.x, a.y) (a.z, e1.x) (e1.y, e1.z) (e2.x, e2.y) (e2.z, id)
+//              e1 = b - a, e2 = c - a in fp64: exactly the values the
+//              reference's ray_triangle forms (geometry.cpp:20-39).
+//   tri_info   per original triangle id: 2 x double2 (normal.xyz, packed)
+//              packed = front | back << 16 | exterior << 32 (as uint64 bits)
+//   mat        per material: double2 (index, is_pec)
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace mcsbr_int {
+
+constexpr int kStackSize = 64;
+constexpr int kLeafMax = 4;
+
+struct SceneView {
+    const float4* nodes;
+    const double2* tri64;
+    const double2* tri_info;  // 2 per triangle
+    const double2* mat;
+    int32_t root_ref;
+    uint32_t n_tri;
+    double diameter;
+    double t_eps;      // 1e-6 * diameter (geometry.hpp:78)
+    double ambient_n;  // materials[0].index()
+    double center[3];  // bounding-sphere centre: origin of the fp32 box frame
+    double skip_radius;  // bounding radius + margin (traversal origin advance)
+};
+
+// Per incidence (one launch aperture), host-planned in fp64.
+struct IncDev {
+    double center[3], u[3], v[3];
+    double half_u, half_v;
+    double k_inc[3], pol_v[3], pol_h[3];
+    double area_weight;       // cell_area / spp
+    int32_t nu, nv;
+    uint64_t entry_begin;     // this shard's entry range [begin, end)
+    uint64_t entry_end;
+    uint64_t tile_begin;      // first global tile index of this incidence
+    uint64_t _pad;
+};
+
+struct RxDev {
+    double k_s[3], rx_v[3], rx_h[3];
+};
+
+// counters block (MCSBR_COUNTER_WORDS = 256 uint64)
+enum : int {
+    kCntLaunched = 0,
+    kCntSegments = 1,
+    kCntContrib = 2,
+    kCntGrazing = 3,
+    kCntCap = 4,
+    kCntOcclusion = 5,
+    kCntFault = 6,  // OR of fault bits (stored via atomicOr)
+    kCntRounds = 7, // max bounce index seen (atomicMax)
+    kCntRaysPerBounce = 8,
+    kCntRouletteCand = 72,
+    kCntRouletteSurv = 136,
+    kCntWords = 256,
+};
+
+struct TraceParams {
+    SceneView scene;
+    const IncDev* inc;
+    uint32_t n_inc;
+    uint32_t n_rx;          // receivers per incidence
+    uint32_t rx_index;      // receiver traced by this launch
+    const RxDev* rx;        // [n_inc * n_rx]
+    const double* k0;       // [nf] wavenumbers 2*pi*f/c
+    uint32_t nf;
+    int occlusion;
+    double* sums;           // [n_inc][n_rx][nf][4] complex (re, im)
+    unsigned long long* counters;
+    unsigned long long* tile_counter;
+    uint64_t total_tiles;
+    uint32_t tile_entries;
+    // McConfig
+    uint32_t spp;
+    uint64_t seed;
+    int32_t max_bounce;
+    int32_t fresnel_strategy;
+    double p_min;
+    int32_t roulette_enabled;
+    int32_t roulette_min_bounce;
+    double roulette_q;
+    int32_t jitter;
+    int32_t rng_mode;
+    // debug / parity instrumentation (all optional)
+    void* contrib_out;                       // mcsbr_contribution[contrib_cap]
+    unsigned long long* contrib_count;
+    uint64_t contrib_cap;
+    void* contrib_scratch;                   // one record per resident thread
+    uint32_t* plog_tri;                      // [plog_n][plog_stride] (incidence 0 only)
+    uint8_t* plog_term;
+    unsigned long long* plog_branch;
+    uint64_t plog_n;
+    uint32_t plog_stride;
+};
+
+// bvh.cu
+struct BvhBuildOut {
+    float4* nodes;
+    double2* tri64;
+    uint32_t n_nodes;
+    int32_t root_ref;
+    uint32_t max_depth;
+    uint32_t n_leaves;
+    float build_ms;
+};
+// Builds the BVH on `stream` from device vertices / triangle indices.
+// Returns a cudaError_t; fills *out (device arrays owned by the caller).
+cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t n_tri,
+                      const double scene_lo[3], const double scene_hi[3], const double center[3],
+                      double box_pad,
+                      cudaStream_t stream, BvhBuildOut* out);
+
+// trace.cu
+cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream,
+                         uint64_t* launches);
+cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,
+                             const double* tmin, uint32_t n, int any_hit, double* t_out,
+                             uint32_t* id_out, cudaStream_t stream);
+// general-F / receiver mode selection helper
+bool trace_uses_register_accumulator(const TraceParams& p);
+
+}  // namespace mcsbr_int

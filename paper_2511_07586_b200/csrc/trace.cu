@@ -1,0 +1,660 @@
+// K2/K3/K4: the persistent Monte Carlo SBR path kernel.
+//
+// Replaces the body of mcsbr::estimate (proj/src/solver_mc.cpp:105-210) and
+// its callees.  One thread owns one path at a time; a warp pulls tiles of
+// launch entries (all from one incidence) from a global atomic tile counter
+// and refills lanes as their paths terminate (path regeneration), so the SIMT
+// lanes stay busy even though path lengths differ.  Per lane and event:
+//
+//   closest hit (K2, fp32 conservative BVH2 descent + fp64 Moller-Trumbore in
+//   the reference's arithmetic)  -> advance -> branch_outcomes (GO Fresnel /
+//   PEC transport) -> MECA currents + contribution -> branch choice and
+//   Russian roulette -> occlusion any-hit toward the receiver (K3) -> phasor
+//   accumulation (K4).
+//
+// The wavefront order of the reference (all first hits of a block, then all
+// second hits, ...) only changes the ORDER in which contributions are summed;
+// every path's arithmetic is independent of it, which is why a depth-first
+// per-thread path with a counter-based RNG keyed on (cell, sample, bounce)
+// reproduces the reference's per-path events bit for bit.
+//
+// Accumulation (K4): F = 1 keeps the 4 channel phasor sums of the lane's
+// current incidence in registers and reduces them across the warp (shuffles)
+// once per tile before one fp64 atomicAdd per channel.  F > 1 stages a
+// per-warp [F][4] complex accumulator in shared memory: each visible
+// contribution is broadcast across the warp and lane l evaluates frequencies
+// l, l+32, ... (fp64 phase, sincos) into its own slots, flushed with atomics
+// once per tile.
+#include <cstdio>
+
+#include "dmath.cuh"
+#include "internal.h"
+#include "physics.cuh"
+#include "rng.cuh"
+#include "mcsbr_gpu.h"
+
+using namespace mcsbr_dev;
+
+namespace mcsbr_int {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ V3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
+
+// ---------------------------------------------------------------------------
+// K2/K3: traversal
+
+struct FRay {
+    float ix, iy, iz;     // 1/dir (fp32, zero components clamped)
+    float oix, oiy, oiz;  // origin * inv, origin in the scene-centred frame
+    double t_skip;        // parameter of the traversal origin along the fp64 ray
+};
+
+__device__ __forceinline__ float safe_inv(double d) {
+    const double a = fabs(d) < 1e-12 ? copysign(1e-12, d) : d;
+    return __double2float_rn(1.0 / a);
+}
+
+// The fp32 boxes live in a frame centred on the scene's bounding sphere.  A
+// ray starting outside the sphere is advanced (for the box tests only) to a
+// conservative lower bound of its sphere entry, so every fp32 coordinate the
+// slab test sees is O(scene radius) and the rounding error stays far below
+// the box padding (build: box_pad = 1e-5 R).  The fp64 triangle test always
+// uses the untouched ray, so hits are exactly the reference's.
+__device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d) {
+    FRay r;
+    const V3 c = {S.center[0], S.center[1], S.center[2]};
+    const V3 oc = o - c;
+    const double dd = dot(d, d);
+    const double b = -dot(oc, d);
+    const double skip = (b - S.skip_radius * sqrt(dd)) / dd;
+    r.t_skip = skip > 0.0 ? skip : 0.0;
+    const V3 ot = oc + d * r.t_skip;
+    r.ix = safe_inv(d.x);
+    r.iy = safe_inv(d.y);
+    r.iz = safe_inv(d.z);
+    r.oix = __fmul_rn(__double2float_rn(ot.x), r.ix);
+    r.oiy = __fmul_rn(__double2float_rn(ot.y), r.iy);
+    r.oiz = __fmul_rn(__double2float_rn(ot.z), r.iz);
+    return r;
+}
+
+// slab test of one child box against [0, tmax]; returns entry distance or +inf
+__device__ __forceinline__ float slab(const FRay& r, float lx, float hx, float ly, float hy, float lz,
+                                      float hz, float tmax) {
+    const float x0 = __fmaf_rn(lx, r.ix, -r.oix), x1 = __fmaf_rn(hx, r.ix, -r.oix);
+    const float y0 = __fmaf_rn(ly, r.iy, -r.oiy), y1 = __fmaf_rn(hy, r.iy, -r.oiy);
+    const float z0 = __fmaf_rn(lz, r.iz, -r.oiz), z1 = __fmaf_rn(hz, r.iz, -r.oiz);
+    const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.0f));
+    const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));
+    return tn <= tf ? tn : __int_as_float(0x7f800000);
+}
+
+// Moller-Trumbore in fp64, geometry.cpp:20-39 operation for operation
+// (e1 = b - a and e2 = c - a are stored precomputed: same IEEE values).
+__device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, V3 d, double t_min,
+                                         double& t_out, uint32_t& id_out) {
+    const double2 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r3 = __ldg(rec + 3),
+                  r4 = __ldg(rec + 4);
+    const V3 a = {r0.x, r0.y, r1.x};
+    const V3 e1 = {r1.y, r2.x, r2.y};
+    const V3 e2 = {r3.x, r3.y, r4.x};
+    const V3 p = cross(d, e2);
+    const double det = dot(e1, p);
+    if (fabs(det) < 1e-14) return false;
+    const double inv_det = 1.0 / det;
+    const V3 s = o - a;
+    const double u = dot(s, p) * inv_det;
+    if (u < 0.0 || u > 1.0) return false;
+    const V3 q = cross(s, e1);
+    const double v = dot(d, q) * inv_det;
+    if (v < 0.0 || u + v > 1.0) return false;
+    const double t = dot(e2, q) * inv_det;
+    if (t <= t_min || t >= 1e300) return false;
+    t_out = t;
+    id_out = static_cast<uint32_t>(__double_as_longlong(r4.y));
+    return true;
+}
+
+// Closest hit (kAny = false): Scene::intersect semantics, geometry.cpp:177-216
+// (nearest t > t_min, equal-t ties to the smallest triangle id).
+// Any hit (kAny = true): Scene::occluded semantics, geometry.cpp:242-244.
+template <bool kAny>
+__device__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
+                         uint32_t& best_id, uint32_t& fault) {
+    const FRay r = make_fray(S, o, d);
+    best_t = __longlong_as_double(0x7ff0000000000000ll);
+    best_id = 0xffffffffu;
+    float tmax = __int_as_float(0x7f800000);
+    int stack[kStackSize];
+    int sp = 0;
+    int ref = S.root_ref;
+    for (;;) {
+        if (ref >= 0) {
+            const float4* nd = S.nodes + 4ll * ref;
+            const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+            const float t0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tmax);
+            const float t1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tmax);
+            const int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            const bool h0 = t0 != __int_as_float(0x7f800000), h1 = t1 != __int_as_float(0x7f800000);
+            if (h0 && h1) {
+                const bool first0 = t0 <= t1;
+                ref = first0 ? c0 : c1;
+                if (sp < kStackSize) stack[sp++] = first0 ? c1 : c0;
+                else fault |= kFaultStack;
+                continue;
+            }
+            if (h0 || h1) {
+                ref = h0 ? c0 : c1;
+                continue;
+            }
+        } else {
+            const uint32_t code = static_cast<uint32_t>(~ref);
+            const uint32_t first = code >> 3, count = code & 7u;
+            for (uint32_t k = 0; k < count; ++k) {
+                double t;
+                uint32_t id;
+                if (tri_test(S.tri64 + 5ull * (first + k), o, d, t_min, t, id)) {
+                    if (t < best_t || (t == best_t && id < best_id)) {
+                        best_t = t;
+                        best_id = id;
+                        if (kAny) return true;
+                        tmax = __double2float_ru((t - r.t_skip) * (1.0 + 1e-9));
+                    }
+                }
+            }
+        }
+        if (sp == 0) break;
+        ref = stack[--sp];
+    }
+    return best_id != 0xffffffffu;
+}
+
+// fill_hit (geometry.cpp:164-175)
+struct HitInfo {
+    V3 normal;
+    double n_incident, n_transmit;
+    bool far_side_pec, exterior_facing, near_is_ambient;
+};
+
+__device__ __forceinline__ HitInfo fill_hit(const SceneView& S, uint32_t id, V3 dir) {
+    const double2 ta = __ldg(S.tri_info + 2ull * id), tb = __ldg(S.tri_info + 2ull * id + 1);
+    const uint64_t packed = static_cast<uint64_t>(__double_as_longlong(tb.y));
+    const V3 nrm = {ta.x, ta.y, tb.x};
+    const bool front = dot(dir, nrm) < 0.0;
+    HitInfo h;
+    h.normal = front ? nrm : -nrm;
+    const uint32_t fm = static_cast<uint32_t>(packed & 0xffffu);
+    const uint32_t bm = static_cast<uint32_t>((packed >> 16) & 0xffffu);
+    const uint32_t near_id = front ? fm : bm, far_id = front ? bm : fm;
+    const double2 nm = __ldg(S.mat + near_id), fr = __ldg(S.mat + far_id);
+    const bool near_pec = nm.y != 0.0, far_pec = fr.y != 0.0;
+    h.n_incident = near_pec ? S.ambient_n : nm.x;
+    h.far_side_pec = far_pec || near_pec;
+    h.n_transmit = far_pec ? 0.0 : fr.x;
+    h.exterior_facing = ((packed >> 32) & 1u) != 0;
+    h.near_is_ambient = near_id == 0;
+    return h;
+}
+
+// ---------------------------------------------------------------------------
+// per-path state (PathState, proj/include/mcsbr/path_engine.hpp:16-28)
+
+struct Path {
+    V3 origin, dir;
+    CV3 e0, e1;
+    double phi, prob, weight, medium_n;
+    int bounce;
+    uint32_t cell, sample;
+    uint64_t entry;
+    uint64_t key;  // counter_prefix(seed, cell, sample) or the Philox ray index
+};
+
+__device__ __forceinline__ double draw(const TraceParams& P, const Path& s, uint64_t bounce,
+                                       uint64_t purpose) {
+    if (P.rng_mode == MCSBR_RNG_REFERENCE) return u53(counter_finish(s.key, bounce, purpose));
+    return philox_uniform(P.seed, s.key, static_cast<uint32_t>(bounce), static_cast<uint32_t>(purpose));
+}
+
+// sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
+__device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
+                                          uint64_t entry, Path& s) {
+    const uint32_t cell = static_cast<uint32_t>(entry / P.spp);
+    const uint32_t sample = static_cast<uint32_t>(entry % P.spp);
+    const uint32_t i = cell % static_cast<uint32_t>(I.nu);
+    const uint32_t j = cell / static_cast<uint32_t>(I.nu);
+    double ju = 0.5, jv = 0.5;
+    if (P.rng_mode == MCSBR_RNG_REFERENCE) {
+        s.key = counter_prefix(P.seed, cell, sample);
+        if (P.jitter) {
+            ju = u53(counter_finish(s.key, 0, kLaunchU));
+            jv = u53(counter_finish(s.key, 0, kLaunchV));
+        }
+    } else {
+        s.key = (static_cast<uint64_t>(inc_idx) << 40) | entry;
+        if (P.jitter) {
+            ju = philox_uniform(P.seed, s.key, 0, kLaunchU);
+            jv = philox_uniform(P.seed, s.key, 0, kLaunchV);
+        }
+    }
+    const double su = -1.0 + 2.0 * (static_cast<double>(i) + ju) / I.nu;
+    const double sv = -1.0 + 2.0 * (static_cast<double>(j) + jv) / I.nv;
+    const V3 c = ld3(I.center), u = ld3(I.u), v = ld3(I.v);
+    const V3 p = (c + u * (su * I.half_u)) + v * (sv * I.half_v);
+    const V3 k = ld3(I.k_inc);
+    s.origin = p;
+    s.dir = k;
+    s.e0 = cvreal(ld3(I.pol_v));
+    s.e1 = cvreal(ld3(I.pol_h));
+    s.phi = P.scene.ambient_n * dot(k, p);
+    s.prob = 1.0;
+    s.weight = 1.0;
+    s.medium_n = P.scene.ambient_n;
+    s.bounce = 0;
+    s.cell = cell;
+    s.sample = sample;
+    s.entry = entry;
+}
+
+// receiver projection of one contribution (SweepAccumulator::add, farfield.cpp:106-128)
+__device__ __forceinline__ void project(const RxDev& R, const CV3& aj0, const CV3& am0, const CV3& aj1,
+                                        const CV3& am1, Cx amp[4]) {
+    const V3 ks = ld3(R.k_s), rv = ld3(R.rx_v), rh = ld3(R.rx_h);
+    const CV3 f0 = cross(ks, cross(ks, aj0)) + cross(ks, am0);
+    const CV3 f1 = cross(ks, cross(ks, aj1)) + cross(ks, am1);
+    amp[0] = dot(f0, rv);  // VV
+    amp[3] = dot(f0, rh);  // HV
+    amp[2] = dot(f1, rv);  // VH
+    amp[1] = dot(f1, rh);  // HH
+}
+
+__device__ __forceinline__ void store_cv(double* p, const CV3& v) {
+    p[0] = v.x.re; p[1] = v.x.im; p[2] = v.y.re; p[3] = v.y.im; p[4] = v.z.re; p[5] = v.z.im;
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(kFull, v, src);
+}
+
+// ---------------------------------------------------------------------------
+// the path kernel
+
+template <bool kRegAcc>
+__global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
+    extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
+    __shared__ unsigned long long s_cnt[kCntWords];
+    for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double* wacc = kRegAcc ? nullptr : smem_acc + static_cast<size_t>(warp) * P.nf * 8;
+    if (!kRegAcc) {
+        for (uint32_t i = lane; i < P.nf * 8; i += 32) wacc[i] = 0.0;
+        __syncwarp();
+    }
+    const SceneView& S = P.scene;
+    uint32_t fault = 0;
+    uint64_t n_launched = 0, n_contrib = 0, n_graze = 0, n_cap = 0, n_occ = 0;
+    int max_round = 0;
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    mcsbr_contribution* scratch =
+        P.contrib_scratch ? static_cast<mcsbr_contribution*>(P.contrib_scratch) + gtid : nullptr;
+
+    for (;;) {
+        // ---- fetch a tile (warp-uniform) ----
+        unsigned long long tile = 0;
+        if (lane == 0) tile = atomicAdd(P.tile_counter, 1ull);
+        tile = __shfl_sync(kFull, tile, 0);
+        if (tile >= P.total_tiles) break;
+        // incidence of this tile: last a with tile_begin[a] <= tile
+        uint32_t lo = 0, hi = P.n_inc;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (P.inc[mid].tile_begin <= tile) lo = mid; else hi = mid;
+        }
+        const uint32_t a = lo;
+        const IncDev& I = P.inc[a];
+        const uint64_t e_begin = I.entry_begin + (tile - I.tile_begin) * P.tile_entries;
+        const uint64_t e_end = min(e_begin + P.tile_entries, I.entry_end);
+        const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + P.rx_index];
+        uint64_t cursor = e_begin;  // warp-uniform
+
+        Cx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        bool alive = false;
+        Path s;
+
+        for (;;) {
+            // ---- regenerate dead lanes from the tile ----
+            const unsigned need = __ballot_sync(kFull, !alive);
+            if (need && cursor < e_end) {
+                const unsigned rank = __popc(need & ((1u << lane) - 1u));
+                const uint64_t mine = cursor + rank;
+                if (!alive && mine < e_end) {
+                    init_path(P, I, a, mine, s);
+                    alive = true;
+                    ++n_launched;
+                }
+                cursor = min(cursor + static_cast<uint64_t>(__popc(need)), e_end);
+            }
+            if (!__any_sync(kFull, alive)) break;
+
+            bool candidate = false;
+            Cx amp[4];
+            double s_path = 0.0;
+            if (alive) {
+                // ---- closest hit (solver_mc.cpp:142-144) ----
+                double t;
+                uint32_t id;
+                atomicAdd(&s_cnt[kCntRaysPerBounce + min(s.bounce, 63)], 1ull);
+                const bool hit = traverse<false>(S, s.origin, s.dir, s.bounce == 0 ? 0.0 : S.t_eps, t,
+                                                 id, fault);
+                if (!hit) {
+                    alive = false;  // escaped
+                } else {
+                    const V3 point = s.origin + s.dir * t;
+                    const HitInfo h = fill_hit(S, id, s.dir);
+                    // advance (path_engine.cpp:17-21)
+                    s.phi += s.medium_n * t;
+                    s.origin = point;
+                    s.bounce += 1;
+                    max_round = max(max_round, s.bounce);
+                    const bool logged = P.plog_tri && a == 0 && s.entry < P.plog_n;
+                    if (logged && static_cast<uint32_t>(s.bounce - 1) < P.plog_stride)
+                        P.plog_tri[s.entry * P.plog_stride + (s.bounce - 1)] = id;
+                    // branch_outcomes (path_engine.cpp:23-54)
+                    const double cos_i = -dot(s.dir, h.normal);
+                    if (cos_i < 1e-6) {
+                        ++n_graze;
+                        alive = false;
+                        if (logged) P.plog_term[s.entry] = 1;
+                    } else {
+                        const bool pec = h.far_side_pec;
+                        const double n1 = s.medium_n;
+                        const double n2 = pec ? n1 : h.n_transmit;
+                        const Coeffs co = pec ? coeffs_pec() : fresnel(n1, n2, cos_i, fault);
+                        const Basis b = sp_basis(s.dir, h.normal, n1, n2, !pec, fault);
+                        const CV3 er0 = interface_transform(s.e0, 0, co, b, fault);
+                        const CV3 er1 = interface_transform(s.e1, 0, co, b, fault);
+                        const bool two = !pec && !co.tir;
+                        CV3 et0 = cvzero(), et1 = cvzero();
+                        if (two) {
+                            et0 = interface_transform(s.e0, 1, co, b, fault);
+                            et1 = interface_transform(s.e1, 1, co, b, fault);
+                        }
+                        // scatter case + chi pre-checks (solver_mc.cpp:150-160)
+                        const int sc = pec ? 0 : (h.near_is_ambient ? 1 : 2);
+                        const bool dark_exit = sc == 2 && co.tir;
+                        candidate = !dark_exit && h.exterior_facing;
+                        if (candidate) {
+                            // meca_currents (farfield.cpp:11-45) for both pols
+                            CV3 j0, m0, j1, m1;
+                            if (sc == 0) {
+                                j0 = cross(h.normal, cross(s.dir, s.e0) * s.medium_n) * 2.0;
+                                j1 = cross(h.normal, cross(s.dir, s.e1) * s.medium_n) * 2.0;
+                                m0 = cvzero();
+                                m1 = cvzero();
+                            } else if (sc == 1) {
+                                j0 = cross(h.normal, (cross(s.dir, s.e0) + cross(b.dir_r, er0)) * s.medium_n);
+                                j1 = cross(h.normal, (cross(s.dir, s.e1) + cross(b.dir_r, er1)) * s.medium_n);
+                                m0 = cross(s.e0 + er0, h.normal);
+                                m1 = cross(s.e1 + er1, h.normal);
+                            } else {
+                                const V3 n_out = -h.normal;
+                                j0 = cross(n_out, cross(b.dir_t, et0) * h.n_transmit);
+                                j1 = cross(n_out, cross(b.dir_t, et1) * h.n_transmit);
+                                m0 = cross(et0, n_out);
+                                m1 = cross(et1, n_out);
+                            }
+                            // make_contribution (farfield.cpp:70-85)
+                            const double cos_n = fabs(dot(s.dir, h.normal));
+                            const double scale = s.weight * I.area_weight / (s.prob * cos_n);
+                            j0 = j0 * scale;
+                            m0 = m0 * scale;
+                            j1 = j1 * scale;
+                            m1 = m1 * scale;
+                            project(R, j0, m0, j1, m1, amp);
+                            s_path = s.phi - dot(ld3(R.k_s), point);
+                            if (scratch) {
+                                store_cv(&scratch->a_j[0][0][0], j0);
+                                store_cv(&scratch->a_m[0][0][0], m0);
+                                store_cv(&scratch->a_j[1][0][0], j1);
+                                store_cv(&scratch->a_m[1][0][0], m1);
+                                scratch->phi_total = s.phi;
+                                scratch->exit_point[0] = point.x;
+                                scratch->exit_point[1] = point.y;
+                                scratch->exit_point[2] = point.z;
+                                scratch->bounce = s.bounce;
+                                scratch->_pad = 0;
+                                scratch->order_key =
+                                    ((static_cast<uint64_t>(s.cell) * P.spp + s.sample) << 8) |
+                                    static_cast<uint64_t>(s.bounce & 0xff);
+                            }
+                        }
+                        if (s.bounce >= P.max_bounce) {  // cap (solver_mc.cpp:176-179)
+                            ++n_cap;
+                            alive = false;
+                            if (logged) P.plog_term[s.entry] = 2;
+                        } else {
+                            // choose_branch (solver_mc.cpp:44-54, :181-190)
+                            int pick = 0;
+                            double pp = 1.0;
+                            if (two) {
+                                double p_reflect = 0.5;
+                                if (P.fresnel_strategy) {
+                                    const double r_bar = 0.5 * (cabs(co.r_s) + cabs(co.r_p));
+                                    const double lo_c = (r_bar < P.p_min) ? P.p_min : r_bar;
+                                    const double hi_c = 1.0 - P.p_min;
+                                    p_reflect = (hi_c < lo_c) ? hi_c : lo_c;
+                                }
+                                const double u = draw(P, s, static_cast<uint64_t>(s.bounce), kBranch);
+                                if (u < p_reflect) {
+                                    pp = p_reflect;
+                                } else {
+                                    pick = 1;
+                                    pp = 1.0 - p_reflect;
+                                }
+                            }
+                            if (logged && pick) P.plog_branch[s.entry] |= 1ull << (s.bounce - 1);
+                            if (pick == 0) {
+                                s.dir = b.dir_r;
+                                s.e0 = er0;
+                                s.e1 = er1;
+                                s.medium_n = n1;
+                            } else {
+                                s.dir = b.dir_t;
+                                s.e0 = et0;
+                                s.e1 = et1;
+                                s.medium_n = n2;
+                            }
+                            s.prob *= pp;
+                            // roulette (solver_mc.cpp:56-64, :192-205)
+                            if (P.roulette_enabled && s.bounce >= P.roulette_min_bounce) {
+                                const int bi = min(s.bounce - 1, 63);
+                                atomicAdd(&s_cnt[kCntRouletteCand + bi], 1ull);
+                                const double u = draw(P, s, static_cast<uint64_t>(s.bounce), kRoulette);
+                                if (u > P.roulette_q) {
+                                    s.weight /= (1.0 - P.roulette_q);
+                                    atomicAdd(&s_cnt[kCntRouletteSurv + bi], 1ull);
+                                } else {
+                                    alive = false;
+                                    if (logged) P.plog_term[s.entry] = 3;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+
+            // ---- chi visibility: occlusion toward the receiver (farfield.cpp:63-68) ----
+            bool visible = candidate;
+            if (candidate && P.occlusion) {
+                double t2;
+                uint32_t id2;
+                ++n_occ;
+                // after advance the path origin is the exit point
+                visible = !traverse<true>(S, s.origin, ld3(R.k_s), S.t_eps, t2, id2, fault);
+            }
+            if (visible) {
+                ++n_contrib;
+                if (scratch) {
+                    const unsigned long long slot = atomicAdd(P.contrib_count, 1ull);
+                    if (slot < P.contrib_cap)
+                        static_cast<mcsbr_contribution*>(P.contrib_out)[slot] = *scratch;
+                }
+            }
+            // ---- phasor accumulation (farfield.cpp:130-146) ----
+            if (kRegAcc) {
+                if (visible) {
+                    double sn, cs;
+                    sincos(-P.k0[0] * s_path, &sn, &cs);
+                    const Cx z = {cs, sn};
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) acc[ch] = acc[ch] + amp[ch] * z;
+                }
+            } else {
+                unsigned vm = __ballot_sync(kFull, visible);
+                while (vm) {
+                    const int src = __ffs(vm) - 1;
+                    vm &= vm - 1;
+                    Cx am[4];
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        am[ch].re = shfl_d(amp[ch].re, src);
+                        am[ch].im = shfl_d(amp[ch].im, src);
+                    }
+                    const double sp = shfl_d(s_path, src);
+                    for (uint32_t f = lane; f < P.nf; f += 32) {
+                        double sn, cs;
+                        sincos(-P.k0[f] * sp, &sn, &cs);
+                        const Cx z = {cs, sn};
+                        double* slot = wacc + f * 8;
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            const Cx v = am[ch] * z;
+                            slot[2 * ch] += v.re;
+                            slot[2 * ch + 1] += v.im;
+                        }
+                    }
+                }
+            }
+        }
+
+        // ---- flush the tile's accumulators ----
+        double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
+        if (kRegAcc) {
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                double re = acc[ch].re, im = acc[ch].im;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    re += __shfl_xor_sync(kFull, re, o);
+                    im += __shfl_xor_sync(kFull, im, o);
+                }
+                if (lane == 0) {
+                    atomicAdd(out + 2 * ch, re);
+                    atomicAdd(out + 2 * ch + 1, im);
+                }
+            }
+        } else {
+            __syncwarp();
+            for (uint32_t i = lane; i < P.nf * 8; i += 32) {
+                const double v = wacc[i];
+                if (v != 0.0) atomicAdd(out + i, v);
+                wacc[i] = 0.0;
+            }
+            __syncwarp();
+        }
+    }
+
+    // ---- counters ----
+    auto wsum = [](uint64_t v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        return v;
+    };
+    n_launched = wsum(n_launched);
+    n_contrib = wsum(n_contrib);
+    n_graze = wsum(n_graze);
+    n_cap = wsum(n_cap);
+    n_occ = wsum(n_occ);
+    const unsigned fault_w = __reduce_or_sync(kFull, fault);
+    const int round_w = __reduce_max_sync(kFull, max_round);
+    if (lane == 0) {
+        atomicAdd(&s_cnt[kCntLaunched], n_launched);
+        atomicAdd(&s_cnt[kCntContrib], n_contrib);
+        atomicAdd(&s_cnt[kCntGrazing], n_graze);
+        atomicAdd(&s_cnt[kCntCap], n_cap);
+        atomicAdd(&s_cnt[kCntOcclusion], n_occ);
+        atomicOr(&s_cnt[kCntFault], static_cast<unsigned long long>(fault_w));
+        atomicMax(&s_cnt[kCntRounds], static_cast<unsigned long long>(round_w));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) {
+        const unsigned long long v = s_cnt[i];
+        if (!v) continue;
+        if (i == kCntFault) atomicOr(P.counters + i, v);
+        else if (i == kCntRounds) atomicMax(P.counters + i, v);
+        else atomicAdd(P.counters + i, v);
+    }
+}
+
+__global__ void intersect_kernel(SceneView S, const double* __restrict__ o, const double* __restrict__ d,
+                                 const double* __restrict__ tmin, uint32_t n, int any_hit,
+                                 double* __restrict__ t_out, uint32_t* __restrict__ id_out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const V3 oo = ld3(o + 3ull * i), dd = ld3(d + 3ull * i);
+    double t;
+    uint32_t id, fault = 0;
+    bool hit;
+    if (any_hit) hit = traverse<true>(S, oo, dd, tmin[i], t, id, fault);
+    else hit = traverse<false>(S, oo, dd, tmin[i], t, id, fault);
+    t_out[i] = hit ? t : __longlong_as_double(0x7ff0000000000000ll);
+    id_out[i] = hit ? id : 0xffffffffu;
+}
+
+}  // namespace
+
+bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
+
+cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
+    const int threads = 128;
+    const bool reg = trace_uses_register_accumulator(p);
+    const size_t smem = reg ? 0 : static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double);
+    int per_sm = 1;
+    cudaError_t e;
+    if (reg) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<true>, threads, smem);
+    } else {
+        if (smem > 48 * 1024) {
+            e = cudaFuncSetAttribute(path_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<false>, threads, smem);
+    }
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
+    const uint64_t warps_needed = p.total_tiles;
+    const uint64_t max_blocks = (warps_needed + threads / 32 - 1) / (threads / 32);
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    if (reg) path_kernel<true><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
+    else path_kernel<false><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d, const double* tmin,
+                             uint32_t n, int any_hit, double* t_out, uint32_t* id_out,
+                             cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    intersect_kernel<<<(n + 127) / 128, 128, 0, stream>>>(s, o, d, tmin, n, any_hit, t_out, id_out);
+    return cudaGetLastError();
+}
+
+}  // namespace mcsbr_int
