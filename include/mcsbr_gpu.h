@@ -257,6 +257,17 @@ MCSBR_API int mcsbr_gpu_finalize(const double* raw_sums, uint32_t n, const doubl
 /* Decode a counter block (device layout above, copied to host) into stats. */
 MCSBR_API int mcsbr_gpu_decode_counters(const uint64_t* counters, mcsbr_stats* stats);
 
+/* Parity instrumentation: run mcsbr_gpu_estimate and record, for launch
+ * entries [0, n_paths) of the incidence, the triangle id of every hit
+ * (tri_ids[p*stride + k] for hit k, 0xFFFFFFFF past the end), the
+ * termination reason term[p] (0 escaped, 1 grazing, 2 bounce cap,
+ * 3 roulette) and the branch bits branch_bits[p] (bit k = transmit chosen
+ * after hit k).  Same layout as the oracle's orc_path_log. */
+MCSBR_API int mcsbr_gpu_path_log(mcsbr_scene* scene, const mcsbr_excitation* excitation,
+                                 const double* frequencies, uint32_t n_frequencies,
+                                 const mcsbr_mc_config* config, uint64_t n_paths, uint32_t stride,
+                                 uint32_t* tri_ids, uint8_t* term, uint64_t* branch_bits);
+
 /* Number of kernel launches the last compute call on this thread issued
  * (evidence for the benchmark's gpu_launches key). */
 MCSBR_API uint64_t mcsbr_gpu_last_launch_count(void);

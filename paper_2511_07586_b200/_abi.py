@@ -188,6 +188,11 @@ SIGNATURES = {
     ),
     "mcsbr_gpu_finalize": (C.c_int, [_DP, C.c_uint32, _DP, C.c_uint32, _DP]),
     "mcsbr_gpu_decode_counters": (C.c_int, [_U64P, C.POINTER(Stats)]),
+    "mcsbr_gpu_path_log": (
+        C.c_int,
+        [C.c_void_p, C.POINTER(Excitation), _DP, C.c_uint32, C.POINTER(McConfigC), C.c_uint64,
+         C.c_uint32, _U32P, C.POINTER(C.c_uint8), _U64P],
+    ),
     "mcsbr_gpu_last_launch_count": (C.c_uint64, []),
 }
 

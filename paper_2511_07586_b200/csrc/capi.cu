@@ -597,10 +597,19 @@ int mcsbr_gpu_intersect(const mcsbr_scene* s, const double* o, const double* d, 
     return MCSBR_OK;
 }
 
+struct PathLog {
+    uint64_t n = 0;
+    uint32_t stride = 0;
+    uint32_t* tri = nullptr;
+    uint8_t* term = nullptr;
+    uint64_t* branch = nullptr;
+};
+
 static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs,
                            uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
                            const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats,
-                           mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+                           mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs,
+                           const PathLog* plog = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!s) return set_err(MCSBR_EINVAL, "null scene");
     int rc = use_device(s);
@@ -629,8 +638,36 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         extra.contrib_count = d_cnt;
         extra.contrib_scratch = d_scratch;
     }
+    uint32_t* d_ptri = nullptr;
+    uint8_t* d_pterm = nullptr;
+    unsigned long long* d_pbr = nullptr;
+    if (plog && plog->n) {
+        const size_t nt = plog->n * plog->stride;
+        CK(cudaMalloc(&d_ptri, sizeof(uint32_t) * nt), "cudaMalloc(plog)");
+        CK(cudaMalloc(&d_pterm, plog->n), "cudaMalloc(plog)");
+        CK(cudaMalloc(&d_pbr, sizeof(unsigned long long) * plog->n), "cudaMalloc(plog)");
+        CK(cudaMemsetAsync(d_ptri, 0xff, sizeof(uint32_t) * nt, s->stream), "memset plog");
+        CK(cudaMemsetAsync(d_pterm, 0, plog->n, s->stream), "memset plog");
+        CK(cudaMemsetAsync(d_pbr, 0, sizeof(unsigned long long) * plog->n, s->stream), "memset plog");
+        extra.plog_tri = d_ptri;
+        extra.plog_term = d_pterm;
+        extra.plog_branch = d_pbr;
+        extra.plog_n = plog->n;
+        extra.plog_stride = plog->stride;
+    }
     float kms = 0.f;
     rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms);
+    if (rc == MCSBR_OK && plog && plog->n) {
+        cudaError_t e2 = cudaMemcpy(plog->tri, d_ptri, sizeof(uint32_t) * plog->n * plog->stride,
+                                    cudaMemcpyDeviceToHost);
+        if (e2 == cudaSuccess) e2 = cudaMemcpy(plog->term, d_pterm, plog->n, cudaMemcpyDeviceToHost);
+        if (e2 == cudaSuccess)
+            e2 = cudaMemcpy(plog->branch, d_pbr, sizeof(uint64_t) * plog->n, cudaMemcpyDeviceToHost);
+        if (e2 != cudaSuccess) rc = cuda_err(e2, "path log readback");
+    }
+    cudaFree(d_ptri);
+    cudaFree(d_pterm);
+    cudaFree(d_pbr);
     if (rc) {
         cudaFree(d_out);
         cudaFree(d_scratch);
@@ -688,6 +725,30 @@ int mcsbr_gpu_estimate(mcsbr_scene* s, const mcsbr_excitation* exc, const double
     std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
     return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, cfg, values, stats, contribs,
                            capacity, n_contribs);
+}
+
+int mcsbr_gpu_path_log(mcsbr_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+                       const mcsbr_mc_config* cfg, uint64_t n_paths, uint32_t stride, uint32_t* tri_ids,
+                       uint8_t* term, uint64_t* branch_bits) {
+    if (!exc || !tri_ids || !term || !branch_bits) return set_err(MCSBR_EINVAL, "path_log: null argument");
+    mcsbr_incidence inc;
+    std::memcpy(inc.k_inc, exc->k_inc, sizeof(inc.k_inc));
+    std::memcpy(inc.pol_v, exc->pol_v, sizeof(inc.pol_v));
+    std::memcpy(inc.pol_h, exc->pol_h, sizeof(inc.pol_h));
+    inc.strata_per_wavelength = 0.0;
+    mcsbr_receiver rx;
+    std::memcpy(rx.k_scatter, exc->k_scatter, sizeof(rx.k_scatter));
+    std::memcpy(rx.rx_v, exc->rx_v, sizeof(rx.rx_v));
+    std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
+    std::vector<double> values(static_cast<size_t>(nf) * 8);
+    PathLog pl;
+    pl.n = n_paths;
+    pl.stride = stride;
+    pl.tri = tri_ids;
+    pl.term = term;
+    pl.branch = branch_bits;
+    return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, cfg, values.data(), nullptr,
+                           nullptr, 0, nullptr, &pl);
 }
 
 int mcsbr_gpu_estimate_batch(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,

@@ -407,6 +407,23 @@ def estimate(scene: Scene, excitation: Excitation, frequencies, config: McConfig
     return McResult(sweep=sweep, stats=stats)
 
 
+def path_log(scene: Scene, excitation: Excitation, frequencies, config: McConfig, n_paths: int,
+             stride: int | None = None):
+    """Per-path event log of the first n_paths launch entries (parity instrumentation):
+    (tri_ids [n, stride] uint32, termination [n] uint8, branch bits [n] uint64)."""
+    stride = int(stride or config.max_bounce)
+    freqs = np.ascontiguousarray(np.asarray(frequencies, dtype=np.float64).reshape(-1))
+    tri = np.zeros((n_paths, stride), dtype=np.uint32)
+    term = np.zeros(n_paths, dtype=np.uint8)
+    br = np.zeros(n_paths, dtype=np.uint64)
+    cfg = config.to_c()
+    _raise(A.lib().mcsbr_gpu_path_log(
+        scene.handle, C.byref(excitation.to_c()), freqs.ctypes.data_as(C.POINTER(C.c_double)),
+        len(freqs), C.byref(cfg), n_paths, stride, tri.ctypes.data_as(C.POINTER(C.c_uint32)),
+        term.ctypes.data_as(C.POINTER(C.c_uint8)), br.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return tri, term, br
+
+
 def estimate_batch(scene: Scene, incidences: list, receivers: list, frequencies,
                    config: McConfig, occlusion_enabled: bool = True):
     """Many incidences (e.g. an azimuth sweep) in ONE device launch.

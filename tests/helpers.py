@@ -1,0 +1,61 @@
+"""Shared builders for the parity tests (scenes, configs, oracle runs)."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import paper_2511_07586_b200 as M
+from paper_2511_07586_b200 import _abi as A
+
+
+def c_config(cfg: M.McConfig) -> A.McConfigC:
+    return cfg.to_c()
+
+
+def oracle_estimate(sd, exc: M.Excitation, freqs, cfg: M.McConfig, contributions=True,
+                    capacity=1 << 21):
+    """Run the C restatement (pinned to the reference) on the same inputs."""
+    ps = oracle.port_scene(sd)
+    return oracle.port_estimate(ps, exc.to_c(), np.asarray(freqs, dtype=np.float64), cfg.to_c(),
+                                contributions, capacity)
+
+
+def sort_contribs(c):
+    return c[np.argsort(c["order_key"], kind="stable")]
+
+
+# (name, scene builder, excitation, frequencies, McConfig) parity cases: PEC,
+# dielectric (Fresnel + 50/50), roulette, TIR-rich nested media, bistatic,
+# multi-frequency, centre sampling.  Sizes keep the oracle at ~0.1 s.
+def parity_cases():
+    cases = []
+    sph = M.make_builtin_scene("sphere", {"subdivisions": 3})
+    cases.append(("sphere_pec", sph, M.monostatic_excitation(0.0, 0.0), [3e9],
+                  M.McConfig(strata_per_wavelength=8, samples_per_stratum=2, max_bounce=8)))
+    cases.append(("sphere_oblique_multif", sph, M.monostatic_excitation(37.0, 21.0),
+                  np.linspace(2e9, 3e9, 7), M.McConfig(strata_per_wavelength=8, samples_per_stratum=1)))
+    glass = M.make_builtin_scene("glass_cube", {"eps_r": 2.25, "size_m": 1.0})
+    cases.append(("glass_fresnel_roulette", glass, M.monostatic_excitation(20.0, 40.0),
+                  np.linspace(1e9, 3e9, 5),
+                  M.McConfig(strata_per_wavelength=6, samples_per_stratum=2, seed=99,
+                             roulette=M.RouletteConfig(enabled=True))))
+    cases.append(("glass_fifty_fifty", glass, M.monostatic_excitation(0.0, 0.0), [1e9, 1.3e9, 2.9e9],
+                  M.McConfig(strata_per_wavelength=6, samples_per_stratum=2,
+                             branch_strategy=M.BranchStrategy.FIFTY_FIFTY, seed=7)))
+    nested = M.make_builtin_scene("nested", {"subdivisions": 2})
+    cases.append(("nested_tir_roulette", nested, M.monostatic_excitation(10.0, 5.0), [3e9],
+                  M.McConfig(strata_per_wavelength=3, samples_per_stratum=1, seed=3, max_bounce=16,
+                             roulette=M.RouletteConfig(enabled=True, min_bounce=3))))
+    dih = M.make_builtin_scene("dihedral", {})
+    cases.append(("dihedral_bistatic_centre", dih, M.bistatic_excitation(45.0, 0.0, 60.0, 10.0), [3e9],
+                  M.McConfig(strata_per_wavelength=6, samples_per_stratum=1, jitter=False)))
+    obj, mm = M.dihedral_grid(0.5, 16)
+    grid = M.load_scene(obj, mm)
+    cases.append(("dihedral_grid_vv", grid, M.monostatic_excitation(90.0, 45.0 + 17.0), [10e9],
+                  M.McConfig(strata_per_wavelength=8, samples_per_stratum=1, max_bounce=4, seed=2)))
+    obj, mm = M.coated_sphere(subdivisions=2, lossless=True)
+    coat = M.load_scene(obj, mm)
+    cases.append(("coated_sphere_lossless", coat, M.bistatic_excitation(90.0, 0.0, 60.0, 0.0), [3e9],
+                  M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, seed=3, max_bounce=16,
+                             roulette=M.RouletteConfig(enabled=True, min_bounce=3))))
+    return cases
