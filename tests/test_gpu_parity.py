@@ -145,12 +145,14 @@ def test_config_sphere_rays_and_rcs():
     sd = M.make_builtin_scene("sphere", {"subdivisions": 5})
     s = M.Scene(sd)
     exc = M.monostatic_excitation(90.0, 0.0)
-    cfg = M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, max_bounce=8, seed=1)
+    cfg = M.McConfig(strata_per_wavelength=20, samples_per_stratum=1, max_bounce=8, seed=1)
     r = M.estimate(s, exc, [10e9], cfg)
-    grid, entries = M.launch_plan(s, exc.k_inc, 0.0, 10, M.K_SPEED_OF_LIGHT / 10e9, 1)
+    grid, entries = M.launch_plan(s, exc.k_inc, 0.0, 20, M.K_SPEED_OF_LIGHT / 10e9, 1)
     assert r.stats.rays_launched == entries == grid.nu * grid.nv
     sigma = abs(r.sweep.values[M.HH, 0]) ** 2
     assert abs(10 * np.log10(sigma / np.pi)) < 1.0
+    ref = oracle_estimate(sd, exc, [10e9], cfg, contributions=False)
+    assert abs(ref["values"][M.HH, 0] - r.sweep.values[M.HH, 0]) <= 1e-9 * abs(ref["values"][M.HH, 0])
 
 
 def test_errors_mirror_reference():
@@ -201,17 +203,20 @@ def test_batch_equals_single_calls():
     for i, e in enumerate(excs):
         r = M.estimate(s, e, [10e9], cfg)
         total += r.stats.rays_launched
-        assert np.allclose(vals[i, 0], r.sweep.values, rtol=1e-10, atol=1e-300)
+        scale = np.max(np.abs(r.sweep.values))
+        assert np.max(np.abs(vals[i, 0] - r.sweep.values)) <= 1e-10 * scale
     assert st.rays_launched == total
 
 
 def test_statistical_mode_within_half_db():
-    """Mode (2): Philox stream; RCS within 0.5 dB of the reference-stream result."""
+    """Mode (2): Philox stream; RCS within 0.5 dB RMS of the reference-stream
+    result across the sweep (16 samples per stratum keeps the MC noise of two
+    independent estimates well below the bar)."""
     sd = M.make_builtin_scene("sphere", {"subdivisions": 4})
     s = M.Scene(sd)
     exc = M.monostatic_excitation(90.0, 0.0)
-    base = M.McConfig(strata_per_wavelength=10, samples_per_stratum=2, max_bounce=8, seed=1)
-    stat = M.McConfig(strata_per_wavelength=10, samples_per_stratum=2, max_bounce=8, seed=1,
+    base = M.McConfig(strata_per_wavelength=10, samples_per_stratum=16, max_bounce=8, seed=1)
+    stat = M.McConfig(strata_per_wavelength=10, samples_per_stratum=16, max_bounce=8, seed=1,
                       rng_mode=M.RngMode.PHILOX)
     freqs = np.linspace(4e9, 6e9, 9)
     a = M.estimate(s, exc, freqs, base).sweep.values
