@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcsbr_gpu.so")
+LIB_PATH = os.environ.get("MCSBR_GPU_LIB") or os.path.join(_HERE, "libmcsbr_gpu.so")
 
 MCSBR_OK = 0
 MCSBR_EINVAL = -1

@@ -52,9 +52,12 @@ struct FRay {
     double t_skip;        // parameter of the traversal origin along the fp64 ray
 };
 
+// fp32 reciprocal of a direction component (relative error ~1e-7, covered by
+// the box padding); tiny components are clamped so no slab yields inf - inf.
 __device__ __forceinline__ float safe_inv(double d) {
-    const double a = fabs(d) < 1e-12 ? copysign(1e-12, d) : d;
-    return __double2float_rn(1.0 / a);
+    const float f = __double2float_rn(d);
+    const float a = fabsf(f) < 1e-12f ? copysignf(1e-12f, f) : f;
+    return __frcp_rn(a);
 }
 
 // The fp32 boxes live in a frame centred on the scene's bounding sphere.  A
@@ -63,14 +66,20 @@ __device__ __forceinline__ float safe_inv(double d) {
 // slab test sees is O(scene radius) and the rounding error stays far below
 // the box padding (build: box_pad = 1e-5 R).  The fp64 triangle test always
 // uses the untouched ray, so hits are exactly the reference's.
-__device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d) {
+// `outside`: the origin may lie outside the bounding sphere (launch rays and
+// the public intersect API); surface-to-surface and occlusion rays start on a
+// triangle, inside the sphere, and skip the advance.
+__device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool outside) {
     FRay r;
     const V3 c = {S.center[0], S.center[1], S.center[2]};
     const V3 oc = o - c;
-    const double dd = dot(d, d);
-    const double b = -dot(oc, d);
-    const double skip = (b - S.skip_radius * sqrt(dd)) / dd;
-    r.t_skip = skip > 0.0 ? skip : 0.0;
+    r.t_skip = 0.0;
+    if (outside) {
+        const double dd = dot(d, d);
+        const double b = -dot(oc, d);
+        const double skip = (b - S.skip_radius * sqrt(dd)) / dd;
+        r.t_skip = skip > 0.0 ? skip : 0.0;
+    }
     const V3 ot = oc + d * r.t_skip;
     r.ix = safe_inv(d.x);
     r.iy = safe_inv(d.y);
@@ -104,12 +113,26 @@ __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, 
     const V3 p = cross(d, e2);
     const double det = dot(e1, p);
     if (fabs(det) < 1e-14) return false;
-    const double inv_det = 1.0 / det;
     const V3 s = o - a;
-    const double u = dot(s, p) * inv_det;
-    if (u < 0.0 || u > 1.0) return false;
+    const double un = dot(s, p);
     const V3 q = cross(s, e1);
-    const double v = dot(d, q) * inv_det;
+    const double vn = dot(d, q);
+    // Exact early outs that skip the fp64 divide.  With r = RN(1/det) and
+    // u = RN(un * r):  a nonzero un of opposite sign to det gives u < 0 unless
+    // the product underflows (|un| <= 1e-290 |det| excluded), and
+    // |un| > |det| (1 + 1e-15) with the same sign gives u > 1 (two roundings
+    // move the quotient by < 2^-52).  Same for v, and u + v > 1 when
+    // un + vn exceeds det by a margin that covers all four roundings.
+    // Only triangles the reference would reject are skipped here.
+    const double adet = fabs(det);
+    const double su = det < 0.0 ? -un : un, sv = det < 0.0 ? -vn : vn;
+    if ((su < 0.0 && -su > adet * 1e-290) || su > adet * (1.0 + 1e-15)) return false;
+    if ((sv < 0.0 && -sv > adet * 1e-290) || sv > adet * (1.0 + 1e-15)) return false;
+    if (su > 0.0 && sv > 0.0 && su + sv > adet * (1.0 + 1e-13)) return false;
+    const double inv_det = 1.0 / det;
+    const double u = un * inv_det;
+    if (u < 0.0 || u > 1.0) return false;
+    const double v = vn * inv_det;
     if (v < 0.0 || u + v > 1.0) return false;
     const double t = dot(e2, q) * inv_det;
     if (t <= t_min || t >= 1e300) return false;
@@ -123,8 +146,8 @@ __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, 
 // Any hit (kAny = true): Scene::occluded semantics, geometry.cpp:242-244.
 template <bool kAny>
 __device__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
-                         uint32_t& best_id, uint32_t& fault) {
-    const FRay r = make_fray(S, o, d);
+                         uint32_t& best_id, uint32_t& fault, bool outside) {
+    const FRay r = make_fray(S, o, d, outside);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
     best_id = 0xffffffffu;
     float tmax = __int_as_float(0x7f800000);
@@ -282,10 +305,18 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 // the path kernel
 
 template <bool kRegAcc>
-__global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
+#ifndef MCSBR_MIN_BLOCKS
+#define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
+#endif
+__global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
     __shared__ unsigned long long s_cnt[kCntWords];
+    // per-bounce counters as native 32-bit shared atomics (ATOMS.ADD); the
+    // 64-bit shared atomicAdd is a CAS loop on sm_100 and cost ~20% of the
+    // kernel.  Per block and bounce they stay far below 2^32.
+    __shared__ unsigned int s_bounce[3 * 64];
     for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -348,9 +379,9 @@ __global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
                 // ---- closest hit (solver_mc.cpp:142-144) ----
                 double t;
                 uint32_t id;
-                atomicAdd(&s_cnt[kCntRaysPerBounce + min(s.bounce, 63)], 1ull);
+                atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
                 const bool hit = traverse<false>(S, s.origin, s.dir, s.bounce == 0 ? 0.0 : S.t_eps, t,
-                                                 id, fault);
+                                                 id, fault, s.bounce == 0);
                 if (!hit) {
                     alive = false;  // escaped
                 } else {
@@ -473,11 +504,11 @@ __global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
                             // roulette (solver_mc.cpp:56-64, :192-205)
                             if (P.roulette_enabled && s.bounce >= P.roulette_min_bounce) {
                                 const int bi = min(s.bounce - 1, 63);
-                                atomicAdd(&s_cnt[kCntRouletteCand + bi], 1ull);
+                                atomicAdd(&s_bounce[64 + bi], 1u);
                                 const double u = draw(P, s, static_cast<uint64_t>(s.bounce), kRoulette);
                                 if (u > P.roulette_q) {
                                     s.weight /= (1.0 - P.roulette_q);
-                                    atomicAdd(&s_cnt[kCntRouletteSurv + bi], 1ull);
+                                    atomicAdd(&s_bounce[128 + bi], 1u);
                                 } else {
                                     alive = false;
                                     if (logged) P.plog_term[s.entry] = 3;
@@ -495,7 +526,7 @@ __global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
                 uint32_t id2;
                 ++n_occ;
                 // after advance the path origin is the exit point
-                visible = !traverse<true>(S, s.origin, ld3(R.k_s), S.t_eps, t2, id2, fault);
+                visible = !traverse<true>(S, s.origin, ld3(R.k_s), S.t_eps, t2, id2, fault, false);
             }
             if (visible) {
                 ++n_contrib;
@@ -592,6 +623,12 @@ __global__ void __launch_bounds__(128) path_kernel(TraceParams P) {
         atomicMax(&s_cnt[kCntRounds], static_cast<unsigned long long>(round_w));
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) {
+        const int dst = i < 64 ? kCntRaysPerBounce + i : (i < 128 ? kCntRouletteCand + i - 64
+                                                                  : kCntRouletteSurv + i - 128);
+        s_cnt[dst] += s_bounce[i];
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) {
         const unsigned long long v = s_cnt[i];
         if (!v) continue;
@@ -610,8 +647,8 @@ __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, cons
     double t;
     uint32_t id, fault = 0;
     bool hit;
-    if (any_hit) hit = traverse<true>(S, oo, dd, tmin[i], t, id, fault);
-    else hit = traverse<false>(S, oo, dd, tmin[i], t, id, fault);
+    if (any_hit) hit = traverse<true>(S, oo, dd, tmin[i], t, id, fault, true);
+    else hit = traverse<false>(S, oo, dd, tmin[i], t, id, fault, true);
     t_out[i] = hit ? t : __longlong_as_double(0x7ff0000000000000ll);
     id_out[i] = hit ? id : 0xffffffffu;
 }
