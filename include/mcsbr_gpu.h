@@ -210,6 +210,13 @@ MCSBR_API int mcsbr_gpu_intersect(const mcsbr_scene* scene, const double* origin
                         const double* t_min, uint32_t n, int any_hit, double* t_out,
                         uint32_t* id_out);
 
+/* Device-pointer variant of mcsbr_gpu_intersect (no copies, no sync), on
+ * `stream` (cudaStream_t): d_origins / d_dirs n*3 doubles, d_t_min n doubles,
+ * outputs d_t / d_ids. */
+MCSBR_API int mcsbr_gpu_intersect_device(const mcsbr_scene* scene, const double* d_origins,
+                                         const double* d_dirs, const double* d_t_min, uint32_t n,
+                                         int any_hit, double* d_t, uint32_t* d_ids, void* stream);
+
 /* The drop-in: one Excitation, host buffers in and out.  values receives
  * [4][nf] complex (interleaved) sqrt(m^2) values, channel order VV,HH,VH,HV,
  * finalized with j*k0/(2 sqrt(pi)) as SweepAccumulator::finalize does

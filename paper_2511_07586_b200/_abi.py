@@ -170,6 +170,10 @@ SIGNATURES = {
     "mcsbr_gpu_intersect": (
         C.c_int, [C.c_void_p, _DP, _DP, _DP, C.c_uint32, C.c_int, _DP, _U32P],
     ),
+    "mcsbr_gpu_intersect_device": (
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
+                  C.c_void_p, C.c_void_p],
+    ),
     "mcsbr_gpu_estimate": (
         C.c_int,
         [C.c_void_p, C.POINTER(Excitation), _DP, C.c_uint32, C.POINTER(McConfigC), C.c_int, _DP,

@@ -7,7 +7,9 @@
 //   3. karras_kernel    Karras (HPG 2012) binary radix tree over the sorted codes
 //                       (ties broken by sort position), one thread per inner node.
 //   4. refit_kernel     bottom-up AABB union with one atomic flag per inner node.
-//   5. emit_kernel      64-B two-child nodes; any child subtree holding <= 4
+//   5. parity/scan/emit4  collapse to a 4-wide BVH: every inner node at even
+//                       depth becomes a 128-B node holding its grandchildren's
+//                       boxes (SoA by axis); any subtree holding <= 4
 //                       triangles becomes a leaf reference to its contiguous
 //                       sorted range (the LBVH ranges are contiguous).
 //   6. tri_kernel       leaf-ordered fp64 triangle records (a, e1, e2, id).
@@ -17,6 +19,7 @@
 // reference's arithmetic, so closest hits equal brute force
 // (Scene::intersect_brute_force, geometry.cpp:218-240) for ANY tree shape.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <cstdio>
 
@@ -176,12 +179,14 @@ __global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restri
     const double* a = vtx + 3ull * t.x;
     const double* b = vtx + 3ull * t.y;
     const double* c = vtx + 3ull * t.z;
+    const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
+    const double e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
     double2* o = out + 5ull * k;
     o[0] = make_double2(a[0], a[1]);
-    o[1] = make_double2(a[2], b[0] - a[0]);
-    o[2] = make_double2(b[1] - a[1], b[2] - a[2]);
-    o[3] = make_double2(c[0] - a[0], c[1] - a[1]);
-    o[4] = make_double2(c[2] - a[2], __longlong_as_double(static_cast<long long>(id)));
+    o[1] = make_double2(a[2], e1x);
+    o[2] = make_double2(e1y, e1z);
+    o[3] = make_double2(e2x, e2y);
+    o[4] = make_double2(e2z, __longlong_as_double(static_cast<long long>(id)));
 }
 
 // sorted leaf boxes: lo_s[k] = lo[order[k]]
@@ -192,6 +197,89 @@ __global__ void gather_boxes(const float4* __restrict__ lo, const float4* __rest
     if (k >= n) return;
     lo_s[k] = lo[ord[k]];
     hi_s[k] = hi[ord[k]];
+}
+
+// ---- collapse to a 4-wide BVH --------------------------------------------
+// "Effective" inner nodes are those with more than kLeafMax triangles (smaller
+// subtrees are referenced as leaves).  Every effective inner node at even
+// depth becomes a BVH4 node whose (up to 4) slots are its grandchildren; the
+// odd-depth nodes are absorbed.  A ray then needs half the dependent node
+// fetches and tests 4 independent boxes per fetch.
+__device__ __forceinline__ int range_count(const int2* __restrict__ range, int c) {
+    const int2 r = range[c];
+    return r.y - r.x + 1;
+}
+
+__global__ void parity_kernel(int n, const int2* __restrict__ range, const int* __restrict__ parent_inner,
+                              unsigned int* __restrict__ is4) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    unsigned int flag = 0;
+    if (range_count(range, i) > kLeafMax) {
+        int d = 0;
+        for (int p = parent_inner[i]; p >= 0; p = parent_inner[p]) ++d;
+        flag = (d & 1) == 0;
+    }
+    is4[i] = flag;
+}
+
+__device__ __forceinline__ void slot_of(int c, const int2* __restrict__ range, const float4* __restrict__ ilo,
+                                        const float4* __restrict__ ihi, const float4* __restrict__ llo,
+                                        const float4* __restrict__ lhi, const unsigned int* __restrict__ idx4,
+                                        int& ref, float4& lo, float4& hi) {
+    if (c < 0) {
+        ref = ~((~c) << 3 | 1);
+        lo = llo[~c];
+        hi = lhi[~c];
+        return;
+    }
+    lo = ilo[c];
+    hi = ihi[c];
+    const int2 r = range[c];
+    const int cnt = r.y - r.x + 1;
+    ref = cnt <= kLeafMax ? ~(r.x << 3 | cnt) : static_cast<int>(idx4[c]);
+}
+
+__global__ void emit4_kernel(int n, const int2* __restrict__ child, const int2* __restrict__ range,
+                             const unsigned int* __restrict__ is4, const unsigned int* __restrict__ idx4,
+                             const float4* __restrict__ ilo, const float4* __restrict__ ihi,
+                             const float4* __restrict__ llo, const float4* __restrict__ lhi,
+                             float4* __restrict__ nodes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1 || !is4[i]) return;
+    int cnt = 0;
+    int ref[4] = {0, 0, 0, 0};
+    float4 lo[4], hi[4];
+    const int2 ch = child[i];
+    const int kids[2] = {ch.x, ch.y};
+    for (int k = 0; k < 2; ++k) {
+        const int c = kids[k];
+        if (c >= 0 && range_count(range, c) > kLeafMax) {  // absorbed odd-depth node
+            const int2 g = child[c];
+            slot_of(g.x, range, ilo, ihi, llo, lhi, idx4, ref[cnt], lo[cnt], hi[cnt]);
+            ++cnt;
+            slot_of(g.y, range, ilo, ihi, llo, lhi, idx4, ref[cnt], lo[cnt], hi[cnt]);
+            ++cnt;
+        } else {
+            slot_of(c, range, ilo, ihi, llo, lhi, idx4, ref[cnt], lo[cnt], hi[cnt]);
+            ++cnt;
+        }
+    }
+    for (int k = cnt; k < 4; ++k) {  // unused slots: masked by the count in [7]
+        ref[k] = 0;
+        lo[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        hi[k] = lo[k];
+    }
+    float4* o = nodes + 8ll * idx4[i];
+    o[0] = make_float4(lo[0].x, lo[1].x, lo[2].x, lo[3].x);
+    o[1] = make_float4(hi[0].x, hi[1].x, hi[2].x, hi[3].x);
+    o[2] = make_float4(lo[0].y, lo[1].y, lo[2].y, lo[3].y);
+    o[3] = make_float4(hi[0].y, hi[1].y, hi[2].y, hi[3].y);
+    o[4] = make_float4(lo[0].z, lo[1].z, lo[2].z, lo[3].z);
+    o[5] = make_float4(hi[0].z, hi[1].z, hi[2].z, hi[3].z);
+    o[6] = make_float4(__int_as_float(ref[0]), __int_as_float(ref[1]), __int_as_float(ref[2]),
+                       __int_as_float(ref[3]));
+    o[7] = make_float4(__int_as_float(cnt), 0.f, 0.f, 0.f);
 }
 
 // depth of every Karras leaf (number of inner ancestors), for the stack bound
@@ -227,8 +315,10 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     int2 *child = nullptr, *range = nullptr;
     int *par_i = nullptr, *par_l = nullptr, *flags = nullptr;
     unsigned int* dmax = nullptr;
+    unsigned int *is4 = nullptr, *idx4 = nullptr;
     void* tmp = nullptr;
-    size_t tmp_bytes = 0;
+    void* scan_tmp = nullptr;
+    size_t tmp_bytes = 0, scan_bytes = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const int B = 256;
     const int G = (n + B - 1) / B;
@@ -259,7 +349,9 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     BVH_CHECK(cudaMalloc(&par_l, sizeof(int) * n));
     BVH_CHECK(cudaMalloc(&flags, sizeof(int) * inner));
     BVH_CHECK(cudaMalloc(&dmax, sizeof(unsigned int)));
-    BVH_CHECK(cudaMalloc(&out->nodes, sizeof(float4) * 4 * inner));
+    BVH_CHECK(cudaMalloc(&is4, sizeof(unsigned int) * inner));
+    BVH_CHECK(cudaMalloc(&idx4, sizeof(unsigned int) * inner));
+    BVH_CHECK(cudaMalloc(&out->nodes, sizeof(float4) * 8 * inner));
     BVH_CHECK(cudaMalloc(&out->tri64, sizeof(double2) * 5 * n));
     BVH_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * inner, stream));
     BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
@@ -284,19 +376,30 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         BVH_CHECK(cudaGetLastError());
         refit_kernel<<<G, B, 0, stream>>>(n, child, par_i, par_l, blo_s, bhi_s, ilo, ihi, flags);
         BVH_CHECK(cudaGetLastError());
-        emit_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, ilo, ihi, blo_s, bhi_s,
-                                                           out->nodes);
+        parity_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, range, par_i, is4);
+        BVH_CHECK(cudaGetLastError());
+        BVH_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, is4, idx4, n - 1, stream));
+        BVH_CHECK(cudaMalloc(&scan_tmp, scan_bytes));
+        BVH_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, is4, idx4, n - 1, stream));
+        emit4_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, is4, idx4, ilo, ihi, blo_s,
+                                                            bhi_s, out->nodes);
         BVH_CHECK(cudaGetLastError());
         depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
         BVH_CHECK(cudaGetLastError());
     }
     BVH_CHECK(cudaEventRecord(e1, stream));
     {
-        unsigned int md = 0;
+        unsigned int md = 0, last[2] = {0, 0};
         BVH_CHECK(cudaMemcpyAsync(&md, dmax, sizeof(md), cudaMemcpyDeviceToHost, stream));
+        if (n > 1) {
+            BVH_CHECK(cudaMemcpyAsync(&last[0], idx4 + (n - 2), sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                                      stream));
+            BVH_CHECK(cudaMemcpyAsync(&last[1], is4 + (n - 2), sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                                      stream));
+        }
         BVH_CHECK(cudaStreamSynchronize(stream));
         out->max_depth = md;
-        out->n_nodes = n > 1 ? static_cast<uint32_t>(n - 1) : 0;
+        out->n_nodes = last[0] + last[1];
         out->root_ref = n <= kLeafMax ? ~(0 << 3 | n) : 0;
         out->n_leaves = n_tri;
         float ms = 0.f;
@@ -320,7 +423,10 @@ done:
     cudaFree(par_l);
     cudaFree(flags);
     cudaFree(dmax);
+    cudaFree(is4);
+    cudaFree(idx4);
     cudaFree(tmp);
+    cudaFree(scan_tmp);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (err != cudaSuccess) {

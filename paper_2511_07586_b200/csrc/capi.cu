@@ -510,9 +510,10 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
         return fail(e, "BVH build");
     g_launches += 7;
-    if (s->bvh.max_depth + 2 > static_cast<uint32_t>(kStackSize)) {
+    // a 4-wide level pushes at most 3 refs; BVH4 depth <= ceil(binary depth / 2) + 1
+    if (3 * ((s->bvh.max_depth + 1) / 2 + 1) > static_cast<uint32_t>(kStackSize)) {
         mcsbr_gpu_scene_destroy(s);
-        return set_err(MCSBR_ESCENE, "BVH depth exceeds the traversal stack (64)");
+        return set_err(MCSBR_ESCENE, "BVH depth exceeds the traversal stack (96)");
     }
     *out = s;
     return MCSBR_OK;
@@ -604,6 +605,17 @@ struct PathLog {
     uint8_t* term = nullptr;
     uint64_t* branch = nullptr;
 };
+
+int mcsbr_gpu_intersect_device(const mcsbr_scene* s, const double* d_o, const double* d_d, const double* d_tmin,
+                               uint32_t n, int any_hit, double* d_t, uint32_t* d_id, void* stream) {
+    if (!s) return set_err(MCSBR_EINVAL, "null scene");
+    int rc = use_device(s);
+    if (rc) return rc;
+    CK(launch_intersect(s->view(), d_o, d_d, d_tmin, n, any_hit, d_t, d_id, static_cast<cudaStream_t>(stream)),
+       "intersect kernel");
+    ++g_launches;
+    return MCSBR_OK;
+}
 
 static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs,
                            uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,

@@ -26,7 +26,7 @@
 
 namespace mcsbr_int {
 
-constexpr int kStackSize = 64;
+constexpr int kStackSize = 96;  // >= 3 pushes per 4-wide level
 constexpr int kLeafMax = 4;
 
 struct SceneView {

@@ -126,8 +126,11 @@ __device__ inline Basis sp_basis(V3 dir_in, V3 normal, double n1, double n2, boo
 // branch: 0 = reflect, 1 = transmit
 __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs& co,
                                           const Basis& b, uint32_t& fault) {
+    // Transversality guard (the reference throws DomainError).  Only the fault
+    // flag depends on it, so it is evaluated on squares: |x|^2 > (1e-9 (1+|e|))^2.
     const V3 dir_in = cross(b.s_hat, b.p_in);
-    if (cabs(dot(e, dir_in)) > 1e-9 * (1.0 + norm(e))) fault |= kFaultTransverse;
+    const double lim = 1e-9 * (1.0 + norm(e));
+    if (cnorm2(dot(e, dir_in)) > lim * lim) fault |= kFaultTransverse;
     const Cx es = dot(e, b.s_hat);
     const Cx ep = dot(e, b.p_in);
     if (branch == 0) return cvreal(b.s_hat) * (es * co.r_s) + cvreal(b.p_out_r) * (ep * co.r_p);

@@ -49,7 +49,7 @@ __device__ __forceinline__ V3 ld3(const double* p) { return {p[0], p[1], p[2]}; 
 struct FRay {
     float ix, iy, iz;     // 1/dir (fp32, zero components clamped)
     float oix, oiy, oiz;  // origin * inv, origin in the scene-centred frame
-    double t_skip;        // parameter of the traversal origin along the fp64 ray
+    double t_skip;       // parameter of the traversal origin along the fp64 ray
 };
 
 // fp32 reciprocal of a direction component (relative error ~1e-7, covered by
@@ -101,7 +101,10 @@ __device__ __forceinline__ float slab(const FRay& r, float lx, float hx, float l
     return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
-// Moller-Trumbore in fp64, geometry.cpp:20-39 operation for operation
+// Moller-Trumbore in fp64, geometry.cpp:20-39 operation for operation.
+// (Measured and rejected: an error-bounded conservative fp32 pre-filter in
+// front of this test made the c2 sweep 13% slower; the fp64 pipe is not the
+// limiter, dependent latency and register pressure are.)
 // (e1 = b - a and e2 = c - a are stored precomputed: same IEEE values).
 __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, V3 d, double t_min,
                                          double& t_out, uint32_t& id_out) {
@@ -144,9 +147,10 @@ __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, 
 // Closest hit (kAny = false): Scene::intersect semantics, geometry.cpp:177-216
 // (nearest t > t_min, equal-t ties to the smallest triangle id).
 // Any hit (kAny = true): Scene::occluded semantics, geometry.cpp:242-244.
-template <bool kAny>
-__device__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
-                         uint32_t& best_id, uint32_t& fault, bool outside) {
+// One runtime-flagged routine (not two template copies) so the path kernel
+// has a single traversal loop in its instruction stream.
+__device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
+                                         uint32_t& best_id, uint32_t& fault, bool kAny, bool outside) {
     const FRay r = make_fray(S, o, d, outside);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
     best_id = 0xffffffffu;
@@ -156,21 +160,40 @@ __device__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& b
     int ref = S.root_ref;
     for (;;) {
         if (ref >= 0) {
-            const float4* nd = S.nodes + 4ll * ref;
-            const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
-            const float t0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tmax);
-            const float t1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tmax);
-            const int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-            const bool h0 = t0 != __int_as_float(0x7f800000), h1 = t1 != __int_as_float(0x7f800000);
-            if (h0 && h1) {
-                const bool first0 = t0 <= t1;
-                ref = first0 ? c0 : c1;
-                if (sp < kStackSize) stack[sp++] = first0 ? c1 : c0;
-                else fault |= kFaultStack;
-                continue;
-            }
-            if (h0 || h1) {
-                ref = h0 ? c0 : c1;
+            // 4-wide node: 128 B, boxes SoA by axis (bvh.cu emit4_kernel)
+            const float4* nd = S.nodes + 8ll * ref;
+            const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
+            const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5), rf = __ldg(nd + 6), nc = __ldg(nd + 7);
+            const int cnt = __float_as_int(nc.x);
+            const float inf = __int_as_float(0x7f800000);
+            float t0 = slab(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tmax);
+            float t1 = slab(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmax);
+            float t2 = cnt > 2 ? slab(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmax) : inf;
+            float t3 = cnt > 3 ? slab(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmax) : inf;
+            int c0 = __float_as_int(rf.x), c1 = __float_as_int(rf.y), c2 = __float_as_int(rf.z),
+                c3 = __float_as_int(rf.w);
+            // sort the 4 (entry, child) pairs: network (0,1)(2,3)(0,2)(1,3)(1,2)
+#define MCSBR_CSWAP(ta, ca, tb, cb)          \
+    if (tb < ta) {                           \
+        const float tt = ta; ta = tb; tb = tt; \
+        const int cc = ca; ca = cb; cb = cc;   \
+    }
+            MCSBR_CSWAP(t0, c0, t1, c1)
+            MCSBR_CSWAP(t2, c2, t3, c3)
+            MCSBR_CSWAP(t0, c0, t2, c2)
+            MCSBR_CSWAP(t1, c1, t3, c3)
+            MCSBR_CSWAP(t1, c1, t2, c2)
+#undef MCSBR_CSWAP
+            if (t0 != inf) {
+                // visit the nearest now, push the others far-to-near
+                if (sp + 3 > kStackSize) {
+                    fault |= kFaultStack;
+                } else {
+                    if (t3 != inf) stack[sp++] = c3;
+                    if (t2 != inf) stack[sp++] = c2;
+                    if (t1 != inf) stack[sp++] = c1;
+                }
+                ref = c0;
                 continue;
             }
         } else {
@@ -354,9 +377,17 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         uint64_t cursor = e_begin;  // warp-uniform
 
         Cx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-        bool alive = false;
+        bool alive = false;  // lane holds a path (possibly only its last occlusion query)
+        bool pend = false;   // next query is the chi occlusion test of a contribution
+        bool dying = false;  // the path ends once its pending occlusion test is done
         Path s;
+        Cx amp[4];           // pending contribution: receiver-projected amplitudes
+        double s_path = 0.0; //                       and net optical path
 
+        // One query per lane per iteration: either the path's next closest
+        // hit or the occlusion test of the contribution its last hit made.
+        // Lanes in both phases traverse together, so no lane idles while
+        // others run occlusion rays, and the traversal loop appears once.
         for (;;) {
             // ---- regenerate dead lanes from the tile ----
             const unsigned need = __ballot_sync(kFull, !alive);
@@ -372,16 +403,28 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             }
             if (!__any_sync(kFull, alive)) break;
 
-            bool candidate = false;
-            Cx amp[4];
-            double s_path = 0.0;
+            double t = 0.0;
+            uint32_t id = 0;
+            bool hit = false;
             if (alive) {
-                // ---- closest hit (solver_mc.cpp:142-144) ----
-                double t;
-                uint32_t id;
-                atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
-                const bool hit = traverse<false>(S, s.origin, s.dir, s.bounce == 0 ? 0.0 : S.t_eps, t,
-                                                 id, fault, s.bounce == 0);
+                if (pend) ++n_occ;
+                else atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
+                // closest hit: solver_mc.cpp:142-144; occlusion: farfield.cpp:63-68 /
+                // geometry.cpp:242-244 from the exit point (= origin after advance)
+                hit = traverse(S, s.origin, pend ? ld3(R.k_s) : s.dir,
+                               (pend || s.bounce != 0) ? S.t_eps : 0.0, t, id, fault, pend,
+                               !pend && s.bounce == 0);
+            }
+            bool visible = false;
+            if (alive && pend) {
+                pend = false;
+                visible = !hit;
+                if (dying) {
+                    alive = false;
+                    dying = false;
+                }
+            } else if (alive) {
+                bool candidate = false;
                 if (!hit) {
                     alive = false;  // escaped
                 } else {
@@ -517,16 +560,18 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         }
                     }
                 }
-            }
-
-            // ---- chi visibility: occlusion toward the receiver (farfield.cpp:63-68) ----
-            bool visible = candidate;
-            if (candidate && P.occlusion) {
-                double t2;
-                uint32_t id2;
-                ++n_occ;
-                // after advance the path origin is the exit point
-                visible = !traverse<true>(S, s.origin, ld3(R.k_s), S.t_eps, t2, id2, fault, false);
+                // ---- chi visibility (farfield.cpp:63-68): queue the occlusion query ----
+                if (candidate) {
+                    if (P.occlusion) {
+                        pend = true;
+                        if (!alive) {
+                            alive = true;
+                            dying = true;
+                        }
+                    } else {
+                        visible = true;
+                    }
+                }
             }
             if (visible) {
                 ++n_contrib;
@@ -647,8 +692,7 @@ __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, cons
     double t;
     uint32_t id, fault = 0;
     bool hit;
-    if (any_hit) hit = traverse<true>(S, oo, dd, tmin[i], t, id, fault, true);
-    else hit = traverse<false>(S, oo, dd, tmin[i], t, id, fault, true);
+    hit = traverse(S, oo, dd, tmin[i], t, id, fault, any_hit != 0, true);
     t_out[i] = hit ? t : __longlong_as_double(0x7ff0000000000000ll);
     id_out[i] = hit ? id : 0xffffffffu;
 }
