@@ -310,7 +310,14 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         CK(cudaEventCreate(&s->ev1), "cudaEventCreate");
     }
     if (kernel_ms) CK(cudaEventRecord(s->ev0, stream), "cudaEventRecord");
-    for (uint32_t r = 0; r < job.n_rx; ++r) {
+    // Bistatic fans (several receivers per incidence, one frequency): trace
+    // once per chunk of 32 receivers (fan mode).  Otherwise one launch per
+    // receiver index (multi-frequency bistatic sweeps re-trace per receiver,
+    // as the reference does).
+    const bool fan = job.n_rx > 1 && trace_fan_supported(nf);
+    const uint32_t step = fan ? 32u : 1u;
+    p.fan = fan ? 1 : 0;
+    for (uint32_t r = 0; r < job.n_rx; r += step) {
         p.rx_index = r;
         CK(cudaMemsetAsync(s->tile.p, 0, sizeof(unsigned long long), stream), "reset tile counter");
         CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");

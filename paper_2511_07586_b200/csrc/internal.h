@@ -81,7 +81,8 @@ struct TraceParams {
     const IncDev* inc;
     uint32_t n_inc;
     uint32_t n_rx;          // receivers per incidence
-    uint32_t rx_index;      // receiver traced by this launch
+    uint32_t rx_index;      // receiver traced by this launch (fan: the first of up to 32)
+    int fan;                // bistatic fan mode (nf == 1)
     const RxDev* rx;        // [n_inc * n_rx]
     const double* k0;       // [nf] wavenumbers 2*pi*f/c
     uint32_t nf;
@@ -137,7 +138,8 @@ cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stre
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,
                              const double* tmin, uint32_t n, int any_hit, double* t_out,
                              uint32_t* id_out, cudaStream_t stream);
-// general-F / receiver mode selection helper
+// general-F / receiver mode selection helpers
 bool trace_uses_register_accumulator(const TraceParams& p);
+bool trace_fan_supported(uint32_t nf);
 
 }  // namespace mcsbr_int

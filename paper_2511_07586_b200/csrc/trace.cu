@@ -327,11 +327,23 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 // ---------------------------------------------------------------------------
 // the path kernel
 
-template <bool kRegAcc>
+// Accumulation modes:
+//   kModeSmem  one receiver, F > 1: per-warp [F][4] shared-memory phasor sums
+//   kModeReg   one receiver, F = 1: per-lane register sums, warp-reduced per tile
+//   kModeFan   a bistatic fan of up to 32 receivers per launch (P.rx_index is
+//              the first), F = 1: lane l owns receiver rx_index + l; every
+//              contribution is broadcast across the warp and each lane runs
+//              its receiver's occlusion test and projection (a coherent
+//              32-ray bundle from one exit point), so paths are traced once
+//              per 32 receivers instead of once per receiver.
+enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
+
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
+template <int kMode>
 __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
+    constexpr bool kRegAcc = kMode != kModeSmem;
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
     __shared__ unsigned long long s_cnt[kCntWords];
     // per-bounce counters as native 32-bit shared atomics (ATOMS.ADD); the
@@ -373,7 +385,10 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         const IncDev& I = P.inc[a];
         const uint64_t e_begin = I.entry_begin + (tile - I.tile_begin) * P.tile_entries;
         const uint64_t e_end = min(e_begin + P.tile_entries, I.entry_end);
-        const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + P.rx_index];
+        // fan mode: lane l evaluates receiver rx_index + l (if it exists)
+        const uint32_t my_rx = P.rx_index + (kMode == kModeFan ? static_cast<uint32_t>(lane) : 0u);
+        const bool has_rx = my_rx < P.n_rx;
+        const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + (has_rx ? my_rx : P.rx_index)];
         uint64_t cursor = e_begin;  // warp-uniform
 
         Cx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
@@ -383,6 +398,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         Path s;
         Cx amp[4];           // pending contribution: receiver-projected amplitudes
         double s_path = 0.0; //                       and net optical path
+        CV3 fj0, fm0, fj1, fm1;  // fan mode: the contribution's currents,
+        double fphi = 0.0;       // optical path
+        V3 fpt = {0.0, 0.0, 0.0};  // and exit point, broadcast to the warp
 
         // One query per lane per iteration: either the path's next closest
         // hit or the occlusion test of the contribution its last hit made.
@@ -416,6 +434,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                                !pend && s.bounce == 0);
             }
             bool visible = false;
+            bool fan = false;
             if (alive && pend) {
                 pend = false;
                 visible = !hit;
@@ -489,8 +508,17 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                             m0 = m0 * scale;
                             j1 = j1 * scale;
                             m1 = m1 * scale;
-                            project(R, j0, m0, j1, m1, amp);
-                            s_path = s.phi - dot(ld3(R.k_s), point);
+                            if (kMode == kModeFan) {
+                                fj0 = j0;
+                                fm0 = m0;
+                                fj1 = j1;
+                                fm1 = m1;
+                                fphi = s.phi;
+                                fpt = point;
+                            } else {
+                                project(R, j0, m0, j1, m1, amp);
+                                s_path = s.phi - dot(ld3(R.k_s), point);
+                            }
                             if (scratch) {
                                 store_cv(&scratch->a_j[0][0][0], j0);
                                 store_cv(&scratch->a_m[0][0][0], m0);
@@ -561,7 +589,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                     }
                 }
                 // ---- chi visibility (farfield.cpp:63-68): queue the occlusion query ----
-                if (candidate) {
+                if (candidate && kMode == kModeFan) {
+                    fan = true;  // evaluated below by the whole warp
+                } else if (candidate) {
                     if (P.occlusion) {
                         pend = true;
                         if (!alive) {
@@ -581,8 +611,47 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         static_cast<mcsbr_contribution*>(P.contrib_out)[slot] = *scratch;
                 }
             }
-            // ---- phasor accumulation (farfield.cpp:130-146) ----
-            if (kRegAcc) {
+            // ---- bistatic fan: every contribution against this launch's receivers ----
+            if (kMode == kModeFan) {
+                unsigned fm = __ballot_sync(kFull, fan);
+                const V3 ks = ld3(R.k_s);
+                while (fm) {
+                    const int src = __ffs(fm) - 1;
+                    fm &= fm - 1;
+                    CV3 c[4] = {fj0, fm0, fj1, fm1};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        c[k].x.re = shfl_d(c[k].x.re, src);
+                        c[k].x.im = shfl_d(c[k].x.im, src);
+                        c[k].y.re = shfl_d(c[k].y.re, src);
+                        c[k].y.im = shfl_d(c[k].y.im, src);
+                        c[k].z.re = shfl_d(c[k].z.re, src);
+                        c[k].z.im = shfl_d(c[k].z.im, src);
+                    }
+                    const double ph = shfl_d(fphi, src);
+                    const V3 pt = {shfl_d(fpt.x, src), shfl_d(fpt.y, src), shfl_d(fpt.z, src)};
+                    if (has_rx) {
+                        bool vis = true;
+                        if (P.occlusion) {
+                            double t2;
+                            uint32_t id2;
+                            ++n_occ;
+                            vis = !traverse(S, pt, ks, S.t_eps, t2, id2, fault, true, false);
+                        }
+                        if (vis) {
+                            ++n_contrib;
+                            Cx am[4];
+                            project(R, c[0], c[1], c[2], c[3], am);
+                            double sn, cs;
+                            sincos(-P.k0[0] * (ph - dot(ks, pt)), &sn, &cs);
+                            const Cx z = {cs, sn};
+#pragma unroll
+                            for (int ch = 0; ch < 4; ++ch) acc[ch] = acc[ch] + am[ch] * z;
+                        }
+                    }
+                }
+            } else if (kRegAcc) {
+                // ---- phasor accumulation (farfield.cpp:130-146) ----
                 if (visible) {
                     double sn, cs;
                     sincos(-P.k0[0] * s_path, &sn, &cs);
@@ -620,7 +689,16 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
 
         // ---- flush the tile's accumulators ----
         double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
-        if (kRegAcc) {
+        if (kMode == kModeFan) {
+            if (has_rx) {  // lane-owned receiver: nf == 1, no warp reduction
+                double* o = P.sums + (static_cast<size_t>(a) * P.n_rx + my_rx) * 8;
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    if (acc[ch].re != 0.0) atomicAdd(o + 2 * ch, acc[ch].re);
+                    if (acc[ch].im != 0.0) atomicAdd(o + 2 * ch + 1, acc[ch].im);
+                }
+            }
+        } else if (kRegAcc) {
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
                 double re = acc[ch].re, im = acc[ch].im;
@@ -701,22 +779,26 @@ __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, cons
 
 bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
 
+bool trace_fan_supported(uint32_t nf) { return nf == 1; }
+
+template <int kMode>
+static cudaError_t occupancy(int* per_sm, int threads, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(path_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, path_kernel<kMode>, threads, smem);
+}
+
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
-    const bool reg = trace_uses_register_accumulator(p);
-    const size_t smem = reg ? 0 : static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double);
+    const int mode = p.fan ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
+    const size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
     int per_sm = 1;
-    cudaError_t e;
-    if (reg) {
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<true>, threads, smem);
-    } else {
-        if (smem > 48 * 1024) {
-            e = cudaFuncSetAttribute(path_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-        }
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<false>, threads, smem);
-    }
+    cudaError_t e = mode == kModeFan   ? occupancy<kModeFan>(&per_sm, threads, smem)
+                    : mode == kModeReg ? occupancy<kModeReg>(&per_sm, threads, smem)
+                                       : occupancy<kModeSmem>(&per_sm, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
@@ -724,8 +806,10 @@ cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stre
     const uint64_t max_blocks = (warps_needed + threads / 32 - 1) / (threads / 32);
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    if (reg) path_kernel<true><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
-    else path_kernel<false><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
+    const unsigned g = static_cast<unsigned>(blocks);
+    if (mode == kModeFan) path_kernel<kModeFan><<<g, threads, smem, stream>>>(p);
+    else if (mode == kModeReg) path_kernel<kModeReg><<<g, threads, smem, stream>>>(p);
+    else path_kernel<kModeSmem><<<g, threads, smem, stream>>>(p);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
