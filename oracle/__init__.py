@@ -122,8 +122,25 @@ def port() -> C.CDLL:
                                    C.POINTER(A.McConfigC), C.c_uint64, C.c_uint64,
                                    C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_uint8),
                                    C.POINTER(C.c_uint64)]
+        L.orc_estimate_range.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
+                                         C.POINTER(A.McConfigC), C.c_uint64, C.c_uint64, _DP,
+                                         C.POINTER(A.Stats), C.POINTER(C.c_uint64)]
         _port = L
     return _port
+
+
+def port_estimate_range(scene_h, exc, freqs, cfg, entry_begin, entry_end):
+    """Raw [nf][4] complex sums over launch entries [entry_begin, entry_end)."""
+    L = port()
+    freqs = np.ascontiguousarray(freqs, dtype=np.float64)
+    raw = np.zeros((len(freqs), 4, 2), dtype=np.float64)
+    st = A.Stats()
+    total = C.c_uint64(0)
+    rc = L.orc_estimate_range(scene_h.h, C.byref(exc), dp(freqs), len(freqs), C.byref(cfg),
+                              entry_begin, entry_end, dp(raw), C.byref(st), C.byref(total))
+    if rc != 0:
+        raise RuntimeError(L.orc_last_error().decode())
+    return raw, st, total.value
 
 
 def dp(a: np.ndarray):

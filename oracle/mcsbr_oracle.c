@@ -951,7 +951,8 @@ static int validate(const mcsbr_mc_config* c) { /* solver_mc.cpp:10-17 */
 static int estimate_impl(const orc_scene* s, const mcsbr_excitation* exc, const double* freqs,
                          uint32_t nf, const mcsbr_mc_config* cfg, double* values, mcsbr_stats* st_out,
                          mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs,
-                         plog_t* plog) {
+                         plog_t* plog, uint64_t range_begin, uint64_t range_end, double* raw_out,
+                         uint64_t* total_out) {
     g_fault = 0;
     if (validate(cfg)) return -1;
     if (nf == 0) { set_err("estimate: empty frequency list"); return -1; }
@@ -989,9 +990,14 @@ static int estimate_impl(const orc_scene* s, const mcsbr_excitation* exc, const 
     block_t blk;
     memset(&blk, 0, sizeof blk);
 
+    if (total_out) *total_out = total;
     for (uint64_t block = 0; block < nblocks; ++block) {
-        const uint64_t begin = block * bs;
-        const uint64_t end = total < begin + bs ? total : begin + bs;
+        uint64_t begin = block * bs;
+        uint64_t end = total < begin + bs ? total : begin + bs;
+        /* optional entry range (multi-rank sharding checks) */
+        if (begin < range_begin) begin = range_begin;
+        if (end > range_end) end = range_end;
+        if (begin >= end) continue;
         if (plog && (end <= plog->first || begin >= plog->first + plog->n)) continue;
         mcsbr_stats* st = &blk.st;
         memset(st, 0, sizeof *st);
@@ -1160,6 +1166,14 @@ static int estimate_impl(const orc_scene* s, const mcsbr_excitation* exc, const 
     tot.block_size = bs;
     if (st_out) *st_out = tot;
     if (n_contribs) *n_contribs = ncontrib_total;
+    /* raw (un-finalized) sums in the device layout [nf][4] complex */
+    if (raw_out) {
+        for (uint32_t i = 0; i < nf; ++i)
+            for (int ch = 0; ch < 4; ++ch) {
+                raw_out[2 * (i * 4 + ch)] = total_acc.sums[ch * nf + i].re;
+                raw_out[2 * (i * 4 + ch) + 1] = total_acc.sums[ch * nf + i].im;
+            }
+    }
     /* finalize, farfield.cpp:154-167 */
     if (values) {
         for (int ch = 0; ch < 4; ++ch) {
@@ -1189,7 +1203,15 @@ fault:
 int orc_estimate(const orc_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
                  const mcsbr_mc_config* cfg, double* values, mcsbr_stats* st,
                  mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
-    return estimate_impl(s, exc, freqs, nf, cfg, values, st, contribs, capacity, n_contribs, NULL);
+    return estimate_impl(s, exc, freqs, nf, cfg, values, st, contribs, capacity, n_contribs, NULL, 0,
+                         UINT64_MAX, NULL, NULL);
+}
+
+int orc_estimate_range(const orc_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+                       const mcsbr_mc_config* cfg, uint64_t entry_begin, uint64_t entry_end, double* raw_sums,
+                       mcsbr_stats* st, uint64_t* total_entries) {
+    return estimate_impl(s, exc, freqs, nf, cfg, NULL, st, NULL, 0, NULL, NULL, entry_begin, entry_end,
+                         raw_sums, total_entries);
 }
 
 int orc_path_log(const orc_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
@@ -1201,5 +1223,5 @@ int orc_path_log(const orc_scene* s, const mcsbr_excitation* exc, const double* 
         term[i] = 0;
         branch_bits[i] = 0;
     }
-    return estimate_impl(s, exc, freqs, nf, cfg, NULL, NULL, NULL, 0, NULL, &pl);
+    return estimate_impl(s, exc, freqs, nf, cfg, NULL, NULL, NULL, 0, NULL, &pl, 0, UINT64_MAX, NULL, NULL);
 }

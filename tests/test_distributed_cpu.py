@@ -1,0 +1,89 @@
+"""CPU, world_size 2 (gloo): the multi-rank reduction path.
+
+Each rank computes the raw accumulators of ITS launch-entry shard
+(distributed.shard_range, the partition mcsbr_gpu_trace_device applies) with
+the oracle standing in for the device trace, then runs the product's
+allreduce_finalize (the same code the NCCL path runs).  The reduced result
+must equal the single-process estimate to fp64 rounding, and the counters
+must add up exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2511_07586_b200 as M
+from paper_2511_07586_b200 import distributed as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case():
+    sd = M.make_builtin_scene("glass_cube", {"eps_r": 2.25, "size_m": 1.0})
+    exc = M.bistatic_excitation(20.0, 40.0, 60.0, 10.0)
+    freqs = np.linspace(1e9, 3e9, 4)
+    cfg = M.McConfig(strata_per_wavelength=6, samples_per_stratum=2, seed=99,
+                     roulette=M.RouletteConfig(enabled=True))
+    return sd, exc, freqs, cfg
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sd, exc, freqs, cfg = _case()
+        ps = oracle.port_scene(sd)
+        _, _, total = oracle.port_estimate_range(ps, exc.to_c(), freqs, cfg.to_c(), 0, 0)
+        b, e = D.shard_range(total, rank, world)
+        raw, st, _ = oracle.port_estimate_range(ps, exc.to_c(), freqs, cfg.to_c(), b, e)
+        sums = torch.from_numpy(raw.reshape(-1).copy())
+        counters = torch.zeros(256, dtype=torch.int64)
+        counters[0] = st.rays_launched
+        counters[2] = st.contributions
+        counters[4] = st.cap_kills
+        for i in range(64):
+            counters[8 + i] = st.rays_per_bounce[i]
+            counters[72 + i] = st.roulette_candidates[i]
+            counters[136 + i] = st.roulette_survivors[i]
+        values, stats = D.allreduce_finalize(sums, counters, freqs, 1)
+        if rank == 0:
+            np.save(out, values.reshape(4, len(freqs)))
+            np.save(out + ".cnt.npy", np.array([stats.rays_launched, stats.contributions,
+                                                 stats.cap_kills, stats.segments_traced]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_range_partition():
+    for entries in (0, 1, 7, 1000, 4_008_004, 10**12 + 3):
+        for world in (1, 2, 3, 8):
+            r = [D.shard_range(entries, k, world) for k in range(world)]
+            assert r[0][0] == 0 and r[-1][1] == entries
+            assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
+            assert max(e - b for b, e in r) - min(e - b for b, e in r) <= 1
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_reduction_matches_single_process(tmp_path):
+    out = str(tmp_path / "vals.npy")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    cnt = np.load(out + ".cnt.npy")
+    sd, exc, freqs, cfg = _case()
+    ref = oracle.port_estimate(oracle.port_scene(sd), exc.to_c(), freqs, cfg.to_c())
+    scale = np.max(np.abs(ref["values"]))
+    assert np.max(np.abs(got - ref["values"])) <= 1e-12 * scale
+    st = ref["stats"]
+    assert list(cnt) == [st.rays_launched, st.contributions, st.cap_kills, st.segments_traced]

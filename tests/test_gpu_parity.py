@@ -235,6 +235,21 @@ def test_bistatic_fan_equals_per_receiver_estimates():
     assert st.contributions == contribs
 
 
+def test_sweep_sharded_single_rank_equals_batch():
+    """distributed.sweep_sharded (device buffers + finalize) == estimate_batch."""
+    from paper_2511_07586_b200 import distributed as D
+
+    obj, mm = M.dihedral_grid(0.5, 8)
+    s = M.Scene(M.load_scene(obj, mm))
+    cfg = M.McConfig(strata_per_wavelength=6, samples_per_stratum=1, max_bounce=4, seed=2)
+    excs = [M.monostatic_excitation(90.0, p) for p in (5.0, 45.0, 85.0)]
+    freqs = np.linspace(9.5e9, 10.5e9, 3)
+    a, sa = M.estimate_batch(s, [(e, 0.0) for e in excs], [[e] for e in excs], freqs, cfg)
+    b, sb = D.sweep_sharded(s, [(e, 0.0) for e in excs], [[e] for e in excs], freqs, cfg)
+    assert np.max(np.abs(a - b)) <= 1e-10 * np.max(np.abs(a))
+    assert sa.rays_launched == sb.rays_launched and sa.contributions == sb.contributions
+
+
 def test_statistical_mode_within_half_db():
     """Mode (2): Philox stream; RCS within 0.5 dB RMS of the reference-stream
     result across the sweep (16 samples per stratum keeps the MC noise of two
