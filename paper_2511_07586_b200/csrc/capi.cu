@@ -97,6 +97,7 @@ struct mcsbr_scene {
     double center[3] = {0, 0, 0};
     double radius = 0.0, diameter = 0.0;
     double ambient_n = 1.0;
+    bool all_pec = false;  // every triangle has a PEC side (kernel specialisation)
     double* d_vtx = nullptr;
     uint4* d_tri = nullptr;
     double2* d_info = nullptr;
@@ -122,6 +123,7 @@ struct mcsbr_scene {
         s.diameter = diameter;
         s.t_eps = 1e-6 * diameter;
         s.ambient_n = ambient_n;
+        s.all_pec = all_pec ? 1 : 0;
         s.center[0] = center[0];
         s.center[1] = center[1];
         s.center[2] = center[2];
@@ -485,6 +487,9 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
         info[2ull * i] = make_double2(tris[i].normal[0], tris[i].normal[1]);
         info[2ull * i + 1] = make_double2(tris[i].normal[2], pd);
     }
+    s->all_pec = true;
+    for (uint32_t i = 0; i < nt && s->all_pec; ++i)
+        s->all_pec = mats[tris[i].front_material].is_pec || mats[tris[i].back_material].is_pec;
     std::vector<double2> mat(nm);
     for (uint32_t i = 0; i < nm; ++i)
         mat[i] = make_double2(mats[i].is_pec ? 0.0 : std::sqrt(mats[i].eps_r * mats[i].mu_r),

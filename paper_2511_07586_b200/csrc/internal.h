@@ -39,6 +39,7 @@ struct SceneView {
     double diameter;
     double t_eps;      // 1e-6 * diameter (geometry.hpp:78)
     double ambient_n;  // materials[0].index()
+    int32_t all_pec;   // every triangle has a PEC side: dielectric code compiled out
     double center[3];  // bounding-sphere centre: origin of the fp32 box frame
     double skip_radius;  // bounding radius + margin (traversal origin advance)
 };

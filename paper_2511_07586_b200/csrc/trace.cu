@@ -258,6 +258,60 @@ struct Path {
     uint64_t key;  // counter_prefix(seed, cell, sample) or the Philox ray index
 };
 
+// Per-thread shared-memory slot (SoA: field f of thread t at base[f * 128 + t])
+// for the state that is NOT needed while a ray is traversed: the two complex
+// fields, phi / prob / weight / medium_n, a pending contribution and the
+// phasor sums.  Only the ray itself stays in registers across a traversal,
+// which removes the register spills (measured: ~15 G local sectors and
+// ~55 GB of DRAM write-back per c2 launch when this state lived in
+// registers under the 128-register budget).  Accesses go through a volatile
+// pointer so the compiler re-reads the slot instead of keeping copies live.
+constexpr int kSlotThreads = 128;
+enum : int {
+    kFE0 = 0, kFE1 = 6, kFPhi = 12, kFProb = 13, kFWeight = 14, kFMedium = 15,
+    kFAmp = 16, kFSPath = 24, kFAcc = 25, kSlotFields = 33,
+};
+
+struct Slot {
+    volatile double* p;
+    __device__ __forceinline__ double get(int f) const { return p[f * kSlotThreads]; }
+    __device__ __forceinline__ void set(int f, double v) const { p[f * kSlotThreads] = v; }
+    __device__ __forceinline__ Cx getc(int f) const { return {get(f), get(f + 1)}; }
+    __device__ __forceinline__ void setc(int f, Cx v) const {
+        set(f, v.re);
+        set(f + 1, v.im);
+    }
+    __device__ __forceinline__ CV3 getv(int f) const { return {getc(f), getc(f + 2), getc(f + 4)}; }
+    __device__ __forceinline__ void setv(int f, const CV3& v) const {
+        setc(f, v.x);
+        setc(f + 2, v.y);
+        setc(f + 4, v.z);
+    }
+};
+
+__device__ __forceinline__ void save_em(const Slot& sl, const Path& s) {
+    sl.setv(kFE0, s.e0);
+    sl.setv(kFE1, s.e1);
+    sl.set(kFPhi, s.phi);
+    sl.set(kFProb, s.prob);
+    sl.set(kFWeight, s.weight);
+    sl.set(kFMedium, s.medium_n);
+}
+
+__device__ __forceinline__ void load_em(const Slot& sl, Path& s) {
+    s.e0 = sl.getv(kFE0);
+    s.e1 = sl.getv(kFE1);
+    s.phi = sl.get(kFPhi);
+    s.prob = sl.get(kFProb);
+    s.weight = sl.get(kFWeight);
+    s.medium_n = sl.get(kFMedium);
+}
+
+__device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) sl.setc(kFAcc + 2 * ch, sl.getc(kFAcc + 2 * ch) + am[ch] * z);
+}
+
 __device__ __forceinline__ double draw(const TraceParams& P, const Path& s, uint64_t bounce,
                                        uint64_t purpose) {
     if (P.rng_mode == MCSBR_RNG_REFERENCE) return u53(counter_finish(s.key, bounce, purpose));
@@ -341,7 +395,7 @@ enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
-template <int kMode>
+template <int kMode, bool kDiel>
 __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeSmem;
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
@@ -350,9 +404,11 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
     // 64-bit shared atomicAdd is a CAS loop on sm_100 and cost ~20% of the
     // kernel.  Per block and bounce they stay far below 2^32.
     __shared__ unsigned int s_bounce[3 * 64];
+    __shared__ double s_state[kSlotFields * kSlotThreads];
     for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) s_cnt[i] = 0;
     for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
+    const Slot sl{s_state + threadIdx.x};
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -391,13 +447,16 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + (has_rx ? my_rx : P.rx_index)];
         uint64_t cursor = e_begin;  // warp-uniform
 
-        Cx acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        if (kRegAcc) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sl.set(kFAcc + k, 0.0);
+        }
         bool alive = false;  // lane holds a path (possibly only its last occlusion query)
         bool pend = false;   // next query is the chi occlusion test of a contribution
         bool dying = false;  // the path ends once its pending occlusion test is done
         Path s;
-        Cx amp[4];           // pending contribution: receiver-projected amplitudes
-        double s_path = 0.0; //                       and net optical path
+        Cx amp[4];           // contribution: receiver-projected amplitudes (slot while pending)
+        double s_path = 0.0; //               and net optical path
         CV3 fj0, fm0, fj1, fm1;  // fan mode: the contribution's currents,
         double fphi = 0.0;       // optical path
         V3 fpt = {0.0, 0.0, 0.0};  // and exit point, broadcast to the warp
@@ -414,6 +473,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
                     init_path(P, I, a, mine, s);
+                    save_em(sl, s);
                     alive = true;
                     ++n_launched;
                 }
@@ -438,6 +498,11 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             if (alive && pend) {
                 pend = false;
                 visible = !hit;
+                if (visible) {  // the queued contribution's amplitudes come back from the slot
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) amp[ch] = sl.getc(kFAmp + 2 * ch);
+                    s_path = sl.get(kFSPath);
+                }
                 if (dying) {
                     alive = false;
                     dying = false;
@@ -447,6 +512,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 if (!hit) {
                     alive = false;  // escaped
                 } else {
+                    load_em(sl, s);
                     const V3 point = s.origin + s.dir * t;
                     const HitInfo h = fill_hit(S, id, s.dir);
                     // advance (path_engine.cpp:17-21)
@@ -464,7 +530,10 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         alive = false;
                         if (logged) P.plog_term[s.entry] = 1;
                     } else {
-                        const bool pec = h.far_side_pec;
+                        // kDiel = false: every triangle has a PEC side (checked at
+                        // scene creation), so far_side_pec always holds and the
+                        // dielectric code (and its registers) is compiled out.
+                        const bool pec = kDiel ? h.far_side_pec : true;
                         const double n1 = s.medium_n;
                         const double n2 = pec ? n1 : h.n_transmit;
                         const Coeffs co = pec ? coeffs_pec() : fresnel(n1, n2, cos_i, fault);
@@ -587,6 +656,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                             }
                         }
                     }
+                    save_em(sl, s);
                 }
                 // ---- chi visibility (farfield.cpp:63-68): queue the occlusion query ----
                 if (candidate && kMode == kModeFan) {
@@ -594,6 +664,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 } else if (candidate) {
                     if (P.occlusion) {
                         pend = true;
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) sl.setc(kFAmp + 2 * ch, amp[ch]);
+                        sl.set(kFSPath, s_path);
                         if (!alive) {
                             alive = true;
                             dying = true;
@@ -631,6 +704,11 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                     const double ph = shfl_d(fphi, src);
                     const V3 pt = {shfl_d(fpt.x, src), shfl_d(fpt.y, src), shfl_d(fpt.z, src)};
                     if (has_rx) {
+                        // project first: only 4 complex amplitudes + s stay live
+                        // across this receiver's occlusion traversal
+                        Cx am[4];
+                        project(R, c[0], c[1], c[2], c[3], am);
+                        const double sp = ph - dot(ks, pt);
                         bool vis = true;
                         if (P.occlusion) {
                             double t2;
@@ -640,13 +718,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         }
                         if (vis) {
                             ++n_contrib;
-                            Cx am[4];
-                            project(R, c[0], c[1], c[2], c[3], am);
                             double sn, cs;
-                            sincos(-P.k0[0] * (ph - dot(ks, pt)), &sn, &cs);
-                            const Cx z = {cs, sn};
-#pragma unroll
-                            for (int ch = 0; ch < 4; ++ch) acc[ch] = acc[ch] + am[ch] * z;
+                            sincos(-P.k0[0] * sp, &sn, &cs);
+                            acc_add(sl, am, Cx{cs, sn});
                         }
                     }
                 }
@@ -655,9 +729,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 if (visible) {
                     double sn, cs;
                     sincos(-P.k0[0] * s_path, &sn, &cs);
-                    const Cx z = {cs, sn};
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) acc[ch] = acc[ch] + amp[ch] * z;
+                    acc_add(sl, amp, Cx{cs, sn});
                 }
             } else {
                 unsigned vm = __ballot_sync(kFull, visible);
@@ -693,15 +765,15 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             if (has_rx) {  // lane-owned receiver: nf == 1, no warp reduction
                 double* o = P.sums + (static_cast<size_t>(a) * P.n_rx + my_rx) * 8;
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    if (acc[ch].re != 0.0) atomicAdd(o + 2 * ch, acc[ch].re);
-                    if (acc[ch].im != 0.0) atomicAdd(o + 2 * ch + 1, acc[ch].im);
+                for (int k = 0; k < 8; ++k) {
+                    const double v = sl.get(kFAcc + k);
+                    if (v != 0.0) atomicAdd(o + k, v);
                 }
             }
         } else if (kRegAcc) {
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
-                double re = acc[ch].re, im = acc[ch].im;
+                double re = sl.get(kFAcc + 2 * ch), im = sl.get(kFAcc + 2 * ch + 1);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     re += __shfl_xor_sync(kFull, re, o);
@@ -781,37 +853,42 @@ bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
 
 bool trace_fan_supported(uint32_t nf) { return nf == 1; }
 
-template <int kMode>
-static cudaError_t occupancy(int* per_sm, int threads, size_t smem) {
+template <int kMode, bool kDiel>
+static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
+                               cudaStream_t stream) {
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(path_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
+        cudaError_t e = cudaFuncSetAttribute(path_kernel<kMode, kDiel>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, path_kernel<kMode>, threads, smem);
+    int per_sm = 1;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<kMode, kDiel>, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
+    const uint64_t max_blocks = (p.total_tiles + threads / 32 - 1) / (threads / 32);
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    path_kernel<kMode, kDiel><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
     const int mode = p.fan ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
     const size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
-    int per_sm = 1;
-    cudaError_t e = mode == kModeFan   ? occupancy<kModeFan>(&per_sm, threads, smem)
-                    : mode == kModeReg ? occupancy<kModeReg>(&per_sm, threads, smem)
-                                       : occupancy<kModeSmem>(&per_sm, threads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
-    const uint64_t warps_needed = p.total_tiles;
-    const uint64_t max_blocks = (warps_needed + threads / 32 - 1) / (threads / 32);
-    if (blocks > max_blocks) blocks = max_blocks;
-    if (blocks < 1) blocks = 1;
-    const unsigned g = static_cast<unsigned>(blocks);
-    if (mode == kModeFan) path_kernel<kModeFan><<<g, threads, smem, stream>>>(p);
-    else if (mode == kModeReg) path_kernel<kModeReg><<<g, threads, smem, stream>>>(p);
-    else path_kernel<kModeSmem><<<g, threads, smem, stream>>>(p);
+    cudaError_t e;
+    if (p.scene.all_pec) {
+        e = mode == kModeFan   ? launch_mode<kModeFan, false>(p, device_sms, threads, smem, stream)
+            : mode == kModeReg ? launch_mode<kModeReg, false>(p, device_sms, threads, smem, stream)
+                               : launch_mode<kModeSmem, false>(p, device_sms, threads, smem, stream);
+    } else {
+        e = mode == kModeFan   ? launch_mode<kModeFan, true>(p, device_sms, threads, smem, stream)
+            : mode == kModeReg ? launch_mode<kModeReg, true>(p, device_sms, threads, smem, stream)
+                               : launch_mode<kModeSmem, true>(p, device_sms, threads, smem, stream);
+    }
     if (launches) ++*launches;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d, const double* tmin,
