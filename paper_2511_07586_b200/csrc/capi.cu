@@ -98,6 +98,8 @@ struct mcsbr_scene {
     double radius = 0.0, diameter = 0.0;
     double ambient_n = 1.0;
     bool all_pec = false;  // every triangle has a PEC side (kernel specialisation)
+    bool lossy = false;    // complex-permittivity transport
+    double* d_nim = nullptr;
     double* d_vtx = nullptr;
     uint4* d_tri = nullptr;
     double2* d_info = nullptr;
@@ -124,6 +126,8 @@ struct mcsbr_scene {
         s.t_eps = 1e-6 * diameter;
         s.ambient_n = ambient_n;
         s.all_pec = all_pec ? 1 : 0;
+        s.lossy = lossy ? 1 : 0;
+        s.mat_nim = d_nim;
         s.center[0] = center[0];
         s.center[1] = center[1];
         s.center[2] = center[2];
@@ -422,10 +426,11 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     if (nm == 0 || !mats) return set_err(MCSBR_ESCENE, "material map: missing 'materials' object");
     if (nv == 0 || !xyz) return set_err(MCSBR_ESCENE, "scene is degenerate (zero extent)");
     if (mats[0].is_pec) return set_err(MCSBR_ESCENE, "material map: ambient material cannot be PEC");
+    if (eps_imag && eps_imag[0] != 0.0)
+        return set_err(MCSBR_EINVAL, "lossy media: the ambient material must be lossless (eps_imag[0] == 0)");
     for (uint32_t i = 0; i < nm; ++i) {
-        if (eps_imag && eps_imag[i] != 0.0)
-            return set_err(MCSBR_EINVAL,
-                           "lossy permittivity (Im eps != 0) is not supported by this build; pass eps_imag = NULL");
+        if (eps_imag && !(eps_imag[i] >= 0.0 && std::isfinite(eps_imag[i])))
+            return set_err(MCSBR_EINVAL, "lossy media: eps_imag must be finite and >= 0 (eps = eps_r - j eps_imag)");
         if (!mats[i].is_pec && (!(mats[i].eps_r > 0.0) || !(mats[i].mu_r > 0.0) ||
                                 !std::isfinite(mats[i].eps_r) || !std::isfinite(mats[i].mu_r)))
             return set_err(MCSBR_ESCENE, "material: eps_r and mu_r must be positive");
@@ -491,9 +496,20 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     for (uint32_t i = 0; i < nt && s->all_pec; ++i)
         s->all_pec = mats[tris[i].front_material].is_pec || mats[tris[i].back_material].is_pec;
     std::vector<double2> mat(nm);
-    for (uint32_t i = 0; i < nm; ++i)
-        mat[i] = make_double2(mats[i].is_pec ? 0.0 : std::sqrt(mats[i].eps_r * mats[i].mu_r),
-                              mats[i].is_pec ? 1.0 : 0.0);
+    std::vector<double> nim(nm, 0.0);
+    s->lossy = eps_imag != nullptr;  // complex-permittivity transport requested
+    for (uint32_t i = 0; i < nm; ++i) {
+        double n_re = mats[i].is_pec ? 0.0 : std::sqrt(mats[i].eps_r * mats[i].mu_r);  // Material::index()
+        if (s->lossy && !mats[i].is_pec && eps_imag[i] != 0.0) {
+            // n = sqrt((eps_r - j eps_i) mu_r), principal root: Re n > 0, Im n < 0
+            const double a = mats[i].eps_r * mats[i].mu_r, b = -eps_imag[i] * mats[i].mu_r;
+            const double m = std::hypot(a, b);
+            n_re = std::sqrt(0.5 * (m + a));
+            nim[i] = b / (2.0 * n_re);
+        }
+        mat[i] = make_double2(n_re, mats[i].is_pec ? 1.0 : 0.0);
+    }
+    if (s->lossy) s->all_pec = false;
 
     auto fail = [&](cudaError_t e2, const char* what) {
         mcsbr_gpu_scene_destroy(s);
@@ -517,6 +533,12 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     if ((e = cudaMemcpyAsync(s->d_mat, mat.data(), sizeof(double2) * nm, cudaMemcpyHostToDevice, s->stream)) !=
         cudaSuccess)
         return fail(e, "upload materials");
+    if (s->lossy) {
+        if ((e = cudaMalloc(&s->d_nim, sizeof(double) * nm)) != cudaSuccess) return fail(e, "cudaMalloc(Im n)");
+        if ((e = cudaMemcpyAsync(s->d_nim, nim.data(), sizeof(double) * nm, cudaMemcpyHostToDevice, s->stream)) !=
+            cudaSuccess)
+            return fail(e, "upload Im n");
+    }
     const double lo3[3] = {lo.x, lo.y, lo.z}, hi3[3] = {hi.x, hi.y, hi.z};
     const double box_pad = 1e-5 * r + 1e-30;
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
@@ -539,6 +561,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     cudaFree(s->d_tri);
     cudaFree(s->d_info);
     cudaFree(s->d_mat);
+    cudaFree(s->d_nim);
     cudaFree(s->bvh.nodes);
     cudaFree(s->bvh.tri64);
     s->inc.release();

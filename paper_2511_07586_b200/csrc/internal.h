@@ -40,6 +40,8 @@ struct SceneView {
     double t_eps;      // 1e-6 * diameter (geometry.hpp:78)
     double ambient_n;  // materials[0].index()
     int32_t all_pec;   // every triangle has a PEC side: dielectric code compiled out
+    int32_t lossy;     // complex-permittivity transport (eps_imag given at scene creation)
+    const double* mat_nim;  // per material Im(n) (lossy scenes), else nullptr
     double center[3];  // bounding-sphere centre: origin of the fp32 box frame
     double skip_radius;  // bounding radius + margin (traversal origin advance)
 };

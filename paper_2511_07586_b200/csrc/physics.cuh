@@ -71,6 +71,95 @@ __device__ inline Coeffs fresnel(double n1, double n2, double cos_i, uint32_t& f
     return c;
 }
 
+// ---- lossy-media extension (not in the reference: Material is real there,
+// em_math.hpp:99-105).  eps = eps_r - j eps_i, n = sqrt(eps mu) with Im n <= 0.
+
+// principal complex square root; exact sqrt(x) for a non-negative real input
+__device__ __forceinline__ Cx csqrt(Cx z) {
+    if (z.im == 0.0) return z.re >= 0.0 ? Cx{sqrt(z.re), 0.0} : Cx{0.0, sqrt(-z.re)};
+    const double m = hypot(z.re, z.im);
+    const double a = sqrt(0.5 * (m + fabs(z.re)));
+    const double b = 0.5 * z.im / a;
+    return z.re >= 0.0 ? Cx{a, b} : Cx{fabs(b), copysign(a, z.im)};
+}
+
+// ---- index-type helpers: the path kernel is written once for NT = double
+// (the reference's lossless model, bit-exact) and NT = Cx (lossy extension).
+__device__ __forceinline__ double re_of(double x) { return x; }
+__device__ __forceinline__ double re_of(Cx x) { return x.re; }
+__device__ __forceinline__ double im_of(double) { return 0.0; }
+__device__ __forceinline__ double im_of(Cx x) { return x.im; }
+__device__ __forceinline__ Cx operator-(Cx a, double b) { return {a.re - b, a.im}; }
+template <typename NT>
+__device__ __forceinline__ NT make_nt(double re, double im);
+template <>
+__device__ __forceinline__ double make_nt<double>(double re, double) { return re; }
+template <>
+__device__ __forceinline__ Cx make_nt<Cx>(double re, double im) { return {re, im}; }
+
+// e^{-j k0 s}: the phase of farfield.cpp:128-145; for a complex optical path
+// the imaginary part (<= 0 in lossy media) gives the attenuation e^{k0 Im s}.
+__device__ __forceinline__ Cx phasor(double k0, double s) {
+    double sn, cs;
+    sincos(-k0 * s, &sn, &cs);
+    return {cs, sn};
+}
+__device__ __forceinline__ Cx phasor(double k0, Cx s) {
+    double sn, cs;
+    sincos(-k0 * s.re, &sn, &cs);
+    const double a = exp(k0 * s.im);
+    return {cs * a, sn * a};
+}
+
+// Fresnel coefficients for complex indices (fresnel() generalised): the
+// transmitted cos_t root is chosen physically (below); `tir` is decided from
+// the real parts (the ray geometry uses Re n).  For real n1, n2 this
+// reproduces fresnel() operation for operation, incl. the -j branch under TIR.
+__device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_t& fault) {
+    Coeffs c;
+    c.tir = tir;
+    if (!(n1.re > 0.0) || !(n2.re > 0.0) || !(cos_i > 0.0 && cos_i <= 1.0) || !isfinite(n1.re) ||
+        !isfinite(n2.re)) {
+        fault |= kFaultFresnel;
+        c.r_s = c.r_p = c.t_s = c.t_p = c.cos_t = {0.0, 0.0};
+        return c;
+    }
+    const double x = 1.0 - cos_i * cos_i;
+    const double sin2_i = (0.0 < x) ? x : 0.0;
+    const Cx q = cdiv(n1, n2);
+    const Cx s2 = (q * q) * sin2_i;
+    // Root choice for k_z = k0 n2 cos_t: a propagating transmitted wave
+    // (|Re k_z| >= |Im k_z|) must carry power away (Re k_z >= 0); an
+    // evanescent one must decay away from the interface (Im k_z <= 0).  For
+    // real indices this gives the reference's branches exactly: the real
+    // root below the critical angle and (0, -sqrt(s2 - 1)) under TIR.
+    Cx cos_t = csqrt(Cx{1.0 - s2.re, -s2.im});
+    const Cx kz = n2 * cos_t;
+    const bool flip = fabs(kz.re) >= fabs(kz.im) ? kz.re < 0.0 : kz.im > 0.0;
+    if (flip) cos_t = {-cos_t.re, -cos_t.im};
+    if (cos_t.re == 0.0) cos_t.re = 0.0;  // no -0 (matches the reference's (0, -x))
+    c.cos_t = cos_t;
+    const Cx ci = {cos_i, 0.0};
+    const Cx den_s = ci * n1 + cos_t * n2;
+    const Cx den_p = ci * n2 + cos_t * n1;
+    c.r_s = cdiv(ci * n1 - cos_t * n2, den_s);
+    c.t_s = cdiv(ci * (n1 * 2.0), den_s);
+    c.r_p = cdiv(ci * n2 - cos_t * n1, den_p);
+    c.t_p = cdiv(ci * (n1 * 2.0), den_p);
+    return c;
+}
+
+// fresnel for either index type; the lossy TIR decision uses the real parts
+__device__ __forceinline__ Coeffs fresnel_any(double n1, double n2, double cos_i, uint32_t& fault) {
+    return fresnel(n1, n2, cos_i, fault);
+}
+__device__ __forceinline__ Coeffs fresnel_any(Cx n1, Cx n2, double cos_i, uint32_t& fault) {
+    const double x = 1.0 - cos_i * cos_i;
+    const double sin2_i = (0.0 < x) ? x : 0.0;
+    const double r = n1.re / n2.re;
+    return fresnel_c(n1, n2, cos_i, r * r * sin2_i > 1.0, fault);
+}
+
 __device__ __forceinline__ V3 reflect_dir(V3 dir, V3 normal, uint32_t& fault) {
     const double dn = dot(dir, normal);
     if (fabs(dn) < 1e-9) fault |= kFaultGrazingDir;

@@ -26,6 +26,7 @@
 // l, l+32, ... (fp64 phase, sincos) into its own slots, flushed with atomics
 // once per tile.
 #include <cstdio>
+#include <type_traits>
 
 #include "dmath.cuh"
 #include "internal.h"
@@ -218,28 +219,32 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
     return best_id != 0xffffffffu;
 }
 
-// fill_hit (geometry.cpp:164-175)
+// fill_hit (geometry.cpp:164-175); NT = Cx adds Im(n) from S.mat_nim
+template <typename NT>
 struct HitInfo {
     V3 normal;
-    double n_incident, n_transmit;
+    NT n_incident, n_transmit;
     bool far_side_pec, exterior_facing, near_is_ambient;
 };
 
-__device__ __forceinline__ HitInfo fill_hit(const SceneView& S, uint32_t id, V3 dir) {
+template <typename NT>
+__device__ __forceinline__ HitInfo<NT> fill_hit(const SceneView& S, uint32_t id, V3 dir) {
     const double2 ta = __ldg(S.tri_info + 2ull * id), tb = __ldg(S.tri_info + 2ull * id + 1);
     const uint64_t packed = static_cast<uint64_t>(__double_as_longlong(tb.y));
     const V3 nrm = {ta.x, ta.y, tb.x};
     const bool front = dot(dir, nrm) < 0.0;
-    HitInfo h;
+    HitInfo<NT> h;
     h.normal = front ? nrm : -nrm;
     const uint32_t fm = static_cast<uint32_t>(packed & 0xffffu);
     const uint32_t bm = static_cast<uint32_t>((packed >> 16) & 0xffffu);
     const uint32_t near_id = front ? fm : bm, far_id = front ? bm : fm;
     const double2 nm = __ldg(S.mat + near_id), fr = __ldg(S.mat + far_id);
     const bool near_pec = nm.y != 0.0, far_pec = fr.y != 0.0;
-    h.n_incident = near_pec ? S.ambient_n : nm.x;
+    const double nim_near = S.mat_nim ? __ldg(S.mat_nim + near_id) : 0.0;
+    const double nim_far = S.mat_nim ? __ldg(S.mat_nim + far_id) : 0.0;
+    h.n_incident = near_pec ? make_nt<NT>(S.ambient_n, 0.0) : make_nt<NT>(nm.x, nim_near);
     h.far_side_pec = far_pec || near_pec;
-    h.n_transmit = far_pec ? 0.0 : fr.x;
+    h.n_transmit = far_pec ? make_nt<NT>(0.0, 0.0) : make_nt<NT>(fr.x, nim_far);
     h.exterior_facing = ((packed >> 32) & 1u) != 0;
     h.near_is_ambient = near_id == 0;
     return h;
@@ -248,10 +253,15 @@ __device__ __forceinline__ HitInfo fill_hit(const SceneView& S, uint32_t id, V3 
 // ---------------------------------------------------------------------------
 // per-path state (PathState, proj/include/mcsbr/path_engine.hpp:16-28)
 
+// NT = double: the reference model; NT = Cx: complex optical path / index
+// (lossy extension).
+template <typename NT>
 struct Path {
     V3 origin, dir;
     CV3 e0, e1;
-    double phi, prob, weight, medium_n;
+    NT phi;
+    double prob, weight;
+    NT medium_n;
     int bounce;
     uint32_t cell, sample;
     uint64_t entry;
@@ -269,7 +279,8 @@ struct Path {
 constexpr int kSlotThreads = 128;
 enum : int {
     kFE0 = 0, kFE1 = 6, kFPhi = 12, kFProb = 13, kFWeight = 14, kFMedium = 15,
-    kFAmp = 16, kFSPath = 24, kFAcc = 25, kSlotFields = 33,
+    kFAmp = 16, kFSPath = 24, kFAcc = 25, kFPhiIm = 33, kFMediumIm = 34, kFSPathIm = 35,
+    kSlotFields = 36,
 };
 
 struct Slot {
@@ -289,22 +300,37 @@ struct Slot {
     }
 };
 
-__device__ __forceinline__ void save_em(const Slot& sl, const Path& s) {
-    sl.setv(kFE0, s.e0);
-    sl.setv(kFE1, s.e1);
-    sl.set(kFPhi, s.phi);
-    sl.set(kFProb, s.prob);
-    sl.set(kFWeight, s.weight);
-    sl.set(kFMedium, s.medium_n);
+__device__ __forceinline__ void slot_set_nt(const Slot& sl, int f, int fim, double v) {
+    (void)fim;
+    sl.set(f, v);
+}
+__device__ __forceinline__ void slot_set_nt(const Slot& sl, int f, int fim, Cx v) {
+    sl.set(f, v.re);
+    sl.set(fim, v.im);
+}
+template <typename NT>
+__device__ __forceinline__ NT slot_get_nt(const Slot& sl, int f, int fim) {
+    return make_nt<NT>(sl.get(f), std::is_same<NT, Cx>::value ? sl.get(fim) : 0.0);
 }
 
-__device__ __forceinline__ void load_em(const Slot& sl, Path& s) {
+template <typename NT>
+__device__ __forceinline__ void save_em(const Slot& sl, const Path<NT>& s) {
+    sl.setv(kFE0, s.e0);
+    sl.setv(kFE1, s.e1);
+    slot_set_nt(sl, kFPhi, kFPhiIm, s.phi);
+    sl.set(kFProb, s.prob);
+    sl.set(kFWeight, s.weight);
+    slot_set_nt(sl, kFMedium, kFMediumIm, s.medium_n);
+}
+
+template <typename NT>
+__device__ __forceinline__ void load_em(const Slot& sl, Path<NT>& s) {
     s.e0 = sl.getv(kFE0);
     s.e1 = sl.getv(kFE1);
-    s.phi = sl.get(kFPhi);
+    s.phi = slot_get_nt<NT>(sl, kFPhi, kFPhiIm);
     s.prob = sl.get(kFProb);
     s.weight = sl.get(kFWeight);
-    s.medium_n = sl.get(kFMedium);
+    s.medium_n = slot_get_nt<NT>(sl, kFMedium, kFMediumIm);
 }
 
 __device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
@@ -312,15 +338,17 @@ __device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
     for (int ch = 0; ch < 4; ++ch) sl.setc(kFAcc + 2 * ch, sl.getc(kFAcc + 2 * ch) + am[ch] * z);
 }
 
-__device__ __forceinline__ double draw(const TraceParams& P, const Path& s, uint64_t bounce,
+template <typename NT>
+__device__ __forceinline__ double draw(const TraceParams& P, const Path<NT>& s, uint64_t bounce,
                                        uint64_t purpose) {
     if (P.rng_mode == MCSBR_RNG_REFERENCE) return u53(counter_finish(s.key, bounce, purpose));
     return philox_uniform(P.seed, s.key, static_cast<uint32_t>(bounce), static_cast<uint32_t>(purpose));
 }
 
 // sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
+template <typename NT>
 __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
-                                          uint64_t entry, Path& s) {
+                                          uint64_t entry, Path<NT>& s) {
     const uint32_t cell = static_cast<uint32_t>(entry / P.spp);
     const uint32_t sample = static_cast<uint32_t>(entry % P.spp);
     const uint32_t i = cell % static_cast<uint32_t>(I.nu);
@@ -348,10 +376,10 @@ __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I,
     s.dir = k;
     s.e0 = cvreal(ld3(I.pol_v));
     s.e1 = cvreal(ld3(I.pol_h));
-    s.phi = P.scene.ambient_n * dot(k, p);
+    s.phi = make_nt<NT>(P.scene.ambient_n * dot(k, p), 0.0);  // lossless ambient (validated)
     s.prob = 1.0;
     s.weight = 1.0;
-    s.medium_n = P.scene.ambient_n;
+    s.medium_n = make_nt<NT>(P.scene.ambient_n, 0.0);
     s.bounce = 0;
     s.cell = cell;
     s.sample = sample;
@@ -377,6 +405,8 @@ __device__ __forceinline__ void store_cv(double* p, const CV3& v) {
 __device__ __forceinline__ double shfl_d(double v, int src) {
     return __shfl_sync(kFull, v, src);
 }
+__device__ __forceinline__ double shfl_nt(double v, int src) { return shfl_d(v, src); }
+__device__ __forceinline__ Cx shfl_nt(Cx v, int src) { return {shfl_d(v.re, src), shfl_d(v.im, src)}; }
 
 // ---------------------------------------------------------------------------
 // the path kernel
@@ -395,9 +425,10 @@ enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
-template <int kMode, bool kDiel>
+template <int kMode, bool kDiel, bool kLossy>
 __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeSmem;
+    using NT = typename std::conditional<kLossy, Cx, double>::type;
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
     __shared__ unsigned long long s_cnt[kCntWords];
     // per-bounce counters as native 32-bit shared atomics (ATOMS.ADD); the
@@ -454,11 +485,11 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         bool alive = false;  // lane holds a path (possibly only its last occlusion query)
         bool pend = false;   // next query is the chi occlusion test of a contribution
         bool dying = false;  // the path ends once its pending occlusion test is done
-        Path s;
+        Path<NT> s;
         Cx amp[4];           // contribution: receiver-projected amplitudes (slot while pending)
-        double s_path = 0.0; //               and net optical path
+        NT s_path{};         //               and net optical path
         CV3 fj0, fm0, fj1, fm1;  // fan mode: the contribution's currents,
-        double fphi = 0.0;       // optical path
+        NT fphi{};               // optical path
         V3 fpt = {0.0, 0.0, 0.0};  // and exit point, broadcast to the warp
 
         // One query per lane per iteration: either the path's next closest
@@ -501,7 +532,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 if (visible) {  // the queued contribution's amplitudes come back from the slot
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) amp[ch] = sl.getc(kFAmp + 2 * ch);
-                    s_path = sl.get(kFSPath);
+                    s_path = slot_get_nt<NT>(sl, kFSPath, kFSPathIm);
                 }
                 if (dying) {
                     alive = false;
@@ -514,9 +545,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 } else {
                     load_em(sl, s);
                     const V3 point = s.origin + s.dir * t;
-                    const HitInfo h = fill_hit(S, id, s.dir);
-                    // advance (path_engine.cpp:17-21)
-                    s.phi += s.medium_n * t;
+                    const HitInfo<NT> h = fill_hit<NT>(S, id, s.dir);
+                    // advance (path_engine.cpp:17-21); complex in lossy media
+                    s.phi = s.phi + s.medium_n * t;
                     s.origin = point;
                     s.bounce += 1;
                     max_round = max(max_round, s.bounce);
@@ -534,10 +565,11 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         // scene creation), so far_side_pec always holds and the
                         // dielectric code (and its registers) is compiled out.
                         const bool pec = kDiel ? h.far_side_pec : true;
-                        const double n1 = s.medium_n;
-                        const double n2 = pec ? n1 : h.n_transmit;
-                        const Coeffs co = pec ? coeffs_pec() : fresnel(n1, n2, cos_i, fault);
-                        const Basis b = sp_basis(s.dir, h.normal, n1, n2, !pec, fault);
+                        const NT n1 = s.medium_n;
+                        const NT n2 = pec ? n1 : h.n_transmit;
+                        const Coeffs co = pec ? coeffs_pec() : fresnel_any(n1, n2, cos_i, fault);
+                        // ray geometry from the real parts (exact for the lossless model)
+                        const Basis b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), !pec, fault);
                         const CV3 er0 = interface_transform(s.e0, 0, co, b, fault);
                         const CV3 er1 = interface_transform(s.e1, 0, co, b, fault);
                         const bool two = !pec && !co.tir;
@@ -593,7 +625,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                                 store_cv(&scratch->a_m[0][0][0], m0);
                                 store_cv(&scratch->a_j[1][0][0], j1);
                                 store_cv(&scratch->a_m[1][0][0], m1);
-                                scratch->phi_total = s.phi;
+                                scratch->phi_total = re_of(s.phi);
                                 scratch->exit_point[0] = point.x;
                                 scratch->exit_point[1] = point.y;
                                 scratch->exit_point[2] = point.z;
@@ -666,7 +698,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         pend = true;
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) sl.setc(kFAmp + 2 * ch, amp[ch]);
-                        sl.set(kFSPath, s_path);
+                        slot_set_nt(sl, kFSPath, kFSPathIm, s_path);
                         if (!alive) {
                             alive = true;
                             dying = true;
@@ -701,14 +733,14 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         c[k].z.re = shfl_d(c[k].z.re, src);
                         c[k].z.im = shfl_d(c[k].z.im, src);
                     }
-                    const double ph = shfl_d(fphi, src);
+                    const NT ph = shfl_nt(fphi, src);
                     const V3 pt = {shfl_d(fpt.x, src), shfl_d(fpt.y, src), shfl_d(fpt.z, src)};
                     if (has_rx) {
                         // project first: only 4 complex amplitudes + s stay live
                         // across this receiver's occlusion traversal
                         Cx am[4];
                         project(R, c[0], c[1], c[2], c[3], am);
-                        const double sp = ph - dot(ks, pt);
+                        const NT sp = ph - dot(ks, pt);
                         bool vis = true;
                         if (P.occlusion) {
                             double t2;
@@ -718,19 +750,13 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         }
                         if (vis) {
                             ++n_contrib;
-                            double sn, cs;
-                            sincos(-P.k0[0] * sp, &sn, &cs);
-                            acc_add(sl, am, Cx{cs, sn});
+                            acc_add(sl, am, phasor(P.k0[0], sp));
                         }
                     }
                 }
             } else if (kRegAcc) {
                 // ---- phasor accumulation (farfield.cpp:130-146) ----
-                if (visible) {
-                    double sn, cs;
-                    sincos(-P.k0[0] * s_path, &sn, &cs);
-                    acc_add(sl, amp, Cx{cs, sn});
-                }
+                if (visible) acc_add(sl, amp, phasor(P.k0[0], s_path));
             } else {
                 unsigned vm = __ballot_sync(kFull, visible);
                 while (vm) {
@@ -742,11 +768,9 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         am[ch].re = shfl_d(amp[ch].re, src);
                         am[ch].im = shfl_d(amp[ch].im, src);
                     }
-                    const double sp = shfl_d(s_path, src);
+                    const NT sp = shfl_nt(s_path, src);
                     for (uint32_t f = lane; f < P.nf; f += 32) {
-                        double sn, cs;
-                        sincos(-P.k0[f] * sp, &sn, &cs);
-                        const Cx z = {cs, sn};
+                        const Cx z = phasor(P.k0[f], sp);
                         double* slot = wacc + f * 8;
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
@@ -853,40 +877,43 @@ bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
 
 bool trace_fan_supported(uint32_t nf) { return nf == 1; }
 
-template <int kMode, bool kDiel>
+template <int kMode, bool kDiel, bool kLossy>
 static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
                                cudaStream_t stream) {
+    auto* k = path_kernel<kMode, kDiel, kLossy>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(path_kernel<kMode, kDiel>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
     int per_sm = 1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<kMode, kDiel>, threads, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
     const uint64_t max_blocks = (p.total_tiles + threads / 32 - 1) / (threads / 32);
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    path_kernel<kMode, kDiel><<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
+    k<<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
     return cudaGetLastError();
+}
+
+template <bool kDiel, bool kLossy>
+static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int threads, size_t smem,
+                               cudaStream_t stream) {
+    return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy>(p, sms, threads, smem, stream)
+           : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy>(p, sms, threads, smem, stream)
+                              : launch_mode<kModeSmem, kDiel, kLossy>(p, sms, threads, smem, stream);
 }
 
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
     const int mode = p.fan ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
     const size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
-    cudaError_t e;
-    if (p.scene.all_pec) {
-        e = mode == kModeFan   ? launch_mode<kModeFan, false>(p, device_sms, threads, smem, stream)
-            : mode == kModeReg ? launch_mode<kModeReg, false>(p, device_sms, threads, smem, stream)
-                               : launch_mode<kModeSmem, false>(p, device_sms, threads, smem, stream);
-    } else {
-        e = mode == kModeFan   ? launch_mode<kModeFan, true>(p, device_sms, threads, smem, stream)
-            : mode == kModeReg ? launch_mode<kModeReg, true>(p, device_sms, threads, smem, stream)
-                               : launch_mode<kModeSmem, true>(p, device_sms, threads, smem, stream);
-    }
+    // three physics instantiations: all-PEC (dielectric code compiled out),
+    // the reference's lossless dielectric model (bit-exact), lossy media
+    cudaError_t e = p.scene.lossy     ? launch_kind<true, true>(mode, p, device_sms, threads, smem, stream)
+                    : p.scene.all_pec ? launch_kind<false, false>(mode, p, device_sms, threads, smem, stream)
+                                      : launch_kind<true, false>(mode, p, device_sms, threads, smem, stream);
     if (launches) ++*launches;
     return e;
 }
