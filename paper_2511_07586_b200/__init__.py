@@ -5,7 +5,7 @@ and solver types mirror the reference headers; all per-ray work runs in the
 hand-written sm_100a CUDA kernels of ``libmcsbr_gpu.so`` (C ABI in
 include/mcsbr_gpu.h).
 """
-from .geometry import (SceneData, SceneError, Material, load_scene, load_scene_files,
+from .geometry import (SceneData, SceneError, Material, load_scene, load_scene_files, airframe,
                        builtin_scene, builtin_scene_names, make_builtin_scene, dihedral_grid,
                        coated_sphere, MeshBuilder)
 from .solver import (Scene, Excitation, monostatic_excitation, bistatic_excitation, McConfig,
@@ -14,7 +14,7 @@ from .solver import (Scene, Excitation, monostatic_excitation, bistatic_excitati
                      launch_rect, rcs_m2, VV, HH, VH, HV, K_SPEED_OF_LIGHT)
 
 __all__ = [
-    "SceneData", "SceneError", "Material", "load_scene", "load_scene_files", "builtin_scene",
+    "SceneData", "SceneError", "Material", "load_scene", "load_scene_files", "airframe", "builtin_scene",
     "builtin_scene_names", "make_builtin_scene", "dihedral_grid", "coated_sphere", "MeshBuilder",
     "Scene", "Excitation", "monostatic_excitation", "bistatic_excitation", "McConfig",
     "RouletteConfig", "BranchStrategy", "RngMode", "SweepResult", "RunStats", "McResult",

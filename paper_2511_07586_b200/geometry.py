@@ -589,6 +589,237 @@ def dihedral_grid(size_m: float = 0.5, n: int = 64) -> tuple[str, str]:
     return m.to_obj(), materials_json('    "plates": {"front": "air", "back": "metal"}')
 
 
+def scene_from_arrays(vertices: np.ndarray, faces: np.ndarray, face_region: np.ndarray,
+                      regions: list[tuple[str, str]], materials: dict,
+                      ambient: str = "air") -> SceneData:
+    """Build a SceneData straight from arrays (large generated meshes), with
+    the same semantics as load_scene: materials ordered ambient-first then by
+    sorted name (nlohmann std::map order), normals cross(b-a, c-a)/|.|,
+    degenerate-triangle rejection, exterior flags and the dielectric parity
+    walk (geometry_io.cpp:101-191).
+
+    faces: (nt, 3) vertex indices; face_region: (nt,) index into `regions`,
+    a list of (front_material, back_material) names; materials: name ->
+    dict(eps_r=, mu_r=, eps_i=, pec=)."""
+    names = [ambient] + sorted(k for k in materials if k != ambient)
+    ids = {n: i for i, n in enumerate(names)}
+    mats = []
+    for n in names:
+        spec = materials[n]
+        m = Material(is_pec=bool(spec.get("pec", False)))
+        if not m.is_pec:
+            m.eps_r = float(spec.get("eps_r", 1.0))
+            m.mu_r = float(spec.get("mu_r", 1.0))
+            m.eps_i = float(spec.get("eps_i", 0.0))
+        mats.append(m)
+    verts = np.ascontiguousarray(vertices, dtype=np.float64)
+    f = np.ascontiguousarray(faces, dtype=np.uint32)
+    nt = len(f)
+    reg = np.array([(ids[a], ids[b]) for a, b in regions], dtype=np.uint16).reshape(-1, 2)
+    fr = reg[np.asarray(face_region)]
+    tris = np.zeros(nt, dtype=TRIANGLE_DTYPE)
+    nx, ny, nz, area2 = triangle_normals(verts, f[:, 0], f[:, 1], f[:, 2])
+    bad = np.nonzero(area2 < 1e-12)[0]
+    if len(bad):
+        raise SceneError(f"degenerate triangle {int(bad[0])}")
+    tris["v0"], tris["v1"], tris["v2"] = f[:, 0], f[:, 1], f[:, 2]
+    tris["normal"][:, 0] = nx / area2
+    tris["normal"][:, 1] = ny / area2
+    tris["normal"][:, 2] = nz / area2
+    tris["front_material"] = fr[:, 0]
+    tris["back_material"] = fr[:, 1]
+    tris["exterior_facing"] = ((fr[:, 0] == 0) | (fr[:, 1] == 0)).astype(np.uint8)
+    for mid in range(1, len(mats)):
+        if not mats[mid].is_pec:
+            _check_region_parity(tris, mid, names[mid])
+    mat_arr = np.zeros(len(mats), dtype=MATERIAL_DTYPE)
+    for i, m in enumerate(mats):
+        mat_arr[i]["eps_r"], mat_arr[i]["mu_r"], mat_arr[i]["is_pec"] = m.eps_r, m.mu_r, int(m.is_pec)
+    eps_i = np.array([m.eps_i for m in mats])
+    sd = SceneData(vertices=verts, triangles=tris, materials=mat_arr, material_names=names,
+                   eps_imag=eps_i if np.any(eps_i != 0.0) else None)
+    return sd.finalize()
+
+
+def scene_to_text(sd: SceneData) -> tuple[str, str]:
+    """Export a SceneData as OBJ + material-map JSON in the reference's formats
+    (geometry_io.cpp:23-160): one OBJ group per (front, back) material pair,
+    vertices printed with %.17g so they round-trip exactly."""
+    tr = sd.triangles
+    pairs = np.stack([tr["front_material"], tr["back_material"]], 1).astype(np.int64)
+    uniq, inv = np.unique(pairs, axis=0, return_inverse=True)
+    inv = inv.reshape(-1)
+    lines = ["v %s %s %s\n" % (_g17(x), _g17(y), _g17(z)) for x, y, z in sd.vertices]
+    order = np.argsort(inv, kind="stable")
+    cur = -1
+    f = np.stack([tr["v0"], tr["v1"], tr["v2"]], 1).astype(np.int64) + 1
+    for i in order:
+        if inv[i] != cur:
+            cur = int(inv[i])
+            lines.append(f"g r{cur}\n")
+        lines.append(f"f {f[i, 0]} {f[i, 1]} {f[i, 2]}\n")
+    names = sd.material_names
+    mats = {}
+    for i, n in enumerate(names):
+        m = sd.materials[i]
+        if m["is_pec"]:
+            mats[n] = {"pec": True}
+        else:
+            mats[n] = {"eps_r": float(m["eps_r"]), "mu_r": float(m["mu_r"])}
+            if sd.eps_imag is not None and sd.eps_imag[i] != 0.0:
+                mats[n]["eps_i"] = float(sd.eps_imag[i])
+    regions = {f"r{k}": {"front": names[a], "back": names[b]} for k, (a, b) in enumerate(uniq)}
+    mm = json.dumps({"ambient": names[0], "materials": mats, "regions": regions}, indent=1)
+    return "".join(lines), mm
+
+
+def _extrude(loops: np.ndarray, cap: bool = True):
+    """Closed surface through a sequence of closed cross-section loops.
+
+    loops: (S, L, 3) -- S stations along the part, L points per closed loop
+    (listed so that the loop turns counter-clockwise seen from the last
+    station looking back).  Quads join consecutive stations, fans close both
+    ends.  Vertices are shared, so the surface is a closed, consistently
+    oriented manifold (outward normals)."""
+    S, L, _ = loops.shape
+    v = loops.reshape(-1, 3)
+    idx = np.arange(S * L).reshape(S, L)
+    a = idx[:-1, :]
+    b = idx[:-1, np.r_[1:L, 0]]
+    c = idx[1:, np.r_[1:L, 0]]
+    d = idx[1:, :]
+    quads = np.stack([a, b, c, d], -1).reshape(-1, 4)
+    faces = [np.stack([quads[:, 0], quads[:, 2], quads[:, 1]], 1),
+             np.stack([quads[:, 0], quads[:, 3], quads[:, 2]], 1)]
+    extra = []
+    if cap:
+        c0 = loops[0].mean(axis=0)
+        c1 = loops[-1].mean(axis=0)
+        i0, i1 = S * L, S * L + 1
+        extra = [c0, c1]
+        r = np.arange(L)
+        rn = np.r_[1:L, 0]
+        faces.append(np.stack([np.full(L, i0), idx[0, r], idx[0, rn]], 1))
+        faces.append(np.stack([np.full(L, i1), idx[-1, rn], idx[-1, r]], 1))
+    verts = np.concatenate([v, np.array(extra).reshape(-1, 3)]) if extra else v
+    return verts, np.concatenate(faces).astype(np.int64)
+
+
+def _slab_loops(stations: np.ndarray, le_x: np.ndarray, chord: np.ndarray, pos: np.ndarray,
+                thick: float, n_chord: int, axis: str) -> np.ndarray:
+    """Rectangular slab cross-sections (chord x thickness) at span stations.
+    axis 'y': wing (span along y, thickness along z); 'z': fin (span along z,
+    thickness along y)."""
+    S = len(stations)
+    u = np.linspace(0.0, 1.0, n_chord + 1)
+    # loop: top from trailing to leading edge, then bottom from leading to trailing
+    xs_top = le_x[:, None] - (1.0 - u)[None, :] * chord[:, None]
+    xs_bot = le_x[:, None] - u[None, :] * chord[:, None]
+    xs = np.concatenate([xs_top, xs_bot[:, 1:-1]], axis=1)
+    hs = np.concatenate([np.full(n_chord + 1, 0.5 * thick), np.full(n_chord - 1, -0.5 * thick)])
+    L = xs.shape[1]
+    out = np.zeros((S, L, 3))
+    out[..., 0] = xs
+    if axis == "y":
+        out[..., 1] = pos[:, None]
+        out[..., 2] = hs[None, :]
+    else:
+        out[..., 2] = pos[:, None]
+        out[..., 1] = hs[None, :]
+    return out
+
+
+def airframe(target_triangles: int = 200_000, seed: int = 4, dielectric_skin: bool = False):
+    """Procedural airframe (BASELINE configs 4/5): a capped
+    cylindrical fuselage 12 m long, 1.5 m diameter, along x (nose at +x); two
+    swept trapezoidal slab wings, 10 m span, 3 m root / 1 m tip chord; a
+    vertical fin 2 m tall.  dielectric_skin: wings and fin get a 2 mm
+    eps 3.5-0.05j skin over a 4 mm eps 10-1.0j skin on a PEC core (three
+    nested closed surfaces per part); the fuselage stays PEC.  `seed` makes
+    a deterministic ±1 mm panel perturbation of the fuselage interior rings.
+    Returns (SceneData, info)."""
+    rng = np.random.default_rng(seed)
+    n_skin = 3 if dielectric_skin else 1
+
+    def count(sc):
+        n_th, n_x = max(16, int(round(128 * sc))), max(8, int(round(390 * sc)))
+        n_c, n_s = max(6, int(round(60 * sc))), max(4, int(round(150 * sc)))
+        n_fc, n_fs = max(6, int(round(40 * sc))), max(4, int(round(60 * sc)))
+        return (2 * n_th * n_x + 2 * n_th + n_skin * (2 * (4 * n_c * n_s + 4 * n_c)
+                                                      + 4 * n_fc * n_fs + 4 * n_fc))
+
+    scale = np.sqrt(target_triangles / 200_000.0)
+    for _ in range(3):  # refine the grid scale so the mesh lands near the target
+        scale *= np.sqrt(target_triangles / count(scale))
+    parts_v, parts_f, parts_r = [], [], []
+    regions: list[tuple[str, str]] = []
+
+    def add(v, f, region):
+        if region not in regions:
+            regions.append(region)
+        off = sum(len(x) for x in parts_v)
+        parts_v.append(v)
+        parts_f.append(f + off)
+        parts_r.append(np.full(len(f), regions.index(region)))
+
+    # fuselage: circle loops in the yz plane, stations along x (tail -> nose)
+    n_th = max(16, int(round(128 * scale)))
+    n_x = max(8, int(round(390 * scale)))
+    x = np.linspace(-6.0, 6.0, n_x + 1)
+    th = np.linspace(0.0, 2 * np.pi, n_th, endpoint=False)
+    r = 0.75 * np.ones((n_x + 1, n_th))
+    r[1:-1] += rng.uniform(-1e-3, 1e-3, size=(n_x - 1, n_th))
+    loops = np.zeros((n_x + 1, n_th, 3))
+    loops[..., 0] = x[:, None]
+    loops[..., 1] = r * np.cos(th)[None, :]
+    loops[..., 2] = r * np.sin(th)[None, :]
+    v, f = _extrude(loops[:, ::-1, :])  # outward normals
+    add(v, f, ("air", "metal"))
+
+    skins = [(0.0, ("skin_in", "metal"))]
+    if dielectric_skin:
+        skins = [(0.0, ("skin_in", "metal")), (0.004, ("skin_out", "skin_in")),
+                 (0.006, ("air", "skin_out"))]
+    else:
+        skins = [(0.0, ("air", "metal"))]
+
+    n_c = max(6, int(round(60 * scale)))
+    n_s = max(4, int(round(150 * scale)))
+    for side in (1.0, -1.0):  # wings
+        s = np.linspace(0.0, 1.0, n_s + 1)
+        y0, y1 = 0.5, 5.0  # root buried in the fuselage (radius 0.75), tip at half span
+        pos = side * (y0 + (y1 - y0) * s)
+        chord_c = 3.0 - 2.0 * s
+        le_c = 1.5 - 1.6 * s  # swept leading edge
+        for off, reg in skins:
+            lo = _slab_loops(s, le_c + off, chord_c + 2 * off, pos, 0.10 + 2 * off, n_c, "y")
+            if side > 0:
+                lo = lo[:, ::-1, :]  # keep outward orientation on the +y wing
+            v, f = _extrude(lo)
+            add(v, f, reg)
+    # vertical fin at the tail
+    n_fc = max(6, int(round(40 * scale)))
+    n_fs = max(4, int(round(60 * scale)))
+    s = np.linspace(0.0, 1.0, n_fs + 1)
+    pos = 0.5 + 2.25 * s  # from inside the fuselage to 2 m above its top (0.75)
+    chord_f = 2.2 - 1.2 * s
+    le_f = -3.8 - 1.0 * s
+    for off, reg in skins:
+        lo = _slab_loops(s, le_f + off, chord_f + 2 * off, pos, 0.08 + 2 * off, n_fc, "z")
+        v, f = _extrude(lo)
+        add(v, f, reg)
+
+    verts = np.concatenate(parts_v)
+    faces = np.concatenate(parts_f)
+    fr = np.concatenate(parts_r)
+    mats = {"air": {"eps_r": 1.0}, "metal": {"pec": True}}
+    if dielectric_skin:
+        mats["skin_out"] = {"eps_r": 3.5, "eps_i": 0.05}
+        mats["skin_in"] = {"eps_r": 10.0, "eps_i": 1.0}
+    sd = scene_from_arrays(verts, faces, fr, regions, mats)
+    return sd, {"triangles": len(faces), "vertices": len(verts), "regions": regions}
+
+
 def coated_sphere(core_r: float = 0.5, t_inner: float = 0.010, t_outer: float = 0.005,
                   eps_inner: complex = 4.0 - 0.1j, eps_outer: complex = 2.2 - 0.01j,
                   subdivisions: int = 5, lossless: bool = False) -> tuple[str, str]:

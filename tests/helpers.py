@@ -58,4 +58,16 @@ def parity_cases():
     cases.append(("coated_sphere_lossless", coat, M.bistatic_excitation(90.0, 0.0, 60.0, 0.0), [3e9],
                   M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, seed=3, max_bounce=16,
                              roulette=M.RouletteConfig(enabled=True, min_bounce=3))))
+    from paper_2511_07586_b200.geometry import airframe
+
+    af, _ = airframe(6_000, seed=4)
+    cases.append(("airframe_pec_isar", af, M.monostatic_excitation(90.0, 2.0),
+                  np.linspace(9.5e9, 10.5e9, 8),
+                  M.McConfig(strata_per_wavelength=1.0, samples_per_stratum=1, seed=4, max_bounce=10)))
+    skin, _ = airframe(6_000, seed=5, dielectric_skin=True)
+    skin.eps_imag = None  # the reference's real-permittivity model of the c5 skins
+    cases.append(("airframe_skin_lossless", skin, M.monostatic_excitation(80.0, -3.0),
+                  np.linspace(8e9, 12e9, 4),
+                  M.McConfig(strata_per_wavelength=0.7, samples_per_stratum=1, seed=5, max_bounce=24,
+                             roulette=M.RouletteConfig(enabled=True, min_bounce=3))))
     return cases

@@ -104,6 +104,43 @@ def test_generators_sizes():
     assert sd.eps_imag is not None and sd.eps_imag.max() == pytest.approx(0.1)
 
 
+def test_airframe_generator_c4_c5():
+    """BASELINE configs 4/5 geometry: triangle budgets, closed consistently
+    oriented dielectric skins (the loader's parity walk), outward normals."""
+    from paper_2511_07586_b200.geometry import airframe
+
+    sd, info = airframe(200_000, seed=4)
+    assert abs(info["triangles"] - 200_000) < 5_000
+    assert sd.material_names == ["air", "metal"] and sd.eps_imag is None
+    assert 6.0 < sd.bounding_radius < 6.5  # 12 m fuselage dominates
+    sd5, info5 = airframe(1_000_000, seed=5, dielectric_skin=True)
+    assert abs(info5["triangles"] - 1_000_000) < 25_000
+    assert sd5.material_names == ["air", "metal", "skin_in", "skin_out"]
+    assert np.allclose(sd5.eps_imag, [0, 0, 1.0, 0.05])
+    # deterministic in the seed, different across seeds
+    a, _ = airframe(20_000, seed=4)
+    b, _ = airframe(20_000, seed=4)
+    c, _ = airframe(20_000, seed=5)
+    assert a.vertices.tobytes() == b.vertices.tobytes()
+    assert a.vertices.tobytes() != c.vertices.tobytes()
+
+
+def test_scene_text_roundtrip():
+    """scene_to_text output reloads through the (reference-compatible) loader
+    to the identical scene."""
+    from paper_2511_07586_b200.geometry import airframe, scene_to_text
+
+    sd, _ = airframe(6_000, seed=5, dielectric_skin=True)
+    obj, mm = scene_to_text(sd)
+    sd2 = M.load_scene(obj, mm)
+    assert sd2.vertices.tobytes() == sd.vertices.tobytes()
+    assert sd2.material_names == sd.material_names
+    key = lambda t: np.lexsort((t["v2"], t["v1"], t["v0"]))  # noqa: E731
+    t1, t2 = sd.triangles[key(sd.triangles)], sd2.triangles[key(sd2.triangles)]
+    assert t1.tobytes() == t2.tobytes()
+    assert np.array_equal(sd2.eps_imag, sd.eps_imag)
+
+
 def test_excitation_bases():
     """solver_common.cpp:15-49: V = theta_hat, H = phi_hat, k_inc = -r_hat."""
     e = M.monostatic_excitation(90.0, 0.0)

@@ -197,7 +197,11 @@ def test_loader_and_builtins_byte_identical_to_reference():
         assert mats.tobytes() == sd.materials.tobytes()
         assert b5.tobytes() == np.r_[sd.bounding_center, sd.bounding_radius, sd.diameter].tobytes()
     # the config generators load in the reference loader too (parity walk etc.)
-    for obj, mm in [M.dihedral_grid(0.5, 8), M.coated_sphere(subdivisions=2, lossless=True)]:
+    from paper_2511_07586_b200.geometry import airframe, scene_to_text
+
+    small_airframe = scene_to_text(airframe(6_000, seed=5, dielectric_skin=True)[0])
+    for obj, mm in [M.dihedral_grid(0.5, 8), M.coated_sphere(subdivisions=2, lossless=True),
+                    small_airframe]:
         h = L.ref_scene_load(obj.encode(), mm.encode())
         assert h, L.ref_last_error()
         L.ref_scene_free(h)
