@@ -881,7 +881,7 @@ template <int kMode, bool kDiel, bool kLossy>
 static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
                                cudaStream_t stream) {
     auto* k = path_kernel<kMode, kDiel, kLossy>;
-    if (smem > 48 * 1024) {
+    if (smem > 0) {  // static state slots + dynamic accumulators may pass 48 KB: opt in
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
