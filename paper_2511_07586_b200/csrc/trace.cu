@@ -150,8 +150,27 @@ __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, 
 // Any hit (kAny = true): Scene::occluded semantics, geometry.cpp:242-244.
 // One runtime-flagged routine (not two template copies) so the path kernel
 // has a single traversal loop in its instruction stream.
+#ifdef MCSBR_TRAVERSAL_STATS
+// diagnostic build only (tools/build_variants.py --stats): per-thread node-visit
+// and triangle-test counts, flushed into counter words 240/241
+__device__ unsigned long long g_visits[2];
+#define MCSBR_STAT(i) (++tstat[i])
+#else
+#define MCSBR_STAT(i) ((void)0)
+#endif
+
 __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
                                          uint32_t& best_id, uint32_t& fault, bool kAny, bool outside) {
+#ifdef MCSBR_TRAVERSAL_STATS
+    uint32_t tstat[2] = {0, 0};
+    struct Flush {
+        uint32_t* s;
+        __device__ ~Flush() {
+            atomicAdd(&g_visits[0], static_cast<unsigned long long>(s[0]));
+            atomicAdd(&g_visits[1], static_cast<unsigned long long>(s[1]));
+        }
+    } flush_{tstat};
+#endif
     const FRay r = make_fray(S, o, d, outside);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
     best_id = 0xffffffffu;
@@ -162,6 +181,7 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
     for (;;) {
         if (ref >= 0) {
             // 4-wide node: 128 B, boxes SoA by axis (bvh.cu emit4_kernel)
+            MCSBR_STAT(0);
             const float4* nd = S.nodes + 8ll * ref;
             const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
             const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5), rf = __ldg(nd + 6), nc = __ldg(nd + 7);
@@ -203,6 +223,7 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             for (uint32_t k = 0; k < count; ++k) {
                 double t;
                 uint32_t id;
+                MCSBR_STAT(1);
                 if (tri_test(S.tri64 + 5ull * (first + k), o, d, t_min, t, id)) {
                     if (t < best_t || (t == best_t && id < best_id)) {
                         best_t = t;
@@ -917,6 +938,13 @@ cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stre
     if (launches) ++*launches;
     return e;
 }
+
+#ifdef MCSBR_TRAVERSAL_STATS
+extern "C" __attribute__((visibility("default"))) void mcsbr_gpu_stats_visits(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_visits, sizeof(g_visits));
+}
+#endif
 
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d, const double* tmin,
                              uint32_t n, int any_hit, double* t_out, uint32_t* id_out,

@@ -7,18 +7,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2511_07586_b200 import build as B  # noqa: E402
 
-for mb in [int(x) for x in sys.argv[1:]] or [1, 2, 3, 4]:
+stats = "--stats" in sys.argv
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+for mb in [int(x) for x in args] or [1, 2, 3, 4]:
     objs = []
+    extra = ["-DMCSBR_TRAVERSAL_STATS"] if stats else []
     for src in B.SOURCES:
         obj = f"/tmp/v{mb}_{src}.o"
-        r = subprocess.run([B.NVCC, *B.FLAGS, f"-DMCSBR_MIN_BLOCKS={mb}", "-c", os.path.join(B.CSRC, src),
-                            "-o", obj], capture_output=True, text=True)
+        r = subprocess.run([B.NVCC, *B.FLAGS, *extra, f"-DMCSBR_MIN_BLOCKS={mb}", "-c",
+                            os.path.join(B.CSRC, src), "-o", obj], capture_output=True, text=True)
         if r.returncode:
             sys.exit(r.stderr[-3000:])
         if src == "trace.cu":
             print(mb, [l.strip() for l in r.stderr.splitlines() if "registers" in l][-3:])
         objs.append(obj)
-    out = os.path.join(B.HERE, f"libmcsbr_gpu_v{mb}.so")
+    out = os.path.join(B.HERE, "libmcsbr_gpu_stats.so" if stats else f"libmcsbr_gpu_v{mb}.so")
     subprocess.run([B.NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs,
                     "-Xcompiler", "-fPIC", "-Xlinker", "--exclude-libs,ALL", "-Xlinker", "-Bsymbolic",
                     "-lcudart_static", "-lrt", "-lpthread", "-ldl"], check=True)
