@@ -342,23 +342,36 @@ def main():
             traffic = None
 
     # ---- e2e: public C ABI from host buffers (scene upload + BVH + sweep + readback) ----
-    e2e_value, h2d, d2h = None, 0, 0
-    if rank == 0:
-        e2e_t = []
-        for k in range(max(args.steps, 1) + 1):
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            s2 = M.Scene(sd, device=local)
-            vals, st2 = M.estimate_batch(s2, [(e, s) for e, s in zip(excs, spws)],
-                                         [[e] for e in excs], freqs, cfg)
-            s2.close()
-            t1 = time.perf_counter()
-            if k > 0:
-                e2e_t.append(t1 - t0)
-        e2e_value = st2.rays_launched / (sum(e2e_t) / len(e2e_t))
-        h2d = (sd.vertices.nbytes + sd.triangles.nbytes + sd.materials.nbytes
-               + C.sizeof(incs) + C.sizeof(rxs) + freqs.nbytes)
-        d2h = vals.nbytes // 2 * 2 + A.MCSBR_COUNTER_WORDS * 8
+    # N = 1: solver.estimate_batch (the drop-in batch call); N > 1: every rank
+    # runs distributed.sweep_sharded (its shard + NCCL all-reduce + finalize);
+    # per step the time is the max over ranks.
+    from paper_2511_07586_b200 import distributed as D
+
+    e2e_t = []
+    inc_list = [(e, s) for e, s in zip(excs, spws)]
+    rx_list = [[e] for e in excs]
+    for k in range(max(args.steps, 1) + 1):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        s2 = M.Scene(sd, device=local)
+        if world > 1:
+            vals, st2 = D.sweep_sharded(s2, inc_list, rx_list, freqs, cfg)
+        else:
+            vals, st2 = M.estimate_batch(s2, inc_list, rx_list, freqs, cfg)
+        s2.close()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        if k > 0:
+            e2e_t.append(dt)
+    e2e_value = st2.rays_launched / (sum(e2e_t) / len(e2e_t))
+    h2d = (sd.vertices.nbytes + sd.triangles.nbytes + sd.materials.nbytes
+           + C.sizeof(incs) + C.sizeof(rxs) + freqs.nbytes)
+    d2h = vals.nbytes + A.MCSBR_COUNTER_WORDS * 8
 
     cpu = None
     rcs_err = None

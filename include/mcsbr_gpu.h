@@ -264,6 +264,28 @@ MCSBR_API int mcsbr_gpu_finalize(const double* raw_sums, uint32_t n, const doubl
 /* Decode a counter block (device layout above, copied to host) into stats. */
 MCSBR_API int mcsbr_gpu_decode_counters(const uint64_t* counters, mcsbr_stats* stats);
 
+/* ---- radar products (reference proj/src/signal_processing.cpp) ----
+ * Computed on the current CUDA device from host arrays.  Errors mirror the
+ * reference's SignalError messages (MCSBR_EINVAL). */
+#define MCSBR_WINDOW_NONE 0
+#define MCSBR_WINDOW_HANN 1
+
+/* range_profile (signal_processing.cpp:66-89): windowed, zero-padded inverse
+ * DFT of one channel's sweep (values: nf complex), centre-shifted; outputs
+ * nf*zero_pad range bins (m) and 20 log10 |.|. */
+MCSBR_API int mcsbr_gpu_range_profile(const double* values, const double* frequencies,
+                                      uint32_t n_frequencies, int window, int zero_pad,
+                                      double* range_m, double* mag_db, double* bin_spacing);
+
+/* isar (signal_processing.cpp:91-162): small-angle range-Doppler image from
+ * one channel's sweeps over a uniform azimuth grid (values: [na][nf]
+ * complex).  Outputs down_range_m[nf*zp], cross_range_m[na*zp],
+ * mag_db[(nf*zp) x (na*zp)] row-major (clipped at peak + floor), *peak_db. */
+MCSBR_API int mcsbr_gpu_isar(const double* values, const double* frequencies, uint32_t n_frequencies,
+                             const double* angles_deg, uint32_t n_angles, int window, int zero_pad,
+                             double dynamic_floor_db, double* down_range_m, double* cross_range_m,
+                             double* mag_db, double* peak_db);
+
 /* Parity instrumentation: run mcsbr_gpu_estimate and record, for launch
  * entries [0, n_paths) of the incidence, the triangle id of every hit
  * (tri_ids[p*stride + k] for hit k, 0xFFFFFFFF past the end), the

@@ -83,6 +83,9 @@ def ref() -> C.CDLL:
                                    C.POINTER(A.McConfigC), C.c_int, _DP, C.POINTER(A.Stats),
                                    C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.ref_slab_reflection.argtypes = [_DP, _DP, C.c_int, C.c_double, C.c_int, _DP]
+        L.ref_range_profile.argtypes = [_DP, _DP, C.c_uint32, C.c_int, C.c_int, _DP, _DP, _DP]
+        L.ref_isar.argtypes = [_DP, _DP, C.c_uint32, _DP, C.c_uint32, C.c_int, C.c_int, C.c_double,
+                               _DP, _DP, _DP, _DP]
         L.ref_plate_rcs.restype = C.c_double
         L.ref_plate_rcs.argtypes = [C.c_double] * 3
         L.ref_sphere_go_rcs.restype = C.c_double

@@ -21,6 +21,7 @@
 #include "mcsbr/path_engine.hpp"
 #include "mcsbr/rng.hpp"
 #include "mcsbr/scenes.hpp"
+#include "mcsbr/signal_processing.hpp"
 #include "mcsbr/solver_common.hpp"
 #include "mcsbr/solver_mc.hpp"
 #include "mcsbr_gpu.h"
@@ -514,6 +515,53 @@ int ref_estimate(const void* sp, const mcsbr_excitation* exc, const double* freq
             std::memcpy(static_cast<void*>(contribs), collected.data(), m * sizeof(Contribution));
             if (n_contribs) *n_contribs = collected.size();
         }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// ---- radar products (signal_processing.cpp) -----------------------------------
+// values: one channel, nf complex; outputs as mcsbr_gpu_range_profile
+int ref_range_profile(const double* values, const double* freqs, uint32_t nf, int window,
+                      int zero_pad, double* range_m, double* mag_db, double* bin_spacing) {
+    try {
+        SweepResult s;
+        s.frequencies.assign(freqs, freqs + nf);
+        for (int ch = 0; ch < kPolChannelCount; ++ch) s.values[ch].assign(nf, complexd{});
+        for (uint32_t k = 0; k < nf; ++k) s.values[kVV][k] = complexd(values[2 * k], values[2 * k + 1]);
+        const RangeProfile p =
+            range_profile(s, kVV, window == MCSBR_WINDOW_HANN ? Window::kHann : Window::kNone, zero_pad);
+        for (size_t i = 0; i < p.range_m.size(); ++i) {
+            range_m[i] = p.range_m[i];
+            mag_db[i] = p.mag_db[i];
+        }
+        *bin_spacing = p.bin_spacing;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// values: one channel, [na][nf] complex
+int ref_isar(const double* values, const double* freqs, uint32_t nf, const double* angles, uint32_t na,
+             int window, int zero_pad, double floor_db, double* down, double* cross, double* mag_db,
+             double* peak_db) {
+    try {
+        std::vector<SweepResult> sweeps(na);
+        for (uint32_t a = 0; a < na; ++a) {
+            sweeps[a].frequencies.assign(freqs, freqs + nf);
+            for (int ch = 0; ch < kPolChannelCount; ++ch) sweeps[a].values[ch].assign(nf, complexd{});
+            for (uint32_t k = 0; k < nf; ++k)
+                sweeps[a].values[kVV][k] = complexd(values[2 * (a * nf + k)], values[2 * (a * nf + k) + 1]);
+        }
+        const IsarImage img = isar(sweeps, std::vector<double>(angles, angles + na), kVV,
+                                   window == MCSBR_WINDOW_HANN ? Window::kHann : Window::kNone, zero_pad,
+                                   floor_db);
+        for (size_t i = 0; i < img.down_range_m.size(); ++i) down[i] = img.down_range_m[i];
+        for (size_t i = 0; i < img.cross_range_m.size(); ++i) cross[i] = img.cross_range_m[i];
+        for (size_t i = 0; i < img.mag_db.size(); ++i) mag_db[i] = img.mag_db[i];
+        *peak_db = img.peak_db;
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -12,6 +12,8 @@ from .solver import (Scene, Excitation, monostatic_excitation, bistatic_excitati
                      RouletteConfig, BranchStrategy, RngMode, SweepResult, RunStats, McResult,
                      LaunchRect, StrataGrid, DomainError, estimate, estimate_batch, launch_plan,
                      launch_rect, rcs_m2, VV, HH, VH, HV, K_SPEED_OF_LIGHT)
+from . import signal
+from .signal import Window, RangeProfile, IsarImage, SignalError, range_profile, isar
 
 __all__ = [
     "SceneData", "SceneError", "Material", "load_scene", "load_scene_files", "airframe", "builtin_scene",
@@ -20,4 +22,5 @@ __all__ = [
     "RouletteConfig", "BranchStrategy", "RngMode", "SweepResult", "RunStats", "McResult",
     "LaunchRect", "StrataGrid", "DomainError", "estimate", "estimate_batch", "launch_plan",
     "launch_rect", "rcs_m2", "VV", "HH", "VH", "HV", "K_SPEED_OF_LIGHT",
+    "signal", "Window", "RangeProfile", "IsarImage", "SignalError", "range_profile", "isar",
 ]

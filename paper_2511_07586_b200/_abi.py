@@ -197,6 +197,13 @@ SIGNATURES = {
         [C.c_void_p, C.POINTER(Excitation), _DP, C.c_uint32, C.POINTER(McConfigC), C.c_uint64,
          C.c_uint32, _U32P, C.POINTER(C.c_uint8), _U64P],
     ),
+    "mcsbr_gpu_range_profile": (
+        C.c_int, [_DP, _DP, C.c_uint32, C.c_int, C.c_int, _DP, _DP, _DP],
+    ),
+    "mcsbr_gpu_isar": (
+        C.c_int, [_DP, _DP, C.c_uint32, _DP, C.c_uint32, C.c_int, C.c_int, C.c_double, _DP, _DP, _DP,
+                  _DP],
+    ),
     "mcsbr_gpu_last_launch_count": (C.c_uint64, []),
 }
 

@@ -394,6 +394,7 @@ int use_device(const mcsbr_scene* s) {
 extern "C" {
 
 const char* mcsbr_gpu_last_error(void) { return g_err.c_str(); }
+void mcsbr_gpu_internal_set_error(const char* msg) { g_err = msg; }  // imaging.cu (not exported)
 int mcsbr_gpu_abi_version(void) { return MCSBR_GPU_ABI_VERSION; }
 uint64_t mcsbr_gpu_last_launch_count(void) { return g_launches; }
 

@@ -202,8 +202,51 @@ def estimate_vectors():
     return out
 
 
+def synthetic_sweeps(rng, freqs, angles, n_pts=5):
+    """Point-scatterer sweeps values[a][k] = sum_i A_i e^{-j 2 k (x_i cos t + y_i sin t)}."""
+    k = 2 * np.pi * np.asarray(freqs) / 299792458.0
+    t = np.radians(angles)
+    pts = rng.uniform(-2, 2, size=(n_pts, 2))
+    amp = rng.normal(size=n_pts) + 1j * rng.normal(size=n_pts)
+    proj = np.cos(t)[:, None] * pts[None, :, 0] + np.sin(t)[:, None] * pts[None, :, 1]  # [a][i]
+    return np.einsum("i,aik->ak", amp, np.exp(-2j * k[None, None, :] * proj[:, :, None]))
+
+
+def signal_vectors(L):
+    rng = np.random.default_rng(21)
+    dp = oracle.dp
+    out = {}
+    freqs = np.linspace(9.5e9, 10.5e9, 64)
+    for name, vals in [("rand", rng.normal(size=64) + 1j * rng.normal(size=64)),
+                       ("pts", synthetic_sweeps(rng, freqs, [0.0])[0])]:
+        for hann in (0, 1):
+            v = np.ascontiguousarray(vals.astype(np.complex128))
+            r = np.zeros(256)
+            db = np.zeros(256)
+            b = np.zeros(1)
+            assert L.ref_range_profile(dp(v.view(np.float64)), dp(freqs), 64, hann, 4, dp(r), dp(db), dp(b)) == 0
+            out[f"rp_{name}_{hann}_in"] = v
+            out[f"rp_{name}_{hann}_range"] = r
+            out[f"rp_{name}_{hann}_db"] = db
+            out[f"rp_{name}_{hann}_bin"] = b
+    out["rp_freqs"] = freqs
+    fi = np.linspace(9.5e9, 10.5e9, 32)
+    ang = np.linspace(-3.0, 3.0, 16)
+    vals = np.ascontiguousarray(synthetic_sweeps(rng, fi, ang, 6).astype(np.complex128))
+    down = np.zeros(128)
+    cross = np.zeros(64)
+    db = np.zeros(128 * 64)
+    pk = np.zeros(1)
+    assert L.ref_isar(dp(vals.view(np.float64)), dp(fi), 32, dp(ang), 16, 1, 4, -40.0, dp(down), dp(cross),
+                      dp(db), dp(pk)) == 0
+    out.update({"isar_in": vals, "isar_freqs": fi, "isar_angles": ang, "isar_down": down,
+                "isar_cross": cross, "isar_db": db.reshape(128, 64), "isar_peak": pk})
+    return out
+
+
 def main():
     L = oracle.ref()
+    np.savez_compressed(os.path.join(HERE, "signal.npz"), **signal_vectors(L))
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_kat(L))
     np.savez_compressed(os.path.join(HERE, "em.npz"), **em_vectors(L))
     np.savez_compressed(os.path.join(HERE, "intersect.npz"), **intersect_vectors())
