@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define MCSBR_GPU_ABI_VERSION 1
+#define MCSBR_GPU_ABI_VERSION 2
 
 /* ---- status codes ------------------------------------------------------ */
 #define MCSBR_OK 0
@@ -142,7 +142,26 @@ typedef struct mcsbr_stats {
     uint64_t roulette_survivors[MCSBR_MAX_BOUNCE_LIMIT];
     double wall_ms;           /* host wall time of the call */
     double kernel_ms;         /* device time of the path kernel (CUDA events) */
+    /* deterministic solver only (solver_det.cpp:119-132): the reference's
+     * "all rays of a block in flight" accounting, max over blocks of the sum
+     * over rays of peak-depth (resp. every snapshot pushed) x sizeof(PathState)
+     * = 192 B; the GPU's actual branch-stack allocation is device_stack_bytes. */
+    uint64_t forced_stack_bytes;
+    uint64_t device_stack_bytes;
 } mcsbr_stats;
+
+/* Mirrors mcsbr::DetConfig (proj/include/mcsbr/solver_det.hpp:12-22).
+ * mcsbr_gpu_default_det_config() returns the reference defaults. */
+typedef struct mcsbr_det_config {
+    double rays_per_wavelength;     /* 20 */
+    int32_t max_bounce;             /* 9, at most MCSBR_MAX_BOUNCE_LIMIT */
+    int32_t force_stack_accounting; /* 0 (accepted; both stack figures are always reported) */
+    double amplitude_cutoff;        /* 0 = disabled; kill branches with max |E| < cutoff */
+    double launch_padding;          /* 0 m */
+    double reference_wavelength;    /* 0 = c / max(frequencies) */
+    int32_t block_size;             /* 8192 launch cells per accounting block */
+    int32_t _pad;
+} mcsbr_det_config;
 
 /* Mirrors mcsbr::Contribution (proj/include/mcsbr/farfield.hpp:45-52), 240 bytes. */
 typedef struct mcsbr_contribution {
@@ -229,6 +248,20 @@ MCSBR_API int mcsbr_gpu_estimate(mcsbr_scene* scene, const mcsbr_excitation* exc
                        const mcsbr_mc_config* config, int workers, double* values,
                        mcsbr_stats* stats, mcsbr_contribution* contributions,
                        uint64_t capacity, uint64_t* n_contributions);
+
+/* Deterministic SBR (mcsbr::solve, proj/src/solver_det.cpp:30-174): midpoint
+ * launch grid, every reflect/transmit branch explored depth-first (reflect
+ * first) with per-thread branch stacks in HBM.  Same buffers and semantics as
+ * mcsbr_gpu_estimate; contributions carry order_key = cell << 24 | event
+ * index, as the reference keys them (solver_det.cpp:104-105). */
+MCSBR_API void mcsbr_gpu_default_det_config(mcsbr_det_config* cfg);
+/* Mirrors DetConfig::validate (proj/src/solver_det.cpp:11-17). */
+MCSBR_API int mcsbr_gpu_validate_det_config(const mcsbr_det_config* cfg);
+MCSBR_API int mcsbr_gpu_solve(mcsbr_scene* scene, const mcsbr_excitation* excitation,
+                              const double* frequencies, uint32_t n_frequencies,
+                              const mcsbr_det_config* config, int workers, double* values,
+                              mcsbr_stats* stats, mcsbr_contribution* contributions,
+                              uint64_t capacity, uint64_t* n_contributions);
 
 /* Batched sweeps in ONE device launch: n_inc incidences, each observed by
  * n_rx receivers (receivers[i*n_rx + r]); occlusion applies to all.  values

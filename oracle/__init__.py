@@ -82,6 +82,16 @@ def ref() -> C.CDLL:
         L.ref_estimate.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
                                    C.POINTER(A.McConfigC), C.c_int, _DP, C.POINTER(A.Stats),
                                    C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_solve.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
+                                C.POINTER(A.DetConfigC), C.c_int, _DP, C.POINTER(A.Stats),
+                                C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_sweep_csv.argtypes = [_DP, _DP, C.c_uint32, C.c_uint64, C.c_char_p, C.c_char_p,
+                                    C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_stats_json.argtypes = [C.POINTER(A.Stats), C.c_char_p, C.c_char_p, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]
+        L.ref_parse_config.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_run_command.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                      C.c_uint64]
         L.ref_slab_reflection.argtypes = [_DP, _DP, C.c_int, C.c_double, C.c_int, _DP]
         L.ref_range_profile.argtypes = [_DP, _DP, C.c_uint32, C.c_int, C.c_int, _DP, _DP, _DP]
         L.ref_isar.argtypes = [_DP, _DP, C.c_uint32, _DP, C.c_uint32, C.c_int, C.c_int, C.c_double,
@@ -125,6 +135,9 @@ def port() -> C.CDLL:
                                    C.POINTER(A.McConfigC), C.c_uint64, C.c_uint64,
                                    C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_uint8),
                                    C.POINTER(C.c_uint64)]
+        L.orc_solve.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
+                                C.POINTER(A.DetConfigC), _DP, C.POINTER(A.Stats), C.c_void_p,
+                                C.c_uint64, C.POINTER(C.c_uint64)]
         L.orc_estimate_range.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
                                          C.POINTER(A.McConfigC), C.c_uint64, C.c_uint64, _DP,
                                          C.POINTER(A.Stats), C.POINTER(C.c_uint64)]
@@ -211,6 +224,59 @@ def port_estimate(scene_h, exc, freqs, cfg, contributions=False, capacity=0):
     L = port()
     return _estimate(L.orc_estimate, L.orc_last_error, scene_h.h, exc, freqs, cfg, contributions,
                      capacity)
+
+
+def ref_solve(scene_h, exc, freqs, cfg, workers=1, contributions=False, capacity=0):
+    L = ref()
+    return _estimate(L.ref_solve, L.ref_last_error, scene_h.h, exc, freqs, cfg, contributions,
+                     capacity, workers)
+
+
+def port_solve(scene_h, exc, freqs, cfg, contributions=False, capacity=0):
+    L = port()
+    return _estimate(L.orc_solve, L.orc_last_error, scene_h.h, exc, freqs, cfg, contributions,
+                     capacity)
+
+
+def _text(fn, *args):
+    n = C.c_uint64(0)
+    rc = fn(*args, None, 0, C.byref(n))
+    buf = C.create_string_buffer(n.value + 1)
+    rc = fn(*args, buf, n.value + 1, C.byref(n))
+    return rc, buf.value.decode()
+
+
+def ref_sweep_csv(values, freqs, seed, solver, config_hash):
+    """The reference's sweep_csv (runner.cpp:80-99) of a [4][nf] complex block."""
+    v = np.ascontiguousarray(np.stack([np.real(values), np.imag(values)], axis=-1), dtype=np.float64)
+    f = np.ascontiguousarray(freqs, dtype=np.float64)
+    rc, t = _text(ref().ref_sweep_csv, dp(v), dp(f), len(f), seed, solver.encode(), config_hash.encode())
+    if rc != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return t
+
+
+def ref_stats_json(stats, solver):
+    rc, t = _text(ref().ref_stats_json, C.byref(stats), solver.encode())
+    if rc != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return t
+
+
+def ref_parse_config(text):
+    """(ok, config_hash or ConfigError message)."""
+    rc, t = _text(ref().ref_parse_config, text.encode())
+    if rc < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return rc == 0, t
+
+
+def ref_run_command(command, config_text, out_dir, workers=1, seed=None):
+    rc = ref().ref_run_command(command.encode(), config_text.encode(), out_dir.encode(), workers,
+                               0 if seed is None else 1, 0 if seed is None else seed)
+    if rc < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return rc
 
 
 def port_path_log(scene_h, exc, freqs, cfg, first, n, stride):

@@ -1225,3 +1225,196 @@ int orc_path_log(const orc_scene* s, const mcsbr_excitation* exc, const double* 
     }
     return estimate_impl(s, exc, freqs, nf, cfg, NULL, NULL, NULL, 0, NULL, &pl, 0, UINT64_MAX, NULL, NULL);
 }
+
+/* ------------------------------------------------------------------------ */
+/* the deterministic solver (proj/src/solver_det.cpp:30-174)                   */
+
+static int validate_det(const mcsbr_det_config* c) { /* solver_det.cpp:11-17 */
+    if (!(c->rays_per_wavelength > 0.0)) { set_err("det: rays_per_wavelength must be > 0"); return -1; }
+    if (c->max_bounce < 1) { set_err("det: max_bounce must be >= 1"); return -1; }
+    if (c->amplitude_cutoff < 0.0) { set_err("det: amplitude_cutoff must be >= 0"); return -1; }
+    if (c->block_size < 1) { set_err("det: block_size must be >= 1"); return -1; }
+    return 0;
+}
+
+int orc_solve(const orc_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+              const mcsbr_det_config* cfg, double* values, mcsbr_stats* st_out,
+              mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+    g_fault = 0;
+    if (validate_det(cfg)) return -1;
+    if (nf == 0) { set_err("solve: empty frequency list"); return -1; }
+    double lambda_ref = cfg->reference_wavelength;
+    if (lambda_ref <= 0.0) lambda_ref = kC / freqs[nf - 1];
+    const rect_t rect = launch_rect(s, vload(exc->k_inc), cfg->launch_padding);
+    /* build_strata, solver_mc.cpp:19-31 */
+    if (!(lambda_ref > 0.0)) { set_err("build_strata: reference wavelength must be > 0"); return -1; }
+    const double target = lambda_ref / cfg->rays_per_wavelength;
+    int nu = (int)ceil(2.0 * rect.half_u / target);
+    int nv = (int)ceil(2.0 * rect.half_v / target);
+    if (nu < 1) nu = 1;
+    if (nv < 1) nv = 1;
+    const double cell_area = (4.0 * rect.half_u * rect.half_v) / ((double)nu * nv);
+    const uint64_t total = (uint64_t)(nu * nv);
+
+    const v3 ks = vload(exc->k_scatter), rv = vload(exc->rx_v), rh = vload(exc->rx_h);
+    const double ambient_n = s->mat_index[0];
+    const cv3 e0_v = cvreal(vload(exc->pol_v)), e0_h = cvreal(vload(exc->pol_h));
+    const double t_eps = 1e-6 * s->diameter;
+    const v3 k_inc = vload(exc->k_inc);
+    const double cutoff = cfg->amplitude_cutoff;
+    const uint64_t bs = (uint64_t)cfg->block_size;
+    const uint64_t nblocks = (total + bs - 1) / bs;
+
+    accum_t total_acc;
+    accum_init(&total_acc, freqs, (int)nf, ks, rv, rh);
+    mcsbr_stats tot;
+    memset(&tot, 0, sizeof tot);
+    uint64_t ncontrib_total = 0;
+    uint64_t stack_cap = 64;
+    path_t* stack = (path_t*)malloc(sizeof(path_t) * stack_cap);
+    block_t blk;
+    memset(&blk, 0, sizeof blk);
+
+    for (uint64_t block = 0; block < nblocks; ++block) {
+        const uint64_t begin = block * bs;
+        const uint64_t end = total < begin + bs ? total : begin + bs;
+        mcsbr_stats* st = &blk.st;
+        memset(st, 0, sizeof *st);
+        blk.ncol = 0;
+        accum_init(&blk.acc, freqs, (int)nf, ks, rv, rh);
+        st->rays_launched = end - begin;
+        uint64_t block_peak = 0, block_forced = 0;
+        for (uint64_t cell = begin; cell < end; ++cell) {
+            /* sample_stratum(jitter = false) + init_path */
+            const uint32_t i = (uint32_t)cell % (uint32_t)nu, j = (uint32_t)cell / (uint32_t)nu;
+            const double su = -1.0 + 2.0 * ((double)i + 0.5) / nu;
+            const double sv = -1.0 + 2.0 * ((double)j + 0.5) / nv;
+            const v3 p = vadd(vadd(rect.center, vmul(rect.u, su * rect.half_u)), vmul(rect.v, sv * rect.half_v));
+            path_t root;
+            memset(&root, 0, sizeof root);
+            root.origin = p;
+            root.dir = k_inc;
+            root.e[0] = e0_v;
+            root.e[1] = e0_h;
+            root.phi = ambient_n * vdot(k_inc, p);
+            root.prob = 1.0;
+            root.weight = 1.0;
+            root.medium_n = ambient_n;
+            root.stratum = (uint32_t)cell;
+            uint64_t sp = 0;
+            stack[sp++] = root;
+            uint64_t ray_peak = 1, ray_pushes = 1;
+            uint32_t event_seq = 0;
+            while (sp > 0) {
+                path_t state = stack[--sp];
+                hit_t hit;
+                if (!closest(s, state.origin, state.dir, state.bounce == 0 ? 0.0 : t_eps, 0, &hit)) continue;
+                ++st->segments_traced;
+                state.phi += state.medium_n * hit.t; /* advance */
+                state.origin = hit.point;
+                state.bounce += 1;
+                if (state.bounce <= MCSBR_MAX_BOUNCE_LIMIT) ++st->rays_per_bounce[state.bounce - 1];
+                if ((uint32_t)state.bounce > st->n_rounds) st->n_rounds = (uint32_t)state.bounce;
+                branchset_t set;
+                branch_outcomes(&state, &hit, &set);
+                if (g_fault) goto fault;
+                if (set.grazing) {
+                    ++st->grazing_kills;
+                    continue;
+                }
+                const int sc = hit.far_side_pec ? 0 : hit.near_is_ambient ? 1 : 2;
+                const int dark_exit = sc == 2 && set.co.tir;
+                int visible = 0;
+                if (!dark_exit && hit.exterior_facing) {
+                    hit_t occ;
+                    visible = !exc->occlusion_enabled || !closest(s, hit.point, ks, t_eps, 1, &occ);
+                }
+                if (visible) {
+                    cv3 j0, m0, j1, m1;
+                    meca(&hit, state.e[0], state.dir, sc, &set.co, &set.b, state.medium_n, &j0, &m0);
+                    meca(&hit, state.e[1], state.dir, sc, &set.co, &set.b, state.medium_n, &j1, &m1);
+                    if (g_fault) goto fault;
+                    const double cos_n = fabs(vdot(state.dir, hit.normal));
+                    const double scale = state.weight * cell_area / (state.prob * cos_n);
+                    mcsbr_contribution c;
+                    memset(&c, 0, sizeof c);
+                    cvstore(&c.a_j[0][0][0], cvmuld(j0, scale));
+                    cvstore(&c.a_m[0][0][0], cvmuld(m0, scale));
+                    cvstore(&c.a_j[1][0][0], cvmuld(j1, scale));
+                    cvstore(&c.a_m[1][0][0], cvmuld(m1, scale));
+                    c.phi_total = state.phi;
+                    vstore(c.exit_point, hit.point);
+                    c.bounce = state.bounce;
+                    c.order_key = ((uint64_t)state.stratum << 24) | (uint64_t)(event_seq++);
+                    accum_add(&blk.acc, &c);
+                    if (contribs) grow_push(&blk, &c);
+                    ++st->contributions;
+                }
+                if (state.bounce >= cfg->max_bounce) {
+                    ++st->cap_kills;
+                    continue;
+                }
+                /* push every surviving branch, transmit first (reflect on top) */
+                for (int k = set.count - 1; k >= 0; --k) {
+                    if (cutoff > 0.0 && dmax(cvnorm(set.new_e[k][0]), cvnorm(set.new_e[k][1])) < cutoff) continue;
+                    if (sp == stack_cap) {
+                        stack_cap *= 2;
+                        stack = (path_t*)realloc(stack, sizeof(path_t) * stack_cap);
+                    }
+                    path_t child = state;
+                    child.dir = set.new_dir[k];
+                    child.e[0] = set.new_e[k][0];
+                    child.e[1] = set.new_e[k][1];
+                    child.medium_n = set.new_n[k];
+                    stack[sp++] = child;
+                    ++ray_pushes;
+                }
+                if (sp + 1 > ray_peak) ray_peak = sp + 1;
+            }
+            block_peak += ray_peak * 192;
+            block_forced += ray_pushes * 192;
+        }
+        for (size_t k = 0; k < 4 * (size_t)nf; ++k) total_acc.sums[k] = cadd(total_acc.sums[k], blk.acc.sums[k]);
+        free(blk.acc.sums);
+        blk.acc.sums = NULL;
+        tot.rays_launched += st->rays_launched;
+        tot.segments_traced += st->segments_traced;
+        tot.contributions += st->contributions;
+        tot.grazing_kills += st->grazing_kills;
+        tot.cap_kills += st->cap_kills;
+        if (st->n_rounds > tot.n_rounds) tot.n_rounds = st->n_rounds;
+        for (int k = 0; k < MCSBR_MAX_BOUNCE_LIMIT; ++k) tot.rays_per_bounce[k] += st->rays_per_bounce[k];
+        if (block_peak > tot.peak_live_state_bytes) tot.peak_live_state_bytes = block_peak;
+        if (block_forced > tot.forced_stack_bytes) tot.forced_stack_bytes = block_forced;
+        if (contribs) {
+            for (uint64_t k = 0; k < blk.ncol && ncontrib_total + k < capacity; ++k)
+                contribs[ncontrib_total + k] = blk.col[k];
+        }
+        ncontrib_total += blk.ncol;
+    }
+    tot.state_bytes_per_ray = 192;
+    tot.block_size = bs;
+    if (st_out) *st_out = tot;
+    if (n_contribs) *n_contribs = ncontrib_total;
+    if (values) { /* finalize, farfield.cpp:154-167 */
+        for (int ch = 0; ch < 4; ++ch) {
+            for (uint32_t i = 0; i < nf; ++i) {
+                const double k0 = 2.0 * kPI * freqs[i] / kC;
+                const cx pre = C(0.0 * k0 / (2.0 * sqrt(kPI)), 1.0 * k0 / (2.0 * sqrt(kPI)));
+                const cx v = cmul(pre, total_acc.sums[ch * nf + i]);
+                values[2 * (ch * nf + i)] = v.re;
+                values[2 * (ch * nf + i) + 1] = v.im;
+            }
+        }
+    }
+    free(total_acc.sums);
+    free(stack);
+    free(blk.col);
+    return 0;
+fault:
+    free(total_acc.sums);
+    free(blk.acc.sums);
+    free(stack);
+    free(blk.col);
+    return -5;
+}

@@ -24,6 +24,9 @@
 #include "mcsbr/signal_processing.hpp"
 #include "mcsbr/solver_common.hpp"
 #include "mcsbr/solver_mc.hpp"
+#include "mcsbr/solver_det.hpp"
+#include "mcsbr/config.hpp"
+#include "mcsbr/runner.hpp"
 #include "mcsbr_gpu.h"
 
 using namespace mcsbr;
@@ -516,6 +519,128 @@ int ref_estimate(const void* sp, const mcsbr_excitation* exc, const double* freq
             if (n_contribs) *n_contribs = collected.size();
         }
         return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// ---- the deterministic solver (solver_det.cpp:30-174) ------------------------
+int ref_solve(const void* sp, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+              const mcsbr_det_config* cfg, int workers, double* values, mcsbr_stats* st,
+              mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+    try {
+        DetConfig d;
+        d.rays_per_wavelength = cfg->rays_per_wavelength;
+        d.max_bounce = cfg->max_bounce;
+        d.amplitude_cutoff = cfg->amplitude_cutoff;
+        d.force_stack_accounting = cfg->force_stack_accounting != 0;
+        d.launch_padding = cfg->launch_padding;
+        d.reference_wavelength = cfg->reference_wavelength;
+        d.block_size = cfg->block_size;
+        std::vector<Contribution> collected;
+        const DetResult r = solve(*static_cast<const Scene*>(sp), to_exc(*exc),
+                                  std::vector<double>(freqs, freqs + nf), d, workers,
+                                  contribs ? &collected : nullptr);
+        for (int ch = 0; ch < kPolChannelCount; ++ch)
+            for (uint32_t i = 0; i < nf; ++i) putc(values + 2 * (ch * nf + i), r.sweep.values[ch][i]);
+        if (st) {
+            std::memset(st, 0, sizeof(*st));
+            st->rays_launched = r.stats.rays_launched;
+            st->segments_traced = r.stats.segments_traced;
+            st->contributions = r.stats.contributions;
+            st->grazing_kills = r.stats.grazing_kills;
+            st->cap_kills = r.stats.cap_kills;
+            st->peak_live_state_bytes = r.stats.peak_live_state_bytes;
+            st->forced_stack_bytes = r.stats.forced_stack_bytes;
+            st->state_bytes_per_ray = r.stats.state_bytes_per_ray;
+            st->block_size = r.stats.block_size;
+            st->n_rounds = static_cast<uint32_t>(r.stats.rays_per_bounce.size());
+            for (size_t i = 0; i < r.stats.rays_per_bounce.size() && i < MCSBR_MAX_BOUNCE_LIMIT; ++i)
+                st->rays_per_bounce[i] = r.stats.rays_per_bounce[i];
+            st->wall_ms = r.stats.wall_ms;
+        }
+        if (contribs) {
+            const uint64_t m = collected.size() < capacity ? collected.size() : capacity;
+            std::memcpy(static_cast<void*>(contribs), collected.data(), m * sizeof(Contribution));
+            if (n_contribs) *n_contribs = collected.size();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// ---- runner artifacts and config (runner.cpp:48-118, config.cpp) -------------
+static int put_text(const std::string& t, char* out, uint64_t cap, uint64_t* len) {
+    *len = t.size();
+    if (out && cap > t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+    return 0;
+}
+
+// sweep_csv of a [4][nf] complex value block
+int ref_sweep_csv(const double* values, const double* freqs, uint32_t nf, uint64_t seed, const char* solver,
+                  const char* config_hash, char* out, uint64_t cap, uint64_t* len) {
+    try {
+        SweepResult s;
+        s.frequencies.assign(freqs, freqs + nf);
+        for (int ch = 0; ch < kPolChannelCount; ++ch) {
+            s.values[ch].resize(nf);
+            for (uint32_t i = 0; i < nf; ++i)
+                s.values[ch][i] = complexd(values[2 * (ch * nf + i)], values[2 * (ch * nf + i) + 1]);
+        }
+        s.seed = seed;
+        s.solver = solver;
+        return put_text(sweep_csv(s, config_hash), out, cap, len);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_stats_json(const mcsbr_stats* st, const char* solver, char* out, uint64_t cap, uint64_t* len) {
+    try {
+        RunStats r;
+        r.rays_launched = st->rays_launched;
+        r.segments_traced = st->segments_traced;
+        r.contributions = st->contributions;
+        r.grazing_kills = st->grazing_kills;
+        r.cap_kills = st->cap_kills;
+        r.peak_live_state_bytes = st->peak_live_state_bytes;
+        r.forced_stack_bytes = st->forced_stack_bytes;
+        r.state_bytes_per_ray = st->state_bytes_per_ray;
+        r.block_size = st->block_size;
+        r.wall_ms = st->wall_ms;
+        r.rays_per_bounce.assign(st->rays_per_bounce, st->rays_per_bounce + st->n_rounds);
+        r.roulette_candidates.assign(st->roulette_candidates, st->roulette_candidates + st->n_rounds);
+        r.roulette_survivors.assign(st->roulette_survivors, st->roulette_survivors + st->n_rounds);
+        return put_text(stats_json(r, solver), out, cap, len);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// parse_config: the config hash, or the ConfigError message (return 1)
+int ref_parse_config(const char* json_text, char* out, uint64_t cap, uint64_t* len) {
+    try {
+        const ExperimentConfig c = parse_config(json_text);
+        return put_text(c.config_hash, out, cap, len);
+    } catch (const ConfigError& e) {
+        put_text(e.what(), out, cap, len);
+        return 1;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// run_command end to end on the CPU reference (all artifacts under out_dir)
+int ref_run_command(const char* command, const char* json_text, const char* out_dir, int workers,
+                    int has_seed, uint64_t seed) {
+    try {
+        const ExperimentConfig c = parse_config(json_text);
+        RunOptions o;
+        o.workers = workers;
+        o.out_dir = out_dir;
+        if (has_seed) o.seed_override = seed;
+        return run_command(command, c, o);
     } catch (const std::exception& e) {
         return fail(e);
     }

@@ -108,6 +108,20 @@ class Stats(C.Structure):
         ("roulette_candidates", C.c_uint64 * MCSBR_MAX_BOUNCE_LIMIT),
         ("roulette_survivors", C.c_uint64 * MCSBR_MAX_BOUNCE_LIMIT),
         ("wall_ms", C.c_double), ("kernel_ms", C.c_double),
+        ("forced_stack_bytes", C.c_uint64), ("device_stack_bytes", C.c_uint64),
+    ]
+
+
+class DetConfigC(C.Structure):
+    _fields_ = [
+        ("rays_per_wavelength", C.c_double),
+        ("max_bounce", C.c_int32),
+        ("force_stack_accounting", C.c_int32),
+        ("amplitude_cutoff", C.c_double),
+        ("launch_padding", C.c_double),
+        ("reference_wavelength", C.c_double),
+        ("block_size", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -177,6 +191,13 @@ SIGNATURES = {
     "mcsbr_gpu_estimate": (
         C.c_int,
         [C.c_void_p, C.POINTER(Excitation), _DP, C.c_uint32, C.POINTER(McConfigC), C.c_int, _DP,
+         C.POINTER(Stats), C.c_void_p, C.c_uint64, _U64P],
+    ),
+    "mcsbr_gpu_default_det_config": (None, [C.POINTER(DetConfigC)]),
+    "mcsbr_gpu_validate_det_config": (C.c_int, [C.POINTER(DetConfigC)]),
+    "mcsbr_gpu_solve": (
+        C.c_int,
+        [C.c_void_p, C.POINTER(Excitation), _DP, C.c_uint32, C.POINTER(DetConfigC), C.c_int, _DP,
          C.POINTER(Stats), C.c_void_p, C.c_uint64, _U64P],
     ),
     "mcsbr_gpu_estimate_batch": (

@@ -193,6 +193,38 @@ int validate(const mcsbr_mc_config* c) {
     return MCSBR_OK;
 }
 
+// DetConfig::validate (solver_det.cpp:11-17)
+int validate_det(const mcsbr_det_config* c) {
+    if (!c) return set_err(MCSBR_EINVAL, "det: null config");
+    if (!(c->rays_per_wavelength > 0.0)) return set_err(MCSBR_EINVAL, "det: rays_per_wavelength must be > 0");
+    if (c->max_bounce < 1) return set_err(MCSBR_EINVAL, "det: max_bounce must be >= 1");
+    if (c->amplitude_cutoff < 0.0) return set_err(MCSBR_EINVAL, "det: amplitude_cutoff must be >= 0");
+    if (c->block_size < 1) return set_err(MCSBR_EINVAL, "det: block_size must be >= 1");
+    if (c->max_bounce > MCSBR_MAX_BOUNCE_LIMIT)
+        return set_err(MCSBR_EINVAL, "det: max_bounce exceeds MCSBR_MAX_BOUNCE_LIMIT (64)");
+    return MCSBR_OK;
+}
+
+// The deterministic solver runs the path engine with this McConfig: one
+// midpoint sample per cell (sample_stratum(..., jitter=false),
+// solver_det.cpp:72-74), no roulette, the det grid density and bounce cap.
+mcsbr_mc_config det_as_mc(const mcsbr_det_config* d) {
+    mcsbr_mc_config c;
+    mcsbr_gpu_default_config(&c);
+    c.strata_per_wavelength = d->rays_per_wavelength;
+    c.samples_per_stratum = 1;
+    c.roulette_enabled = 0;
+    c.max_bounce = d->max_bounce;
+    c.jitter = 0;
+    c.seed = 0;
+    c.reference_wavelength = d->reference_wavelength;
+    c.launch_padding = d->launch_padding;
+    c.block_size = d->block_size;
+    return c;
+}
+
+constexpr uint64_t kPathStateBytes = 192;  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
+
 struct Job {
     std::vector<IncDev> inc;
     std::vector<RxDev> rx;
@@ -206,8 +238,9 @@ struct Job {
 // Plan all incidences of a batch for one shard.
 int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
              const mcsbr_receiver* rxs, uint32_t n_rx, const double* freqs, uint32_t nf,
-             const mcsbr_mc_config* cfg, uint32_t shard, uint32_t nshard, int warps_hint, Job* job) {
-    int rc = validate(cfg);
+             const mcsbr_mc_config* cfg, uint32_t shard, uint32_t nshard, int warps_hint, Job* job,
+             bool det = false) {
+    int rc = det ? MCSBR_OK : validate(cfg);  // det: validated as DetConfig by the caller
     if (rc) return rc;
     if (nf == 0 || !freqs) return set_err(MCSBR_EINVAL, "estimate: empty frequency list");
     if (n_inc == 0) return set_err(MCSBR_EINVAL, "estimate: no incidences");
@@ -657,14 +690,15 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
                            uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
                            const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats,
                            mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs,
-                           const PathLog* plog = nullptr) {
+                           const PathLog* plog = nullptr, const mcsbr_det_config* det = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!s) return set_err(MCSBR_EINVAL, "null scene");
     int rc = use_device(s);
     if (rc) return rc;
     Job job;
-    rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, 0, 1, s->sms * 16, &job);
+    rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, 0, 1, s->sms * 16, &job, det != nullptr);
     if (rc) return rc;
+    if (det && (n_inc != 1 || n_rx != 1)) return set_err(MCSBR_EINVAL, "solve: one excitation per call");
     const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
     CK(s->sums.reserve(nsum), "cudaMalloc(sums)");
     CK(s->counters.reserve(kCntWords), "cudaMalloc(counters)");
@@ -703,8 +737,45 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         extra.plog_n = plog->n;
         extra.plog_stride = plog->stride;
     }
+    // deterministic: branch stacks for every resident thread + block accounting
+    double* d_stack = nullptr;
+    unsigned long long* d_blocks = nullptr;
+    uint64_t det_nblocks = 0, stack_bytes = 0;
+    if (det) {
+        const uint64_t threads = static_cast<uint64_t>(s->sms) * MCSBR_DET_THREADS_PER_SM;
+        const uint32_t depth = static_cast<uint32_t>(det->max_bounce);
+        stack_bytes = sizeof(double) * kDetFields * depth * threads;
+        det_nblocks = (job.total_entries + det->block_size - 1) / static_cast<uint64_t>(det->block_size);
+        cudaError_t e0 = cudaMalloc(&d_stack, stack_bytes);
+        if (e0 == cudaSuccess) e0 = cudaMalloc(&d_blocks, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1));
+        if (e0 == cudaSuccess)
+            e0 = cudaMemsetAsync(d_blocks, 0, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1), s->stream);
+        if (e0 != cudaSuccess) {
+            cudaFree(d_stack);
+            cudaFree(d_blocks);
+            cudaFree(d_out);
+            cudaFree(d_scratch);
+            cudaFree(d_cnt);
+            return cuda_err(e0, "cudaMalloc(branch stacks)");
+        }
+        extra.det = 1;
+        extra.det_cutoff = det->amplitude_cutoff;
+        extra.det_stack = d_stack;
+        extra.det_depth = depth;
+        extra.det_threads = threads;
+        extra.det_blocks = d_blocks;
+        extra.det_block_size = static_cast<uint64_t>(det->block_size);
+    }
     float kms = 0.f;
     rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms);
+    std::vector<unsigned long long> det_acc(2 * det_nblocks);
+    if (rc == MCSBR_OK && det && det_nblocks) {
+        const cudaError_t e2 = cudaMemcpy(det_acc.data(), d_blocks, sizeof(unsigned long long) * det_acc.size(),
+                                          cudaMemcpyDeviceToHost);
+        if (e2 != cudaSuccess) rc = cuda_err(e2, "branch accounting readback");
+    }
+    cudaFree(d_stack);
+    cudaFree(d_blocks);
     if (rc == MCSBR_OK && plog && plog->n) {
         cudaError_t e2 = cudaMemcpy(plog->tri, d_ptri, sizeof(uint32_t) * plog->n * plog->stride,
                                     cudaMemcpyDeviceToHost);
@@ -750,6 +821,17 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         decode(cnt, stats);
         stats->block_size = static_cast<uint64_t>(cfg->block_size);
         stats->peak_live_state_bytes = static_cast<uint64_t>(s->sms) * 2048 * stats->state_bytes_per_ray;
+        if (det) {  // RunStats::merge keeps the max over blocks (solver_common.cpp:64-65)
+            uint64_t peak = 0, push = 0;
+            for (uint64_t b = 0; b < det_nblocks; ++b) {
+                peak = std::max<uint64_t>(peak, det_acc[2 * b]);
+                push = std::max<uint64_t>(push, det_acc[2 * b + 1]);
+            }
+            stats->state_bytes_per_ray = kPathStateBytes;
+            stats->peak_live_state_bytes = peak * kPathStateBytes;
+            stats->forced_stack_bytes = push * kPathStateBytes;
+            stats->device_stack_bytes = stack_bytes;
+        }
         stats->kernel_ms = kms;
         stats->wall_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -773,6 +855,41 @@ int mcsbr_gpu_estimate(mcsbr_scene* s, const mcsbr_excitation* exc, const double
     std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
     return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, cfg, values, stats, contribs,
                            capacity, n_contribs);
+}
+
+void mcsbr_gpu_default_det_config(mcsbr_det_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->rays_per_wavelength = 20.0;
+    c->max_bounce = 9;
+    c->force_stack_accounting = 0;
+    c->amplitude_cutoff = 0.0;
+    c->launch_padding = 0.0;
+    c->reference_wavelength = 0.0;
+    c->block_size = 8192;
+}
+
+int mcsbr_gpu_validate_det_config(const mcsbr_det_config* cfg) { return validate_det(cfg); }
+
+int mcsbr_gpu_solve(mcsbr_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
+                    const mcsbr_det_config* cfg, int workers, double* values, mcsbr_stats* stats,
+                    mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
+    (void)workers;
+    int rc = validate_det(cfg);
+    if (rc) return rc;
+    if (nf == 0 || !freqs) return set_err(MCSBR_EINVAL, "solve: empty frequency list");
+    if (!exc) return set_err(MCSBR_EINVAL, "solve: null excitation");
+    const mcsbr_mc_config mc = det_as_mc(cfg);
+    mcsbr_incidence inc;
+    std::memcpy(inc.k_inc, exc->k_inc, sizeof(inc.k_inc));
+    std::memcpy(inc.pol_v, exc->pol_v, sizeof(inc.pol_v));
+    std::memcpy(inc.pol_h, exc->pol_h, sizeof(inc.pol_h));
+    inc.strata_per_wavelength = 0.0;
+    mcsbr_receiver rx;
+    std::memcpy(rx.k_scatter, exc->k_scatter, sizeof(rx.k_scatter));
+    std::memcpy(rx.rx_v, exc->rx_v, sizeof(rx.rx_v));
+    std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
+    return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, &mc, values, stats, contribs,
+                           capacity, n_contribs, nullptr, cfg);
 }
 
 int mcsbr_gpu_path_log(mcsbr_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,

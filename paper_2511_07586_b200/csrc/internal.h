@@ -116,7 +116,19 @@ struct TraceParams {
     unsigned long long* plog_branch;
     uint64_t plog_n;
     uint32_t plog_stride;
+    // deterministic solver (solver_det.cpp): every branch explored depth-first
+    int det;                                 // 1 = deterministic mode
+    double det_cutoff;                       // amplitude_cutoff (0 = off)
+    double* det_stack;                       // [kDetFields][det_depth][det_threads]
+    uint32_t det_depth;                      // stack entries per thread (max_bounce)
+    uint64_t det_threads;                    // threads the stack was sized for
+    unsigned long long* det_blocks;          // [n_blocks][2]: sum peak depth, sum pushes
+    uint64_t det_block_size;                 // cells per accounting block
 };
+constexpr int kDetFields = 24;  // origin 3, dir 3, e0 6, e1 6, phi 2, medium 2, bounce 1 (+1 spare)
+// branch stacks are sized for 4 resident 128-thread blocks per SM (the path
+// kernel's launch bound); launch_trace caps a det grid at the stack capacity
+#define MCSBR_DET_THREADS_PER_SM 512
 
 // bvh.cu
 struct BvhBuildOut {

@@ -430,6 +430,56 @@ __device__ __forceinline__ double shfl_nt(double v, int src) { return shfl_d(v, 
 __device__ __forceinline__ Cx shfl_nt(Cx v, int src) { return {shfl_d(v.re, src), shfl_d(v.im, src)}; }
 
 // ---------------------------------------------------------------------------
+// deterministic mode: per-thread branch stack in HBM, SoA over threads
+// (field f, depth d of thread t at det_stack[(f * depth + d) * threads + t]) so
+// that lanes pushing together write coalesced.  An entry is the reference's
+// child PathState (solver_det.cpp:134-147) minus what is constant per root.
+
+__device__ __forceinline__ double& det_at(const TraceParams& P, uint64_t t, int d, int f) {
+    return P.det_stack[(static_cast<size_t>(f) * P.det_depth + d) * P.det_threads + t];
+}
+
+template <typename NT>
+__device__ __forceinline__ void det_push(const TraceParams& P, uint64_t t, int d, V3 o, V3 dir, const CV3& e0,
+                                         const CV3& e1, NT phi, NT n, int bounce) {
+    const double v[23] = {o.x, o.y, o.z, dir.x, dir.y, dir.z,
+                          e0.x.re, e0.x.im, e0.y.re, e0.y.im, e0.z.re, e0.z.im,
+                          e1.x.re, e1.x.im, e1.y.re, e1.y.im, e1.z.re, e1.z.im,
+                          re_of(phi), im_of(phi), re_of(n), im_of(n), static_cast<double>(bounce)};
+#pragma unroll
+    for (int f = 0; f < 23; ++f) det_at(P, t, d, f) = v[f];
+}
+
+template <typename NT>
+__device__ __forceinline__ void det_pop(const TraceParams& P, uint64_t t, int d, Path<NT>& s) {
+    double v[23];
+#pragma unroll
+    for (int f = 0; f < 23; ++f) v[f] = det_at(P, t, d, f);
+    s.origin = {v[0], v[1], v[2]};
+    s.dir = {v[3], v[4], v[5]};
+    s.e0 = {{v[6], v[7]}, {v[8], v[9]}, {v[10], v[11]}};
+    s.e1 = {{v[12], v[13]}, {v[14], v[15]}, {v[16], v[17]}};
+    s.phi = make_nt<NT>(v[18], v[19]);
+    s.medium_n = make_nt<NT>(v[20], v[21]);
+    s.bounce = static_cast<int>(v[22]);
+    s.prob = 1.0;
+    s.weight = 1.0;
+}
+
+// norm(ComplexVec3) (em_math.hpp:91-93): sqrt(|x|^2 + |y|^2 + |z|^2)
+__device__ __forceinline__ double cvnorm(const CV3& v) {
+    return sqrt((v.x.re * v.x.re + v.x.im * v.x.im) + (v.y.re * v.y.re + v.y.im * v.y.im) +
+                (v.z.re * v.z.re + v.z.im * v.z.im));
+}
+
+// add a lane's stack accounting for one reference block (solver_det.cpp:127-132)
+__device__ __forceinline__ void det_flush(const TraceParams& P, uint64_t blk, uint64_t peak, uint64_t push) {
+    if (blk == ~0ull || (peak == 0 && push == 0)) return;
+    atomicAdd(P.det_blocks + 2 * blk, static_cast<unsigned long long>(peak));
+    atomicAdd(P.det_blocks + 2 * blk + 1, static_cast<unsigned long long>(push));
+}
+
+// ---------------------------------------------------------------------------
 // the path kernel
 
 // Accumulation modes:
@@ -446,7 +496,12 @@ enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
-template <int kMode, bool kDiel, bool kLossy>
+// kDet: the deterministic solver (solver_det.cpp:30-174) on the same engine:
+// midpoint launch (P.jitter = 0, spp = 1), no draws; at a two-branch hit the
+// reflect child continues in registers and the transmit child goes on the
+// lane's branch stack; a dead lane pops its own stack before it takes a new
+// entry, which reproduces the reference's depth-first, reflect-first order.
+template <int kMode, bool kDiel, bool kLossy, bool kDet>
 __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeSmem;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
@@ -476,6 +531,12 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     mcsbr_contribution* scratch =
         P.contrib_scratch ? static_cast<mcsbr_contribution*>(P.contrib_scratch) + gtid : nullptr;
+    // deterministic mode: branch-stack height, event_seq of the root ray, and
+    // the reference's stack accounting (peak depth / pushes per root ray,
+    // summed per accounting block of det_block_size cells)
+    int dsp = 0;
+    uint32_t dev = 0, dpeak = 0;
+    uint64_t dacc_peak = 0, dacc_push = 0, dblk = ~0ull;
 
     for (;;) {
         // ---- fetch a tile (warp-uniform) ----
@@ -518,6 +579,12 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
         // Lanes in both phases traverse together, so no lane idles while
         // others run occlusion rays, and the traversal loop appears once.
         for (;;) {
+            // ---- deterministic: a dead lane resumes its own pending branch ----
+            if (kDet && !alive && dsp > 0) {
+                det_pop(P, gtid, --dsp, s);
+                save_em(sl, s);
+                alive = true;
+            }
             // ---- regenerate dead lanes from the tile ----
             const unsigned need = __ballot_sync(kFull, !alive);
             if (need && cursor < e_end) {
@@ -528,6 +595,18 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                     save_em(sl, s);
                     alive = true;
                     ++n_launched;
+                    if (kDet) {  // a new root ray (solver_det.cpp:72-82)
+                        const uint64_t blk = s.cell / P.det_block_size;
+                        dacc_peak += dpeak;
+                        if (blk != dblk) {
+                            det_flush(P, dblk, dacc_peak, dacc_push);
+                            dacc_peak = dacc_push = 0;
+                            dblk = blk;
+                        }
+                        dpeak = 1;
+                        dacc_push += 1;
+                        dev = 0;
+                    }
                 }
                 cursor = min(cursor + static_cast<uint64_t>(__popc(need)), e_end);
             }
@@ -538,7 +617,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             bool hit = false;
             if (alive) {
                 if (pend) ++n_occ;
-                else atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
+                else if (!kDet) atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
                 // closest hit: solver_mc.cpp:142-144; occlusion: farfield.cpp:63-68 /
                 // geometry.cpp:242-244 from the exit point (= origin after advance)
                 hit = traverse(S, s.origin, pend ? ld3(R.k_s) : s.dir,
@@ -572,6 +651,8 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                     s.origin = point;
                     s.bounce += 1;
                     max_round = max(max_round, s.bounce);
+                    // the deterministic solver counts segments that hit (solver_det.cpp:88-93)
+                    if (kDet) atomicAdd(&s_bounce[min(s.bounce - 1, 63)], 1u);
                     const bool logged = P.plog_tri && a == 0 && s.entry < P.plog_n;
                     if (logged && static_cast<uint32_t>(s.bounce - 1) < P.plog_stride)
                         P.plog_tri[s.entry * P.plog_stride + (s.bounce - 1)] = id;
@@ -653,14 +734,51 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                                 scratch->bounce = s.bounce;
                                 scratch->_pad = 0;
                                 scratch->order_key =
-                                    ((static_cast<uint64_t>(s.cell) * P.spp + s.sample) << 8) |
-                                    static_cast<uint64_t>(s.bounce & 0xff);
+                                    kDet ? (static_cast<uint64_t>(s.cell) << 24 | dev)  // solver_det.cpp:104
+                                         : ((static_cast<uint64_t>(s.cell) * P.spp + s.sample) << 8) |
+                                               static_cast<uint64_t>(s.bounce & 0xff);
                             }
                         }
                         if (s.bounce >= P.max_bounce) {  // cap (solver_mc.cpp:176-179)
                             ++n_cap;
                             alive = false;
                             if (logged) P.plog_term[s.entry] = 2;
+                        } else if (kDet) {
+                            // every surviving branch (solver_det.cpp:127-147)
+                            bool keep_r = true, keep_t = two;
+                            if (P.det_cutoff > 0.0) {
+                                const double nr0 = cvnorm(er0), nr1 = cvnorm(er1);
+                                keep_r = !(((nr0 < nr1) ? nr1 : nr0) < P.det_cutoff);
+                                if (two) {
+                                    const double nt0 = cvnorm(et0), nt1 = cvnorm(et1);
+                                    keep_t = !(((nt0 < nt1) ? nt1 : nt0) < P.det_cutoff);
+                                }
+                            }
+                            if (keep_r && keep_t) {
+                                if (dsp >= static_cast<int>(P.det_depth)) {
+                                    fault |= kFaultStack;
+                                } else {
+                                    det_push(P, gtid, dsp, s.origin, b.dir_t, et0, et1, s.phi, n2, s.bounce);
+                                    ++dsp;
+                                }
+                            }
+                            const uint32_t kept = static_cast<uint32_t>(keep_r) + static_cast<uint32_t>(keep_t);
+                            dacc_push += kept;
+                            if (keep_r) {
+                                s.dir = b.dir_r;
+                                s.e0 = er0;
+                                s.e1 = er1;
+                                s.medium_n = n1;
+                            } else if (keep_t) {
+                                s.dir = b.dir_t;
+                                s.e0 = et0;
+                                s.e1 = et1;
+                                s.medium_n = n2;
+                            } else {
+                                alive = false;
+                            }
+                            // reference stack height after its pushes, + 1 (solver_det.cpp:148)
+                            dpeak = max(dpeak, static_cast<uint32_t>(dsp) + (kept ? 1u : 0u) + 1u);
                         } else {
                             // choose_branch (solver_mc.cpp:44-54, :181-190)
                             int pick = 0;
@@ -731,6 +849,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             }
             if (visible) {
                 ++n_contrib;
+                if (kDet) ++dev;
                 if (scratch) {
                     const unsigned long long slot = atomicAdd(P.contrib_count, 1ull);
                     if (slot < P.contrib_cap)
@@ -804,6 +923,13 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             }
         }
 
+        if (kDet) {  // every root of the tile is finished
+            dacc_peak += dpeak;
+            dpeak = 0;
+            det_flush(P, dblk, dacc_peak, dacc_push);
+            dacc_peak = dacc_push = 0;
+            dblk = ~0ull;
+        }
         // ---- flush the tile's accumulators ----
         double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
         if (kMode == kModeFan) {
@@ -898,10 +1024,10 @@ bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
 
 bool trace_fan_supported(uint32_t nf) { return nf == 1; }
 
-template <int kMode, bool kDiel, bool kLossy>
+template <int kMode, bool kDiel, bool kLossy, bool kDet>
 static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
                                cudaStream_t stream) {
-    auto* k = path_kernel<kMode, kDiel, kLossy>;
+    auto* k = path_kernel<kMode, kDiel, kLossy, kDet>;
     if (smem > 0) {  // static state slots + dynamic accumulators may pass 48 KB: opt in
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -913,6 +1039,7 @@ static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads
     uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
     const uint64_t max_blocks = (p.total_tiles + threads / 32 - 1) / (threads / 32);
     if (blocks > max_blocks) blocks = max_blocks;
+    if (kDet && blocks * threads > p.det_threads) blocks = p.det_threads / threads;  // stack capacity
     if (blocks < 1) blocks = 1;
     k<<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p);
     return cudaGetLastError();
@@ -921,14 +1048,17 @@ static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads
 template <bool kDiel, bool kLossy>
 static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int threads, size_t smem,
                                cudaStream_t stream) {
-    return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy>(p, sms, threads, smem, stream)
-           : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy>(p, sms, threads, smem, stream)
-                              : launch_mode<kModeSmem, kDiel, kLossy>(p, sms, threads, smem, stream);
+    if (p.det)  // one receiver per launch (the deterministic solver has no fan mode)
+        return mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, true>(p, sms, threads, smem, stream)
+                                : launch_mode<kModeSmem, kDiel, kLossy, true>(p, sms, threads, smem, stream);
+    return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false>(p, sms, threads, smem, stream)
+           : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false>(p, sms, threads, smem, stream)
+                              : launch_mode<kModeSmem, kDiel, kLossy, false>(p, sms, threads, smem, stream);
 }
 
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
-    const int mode = p.fan ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
+    const int mode = (p.fan && !p.det) ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
     const size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
     // three physics instantiations: all-PEC (dielectric code compiled out),
     // the reference's lossless dielectric model (bit-exact), lossy media

@@ -167,6 +167,33 @@ class McConfig:
         _raise(A.lib().mcsbr_gpu_validate_config(C.byref(self.to_c())))
 
 
+@dataclass
+class DetConfig:
+    """mcsbr::DetConfig (solver_det.hpp:12-22)."""
+    rays_per_wavelength: float = 20.0
+    max_bounce: int = 9
+    amplitude_cutoff: float = 0.0
+    force_stack_accounting: bool = False
+    launch_padding: float = 0.0
+    reference_wavelength: float = 0.0
+    block_size: int = 8192
+
+    def to_c(self) -> A.DetConfigC:
+        c = A.DetConfigC()
+        c.rays_per_wavelength = float(self.rays_per_wavelength)
+        c.max_bounce = int(self.max_bounce)
+        c.amplitude_cutoff = float(self.amplitude_cutoff)
+        c.force_stack_accounting = 1 if self.force_stack_accounting else 0
+        c.launch_padding = float(self.launch_padding)
+        c.reference_wavelength = float(self.reference_wavelength)
+        c.block_size = int(self.block_size)
+        return c
+
+    def validate(self) -> None:
+        """DetConfig::validate (solver_det.cpp:11-17)."""
+        _raise(A.lib().mcsbr_gpu_validate_det_config(C.byref(self.to_c())))
+
+
 # ---------------------------------------------------------------------------
 # results (farfield.hpp:73-80, solver_common.hpp:37-53)
 
@@ -175,7 +202,7 @@ class McConfig:
 class SweepResult:
     frequencies: np.ndarray
     values: np.ndarray  # complex [4][nf]: VV, HH, VH, HV
-    solver: str = "mc-b200"
+    solver: str = "mc"
     seed: int = 0
     rays_launched: int = 0
     contributions: int = 0
@@ -197,6 +224,8 @@ class RunStats:
     block_size: int = 0
     wall_ms: float = 0.0
     kernel_ms: float = 0.0
+    forced_stack_bytes: int = 0
+    device_stack_bytes: int = 0
 
     @staticmethod
     def from_c(st: A.Stats) -> "RunStats":
@@ -212,11 +241,18 @@ class RunStats:
             peak_live_state_bytes=st.peak_live_state_bytes,
             state_bytes_per_ray=st.state_bytes_per_ray, block_size=st.block_size,
             wall_ms=st.wall_ms, kernel_ms=st.kernel_ms,
+            forced_stack_bytes=st.forced_stack_bytes, device_stack_bytes=st.device_stack_bytes,
         )
 
 
 @dataclass
 class McResult:
+    sweep: SweepResult
+    stats: RunStats
+
+
+@dataclass
+class DetResult:
     sweep: SweepResult
     stats: RunStats
 
@@ -405,6 +441,36 @@ def estimate(scene: Scene, excitation: Excitation, frequencies, config: McConfig
                         seed=config.seed, rays_launched=stats.rays_launched,
                         contributions=stats.contributions)
     return McResult(sweep=sweep, stats=stats)
+
+
+def solve(scene: Scene, excitation: Excitation, frequencies, config: DetConfig,
+          workers: int = 1, contributions_out: list | None = None,
+          contributions_capacity: int = 1 << 22) -> DetResult:
+    """mcsbr::solve (solver_det.hpp:29-31), the deterministic SBR baseline, on the GPU."""
+    freqs = np.ascontiguousarray(np.asarray(frequencies, dtype=np.float64).reshape(-1))
+    nf = len(freqs)
+    values = np.zeros((4, max(nf, 1), 2), dtype=np.float64)
+    st = A.Stats()
+    cfg = config.to_c()
+    exc = excitation.to_c()
+    buf = None
+    n_c = C.c_uint64(0)
+    cap = 0
+    if contributions_out is not None:
+        cap = int(contributions_capacity)
+        buf = np.zeros(cap, dtype=A.CONTRIBUTION_DTYPE)
+    _raise(A.lib().mcsbr_gpu_solve(
+        scene.handle, C.byref(exc), freqs.ctypes.data_as(C.POINTER(C.c_double)), nf, C.byref(cfg),
+        int(workers), values.ctypes.data_as(C.POINTER(C.c_double)), C.byref(st),
+        buf.ctypes.data if buf is not None else None, cap, C.byref(n_c)))
+    if contributions_out is not None:
+        if n_c.value > cap:
+            raise ValueError(f"contributions_out capacity {cap} < {n_c.value}")
+        contributions_out.append(buf[: n_c.value].copy())
+    stats = RunStats.from_c(st)
+    sweep = SweepResult(frequencies=freqs, values=values[..., 0] + 1j * values[..., 1],
+                        solver="deterministic", seed=0, rays_launched=stats.rays_launched)
+    return DetResult(sweep=sweep, stats=stats)
 
 
 def path_log(scene: Scene, excitation: Excitation, frequencies, config: McConfig, n_paths: int,

@@ -12,6 +12,7 @@ Outputs (committed; the GPU box and the CPU test suite only read them):
                  farfield.cpp)
   intersect.npz  Scene::intersect on seeded random rays, 3 builtin scenes
   estimate.npz   full estimate() sweeps (values, stats, contribution digests)
+  det.npz        full solve() (deterministic SBR) sweeps, same fields + stack accounting
                  for the parity cases of tests/helpers.py
 """
 from __future__ import annotations
@@ -202,6 +203,24 @@ def estimate_vectors():
     return out
 
 
+def det_vectors():
+    """Deterministic solver (solver_det.cpp:30-174) on the reference."""
+    from tests.helpers import det_cases, det_stats_vector
+
+    out = {}
+    for name, sd, exc, freqs, cfg in det_cases():
+        rs = oracle.ref_scene(sd)
+        r = oracle.ref_solve(rs, exc.to_c(), np.asarray(freqs, float), cfg.to_c(), 1, True, 1 << 21)
+        c = r["contributions"]
+        c = c[np.argsort(c["order_key"], kind="stable")]
+        out[f"{name}_values"] = r["values"]
+        out[f"{name}_stats"] = det_stats_vector(r["stats"])
+        out[f"{name}_contrib_sha256"] = np.frombuffer(hashlib.sha256(c.tobytes()).digest(),
+                                                      dtype=np.uint8)
+        out[f"{name}_contrib_head"] = c[:64]
+    return out
+
+
 def synthetic_sweeps(rng, freqs, angles, n_pts=5):
     """Point-scatterer sweeps values[a][k] = sum_i A_i e^{-j 2 k (x_i cos t + y_i sin t)}."""
     k = 2 * np.pi * np.asarray(freqs) / 299792458.0
@@ -251,6 +270,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "em.npz"), **em_vectors(L))
     np.savez_compressed(os.path.join(HERE, "intersect.npz"), **intersect_vectors())
     np.savez_compressed(os.path.join(HERE, "estimate.npz"), **estimate_vectors())
+    np.savez_compressed(os.path.join(HERE, "det.npz"), **det_vectors())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -71,3 +71,40 @@ def parity_cases():
                   M.McConfig(strata_per_wavelength=0.7, samples_per_stratum=1, seed=5, max_bounce=24,
                              roulette=M.RouletteConfig(enabled=True, min_bounce=3))))
     return cases
+
+
+# (name, scene, excitation, frequencies, DetConfig) deterministic-solver cases:
+# branching dielectrics with and without the amplitude cutoff, TIR-rich nested
+# media, PEC, bistatic, the coated sphere.  Oracle cost ~0.1-1 s each.
+def det_cases():
+    cases = []
+    glass = M.make_builtin_scene("glass_cube", {"eps_r": 2.25, "size_m": 1.0})
+    cases.append(("det_glass", glass, M.monostatic_excitation(20.0, 40.0), np.linspace(1e9, 3e9, 5),
+                  M.DetConfig(rays_per_wavelength=6, max_bounce=6, block_size=700)))
+    cases.append(("det_glass_cutoff", glass, M.monostatic_excitation(0.0, 0.0), [1e9, 2e9],
+                  M.DetConfig(rays_per_wavelength=6, max_bounce=9, amplitude_cutoff=0.2)))
+    nested = M.make_builtin_scene("nested", {"subdivisions": 2})
+    cases.append(("det_nested", nested, M.monostatic_excitation(10.0, 5.0), [3e9],
+                  M.DetConfig(rays_per_wavelength=3, max_bounce=12, amplitude_cutoff=0.05,
+                              block_size=300)))
+    sph = M.make_builtin_scene("sphere", {"subdivisions": 3})
+    # oblique: at normal incidence the midpoint grid puts rays exactly on the
+    # icosphere's edges, where the reference's own BVH misses (SURVEY.md sec. 7,
+    # hard part 1) and disagrees with its brute force, which we follow
+    cases.append(("det_sphere_pec", sph, M.monostatic_excitation(37.0, 21.0), [3e9],
+                  M.DetConfig(rays_per_wavelength=8, max_bounce=8)))
+    stub = M.make_builtin_scene("airplane_stub", {"eps_r": 2.0})
+    cases.append(("det_stub_bistatic", stub, M.bistatic_excitation(70.0, 10.0, 50.0, 40.0),
+                  np.linspace(2e9, 3e9, 3), M.DetConfig(rays_per_wavelength=4, max_bounce=7)))
+    obj, mm = M.coated_sphere(subdivisions=2, lossless=True)
+    coat = M.load_scene(obj, mm)
+    cases.append(("det_coated_sphere", coat, M.monostatic_excitation(90.0, 0.0), [3e9],
+                  M.DetConfig(rays_per_wavelength=6, max_bounce=10, amplitude_cutoff=0.02)))
+    return cases
+
+
+def det_stats_vector(st):
+    return np.array([st.rays_launched, st.segments_traced, st.contributions, st.grazing_kills,
+                     st.cap_kills, st.peak_live_state_bytes, st.forced_stack_bytes,
+                     st.state_bytes_per_ray, st.n_rounds] + list(st.rays_per_bounce[:32]),
+                    dtype=np.uint64)

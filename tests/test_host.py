@@ -30,7 +30,14 @@ def test_library_exports_every_header_symbol():
 def test_library_cpu_entry_points():
     """Host-only entry points work without a device; compute ones fail loudly."""
     L = A.lib()
-    assert L.mcsbr_gpu_abi_version() == 1
+    assert L.mcsbr_gpu_abi_version() == 2
+    det = A.DetConfigC()
+    L.mcsbr_gpu_default_det_config(C.byref(det))
+    assert (det.rays_per_wavelength, det.max_bounce, det.amplitude_cutoff, det.block_size) == (20.0, 9, 0.0, 8192)
+    assert L.mcsbr_gpu_validate_det_config(C.byref(det)) == 0
+    det.max_bounce = 0
+    assert L.mcsbr_gpu_validate_det_config(C.byref(det)) == A.MCSBR_EINVAL
+    assert b"det: max_bounce must be >= 1" in L.mcsbr_gpu_last_error()
     cfg = A.McConfigC()
     L.mcsbr_gpu_default_config(C.byref(cfg))
     assert cfg.strata_per_wavelength == 10.0 and cfg.samples_per_stratum == 16

@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 import paper_2511_07586_b200 as M
-from tests.helpers import parity_cases, sort_contribs
+from tests.helpers import det_cases, det_stats_vector, parity_cases, sort_contribs
 
 G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 dp = oracle.dp
@@ -157,6 +157,24 @@ def test_estimate_golden(case):
     assert c[:64].tobytes() == g[f"{name}_contrib_head"].tobytes()
 
 
+DET = det_cases()
+
+
+@pytest.mark.parametrize("case", DET, ids=[c[0] for c in DET])
+def test_solve_golden(case):
+    """C restatement of the deterministic solver == reference solve() bit for bit
+    (values, stats incl. the stack accounting, every contribution)."""
+    name, sd, exc, freqs, cfg = case
+    g = load("det.npz")
+    r = oracle.port_solve(oracle.port_scene(sd), exc.to_c(), np.asarray(freqs, float), cfg.to_c(),
+                          True, 1 << 21)
+    assert r["values"].tobytes() == g[f"{name}_values"].tobytes()
+    assert np.array_equal(det_stats_vector(r["stats"]), g[f"{name}_stats"])
+    c = sort_contribs(r["contributions"])
+    assert hashlib.sha256(c.tobytes()).digest() == g[f"{name}_contrib_sha256"].tobytes()
+    assert c[:64].tobytes() == g[f"{name}_contrib_head"].tobytes()
+
+
 # --------------------------------------------------------------------------
 # live reference (skipped when oracle/_ref has not been built)
 
@@ -189,6 +207,27 @@ def test_oracle_equals_reference_on_fresh_cases():
             b = oracle.port_estimate(ps, exc.to_c(), freqs, cfg.to_c(), True, 1 << 20)
             assert a["values"].tobytes() == b["values"].tobytes()
             assert a["contributions"].tobytes() == b["contributions"].tobytes()
+
+
+@pytest.mark.ref
+@needs_ref
+def test_solve_oracle_equals_reference_on_fresh_cases():
+    rng = np.random.default_rng(11)
+    for sd in [M.make_builtin_scene("glass_cube", {"eps_r": 3.1, "size_m": 0.7}),
+               M.make_builtin_scene("nested", {"subdivisions": 2})]:
+        rs, ps = oracle.ref_scene(sd), oracle.port_scene(sd)
+        for _ in range(3):
+            exc = M.monostatic_excitation(rng.uniform(0, 180), rng.uniform(0, 360))
+            cfg = M.DetConfig(rays_per_wavelength=float(rng.uniform(2, 5)),
+                              max_bounce=int(rng.integers(1, 10)),
+                              amplitude_cutoff=float(rng.choice([0.0, 0.1, 0.3])),
+                              block_size=int(rng.integers(50, 5000)))
+            freqs = np.linspace(1e9, 3e9, int(rng.integers(1, 4)))
+            a = oracle.ref_solve(rs, exc.to_c(), freqs, cfg.to_c(), 2, True, 1 << 20)
+            b = oracle.port_solve(ps, exc.to_c(), freqs, cfg.to_c(), True, 1 << 20)
+            assert a["values"].tobytes() == b["values"].tobytes()
+            assert a["contributions"].tobytes() == b["contributions"].tobytes()
+            assert np.array_equal(det_stats_vector(a["stats"]), det_stats_vector(b["stats"]))
 
 
 @pytest.mark.ref
