@@ -23,18 +23,23 @@ from paper_2511_07586_b200 import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libmcsbr_ref.so")
+# the reference with its solver TUs swapped for the product's drop-in
+# (paper_2511_07586_b200/dropin/solver_b200.cpp): `make -C oracle dropin`
+DROPIN_SO = os.path.join(HERE, "_ref", "libmcsbr_ref_b200.so")
 PORT_SO = os.path.join(HERE, "libmcsbr_oracle.so")
 
 _DP = C.POINTER(C.c_double)
 _ref = None
+_dropin = None
 _port = None
 
 
 def build(ref_too: bool = True) -> None:
-    """Compile the C restatement and, when /root/reference exists, the reference."""
+    """Compile the C restatement and, when /root/reference exists, the reference
+    and the drop-in integration library (needs the product library built first)."""
     subprocess.run(["make", "-s", "-C", HERE], check=True)
     if ref_too and os.path.isdir("/root/reference/proj/src"):
-        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "ref", "dropin"], check=True)
 
 
 def have_ref() -> bool:
@@ -46,62 +51,79 @@ def ref() -> C.CDLL:
     if _ref is None:
         if not os.path.exists(REF_SO):
             raise FileNotFoundError(f"{REF_SO} not built (make -C oracle ref)")
-        L = C.CDLL(REF_SO)
-        L.ref_last_error.restype = C.c_char_p
-        L.ref_counter_hash.restype = C.c_uint64
-        L.ref_counter_hash.argtypes = [C.c_uint64] * 5
-        L.ref_counter_uniform.restype = C.c_double
-        L.ref_counter_uniform.argtypes = [C.c_uint64] * 5
-        L.ref_fresnel.argtypes = [C.c_double, C.c_double, C.c_double, _DP]
-        L.ref_sp_basis.argtypes = [_DP, _DP, C.c_double, C.c_double, _DP]
-        L.ref_interface_transform.argtypes = [_DP, C.c_int, _DP, _DP, _DP]
-        L.ref_branch_outcomes.argtypes = [_DP, _DP, _DP]
-        L.ref_meca_currents.argtypes = [_DP, _DP, _DP, C.c_int, _DP]
-        L.ref_meca_currents_hot.argtypes = [_DP, _DP, _DP, C.c_int, _DP, _DP, C.c_double, _DP]
-        L.ref_evaluate_sweep.argtypes = [C.c_void_p, C.c_uint64, _DP, C.c_uint32, _DP, _DP, _DP, _DP]
-        L.ref_monostatic_excitation.argtypes = [C.c_double, C.c_double, C.POINTER(A.Excitation)]
-        L.ref_bistatic_excitation.argtypes = [C.c_double] * 4 + [C.POINTER(A.Excitation)]
-        L.ref_scene_load.restype = C.c_void_p
-        L.ref_scene_load.argtypes = [C.c_char_p, C.c_char_p]
-        L.ref_scene_builtin.restype = C.c_void_p
-        L.ref_scene_builtin.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), _DP, C.c_int]
-        L.ref_builtin_text.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), _DP, C.c_int,
-                                       C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
-                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
-        L.ref_scene_free.argtypes = [C.c_void_p]
-        L.ref_scene_sizes.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
-        L.ref_scene_export.argtypes = [C.c_void_p, _DP, C.c_void_p, C.c_void_p, _DP]
-        L.ref_scene_from_arrays.restype = C.c_void_p
-        L.ref_scene_from_arrays.argtypes = [_DP, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p,
-                                            C.c_uint32]
-        L.ref_intersect.argtypes = [C.c_void_p, _DP, _DP, _DP, C.c_uint64, C.c_int, _DP]
-        L.ref_launch_rect.argtypes = [C.c_void_p, _DP, C.c_double, _DP]
-        L.ref_build_strata.argtypes = [_DP, C.c_double, C.c_double, C.POINTER(C.c_int32), _DP]
-        L.ref_sample_stratum.argtypes = [_DP, C.c_int32, C.c_int32, C.c_uint32, C.c_uint32,
-                                         C.c_uint64, C.c_int, _DP]
-        L.ref_estimate.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
-                                   C.POINTER(A.McConfigC), C.c_int, _DP, C.POINTER(A.Stats),
-                                   C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
-        L.ref_solve.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
-                                C.POINTER(A.DetConfigC), C.c_int, _DP, C.POINTER(A.Stats),
-                                C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
-        L.ref_sweep_csv.argtypes = [_DP, _DP, C.c_uint32, C.c_uint64, C.c_char_p, C.c_char_p,
-                                    C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
-        L.ref_stats_json.argtypes = [C.POINTER(A.Stats), C.c_char_p, C.c_char_p, C.c_uint64,
-                                     C.POINTER(C.c_uint64)]
-        L.ref_parse_config.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
-        L.ref_run_command.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
-                                      C.c_uint64]
-        L.ref_slab_reflection.argtypes = [_DP, _DP, C.c_int, C.c_double, C.c_int, _DP]
-        L.ref_range_profile.argtypes = [_DP, _DP, C.c_uint32, C.c_int, C.c_int, _DP, _DP, _DP]
-        L.ref_isar.argtypes = [_DP, _DP, C.c_uint32, _DP, C.c_uint32, C.c_int, C.c_int, C.c_double,
-                               _DP, _DP, _DP, _DP]
-        L.ref_plate_rcs.restype = C.c_double
-        L.ref_plate_rcs.argtypes = [C.c_double] * 3
-        L.ref_sphere_go_rcs.restype = C.c_double
-        L.ref_sphere_go_rcs.argtypes = [C.c_double]
-        _ref = L
+        _ref = _bind_shim(C.CDLL(REF_SO))
     return _ref
+
+
+def have_dropin() -> bool:
+    return os.path.exists(DROPIN_SO)
+
+
+def dropin() -> C.CDLL:
+    """The reference's own code with estimate()/solve() on the GPU (f3)."""
+    global _dropin
+    if _dropin is None:
+        if not os.path.exists(DROPIN_SO):
+            raise FileNotFoundError(f"{DROPIN_SO} not built (make -C oracle dropin)")
+        _dropin = _bind_shim(C.CDLL(DROPIN_SO))
+    return _dropin
+
+
+def _bind_shim(L: C.CDLL) -> C.CDLL:
+    L.ref_last_error.restype = C.c_char_p
+    L.ref_counter_hash.restype = C.c_uint64
+    L.ref_counter_hash.argtypes = [C.c_uint64] * 5
+    L.ref_counter_uniform.restype = C.c_double
+    L.ref_counter_uniform.argtypes = [C.c_uint64] * 5
+    L.ref_fresnel.argtypes = [C.c_double, C.c_double, C.c_double, _DP]
+    L.ref_sp_basis.argtypes = [_DP, _DP, C.c_double, C.c_double, _DP]
+    L.ref_interface_transform.argtypes = [_DP, C.c_int, _DP, _DP, _DP]
+    L.ref_branch_outcomes.argtypes = [_DP, _DP, _DP]
+    L.ref_meca_currents.argtypes = [_DP, _DP, _DP, C.c_int, _DP]
+    L.ref_meca_currents_hot.argtypes = [_DP, _DP, _DP, C.c_int, _DP, _DP, C.c_double, _DP]
+    L.ref_evaluate_sweep.argtypes = [C.c_void_p, C.c_uint64, _DP, C.c_uint32, _DP, _DP, _DP, _DP]
+    L.ref_monostatic_excitation.argtypes = [C.c_double, C.c_double, C.POINTER(A.Excitation)]
+    L.ref_bistatic_excitation.argtypes = [C.c_double] * 4 + [C.POINTER(A.Excitation)]
+    L.ref_scene_load.restype = C.c_void_p
+    L.ref_scene_load.argtypes = [C.c_char_p, C.c_char_p]
+    L.ref_scene_builtin.restype = C.c_void_p
+    L.ref_scene_builtin.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), _DP, C.c_int]
+    L.ref_builtin_text.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), _DP, C.c_int,
+                                   C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    L.ref_scene_free.argtypes = [C.c_void_p]
+    L.ref_scene_sizes.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
+    L.ref_scene_export.argtypes = [C.c_void_p, _DP, C.c_void_p, C.c_void_p, _DP]
+    L.ref_scene_from_arrays.restype = C.c_void_p
+    L.ref_scene_from_arrays.argtypes = [_DP, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p,
+                                        C.c_uint32]
+    L.ref_intersect.argtypes = [C.c_void_p, _DP, _DP, _DP, C.c_uint64, C.c_int, _DP]
+    L.ref_launch_rect.argtypes = [C.c_void_p, _DP, C.c_double, _DP]
+    L.ref_build_strata.argtypes = [_DP, C.c_double, C.c_double, C.POINTER(C.c_int32), _DP]
+    L.ref_sample_stratum.argtypes = [_DP, C.c_int32, C.c_int32, C.c_uint32, C.c_uint32,
+                                     C.c_uint64, C.c_int, _DP]
+    L.ref_estimate.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
+                               C.POINTER(A.McConfigC), C.c_int, _DP, C.POINTER(A.Stats),
+                               C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.ref_solve.argtypes = [C.c_void_p, C.POINTER(A.Excitation), _DP, C.c_uint32,
+                            C.POINTER(A.DetConfigC), C.c_int, _DP, C.POINTER(A.Stats),
+                            C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.ref_sweep_csv.argtypes = [_DP, _DP, C.c_uint32, C.c_uint64, C.c_char_p, C.c_char_p,
+                                C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.ref_stats_json.argtypes = [C.POINTER(A.Stats), C.c_char_p, C.c_char_p, C.c_uint64,
+                                 C.POINTER(C.c_uint64)]
+    L.ref_parse_config.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.ref_run_command.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                  C.c_uint64]
+    L.ref_slab_reflection.argtypes = [_DP, _DP, C.c_int, C.c_double, C.c_int, _DP]
+    L.ref_range_profile.argtypes = [_DP, _DP, C.c_uint32, C.c_int, C.c_int, _DP, _DP, _DP]
+    L.ref_isar.argtypes = [_DP, _DP, C.c_uint32, _DP, C.c_uint32, C.c_int, C.c_int, C.c_double,
+                           _DP, _DP, _DP, _DP]
+    L.ref_plate_rcs.restype = C.c_double
+    L.ref_plate_rcs.argtypes = [C.c_double] * 3
+    L.ref_sphere_go_rcs.restype = C.c_double
+    L.ref_sphere_go_rcs.argtypes = [C.c_double]
+    return L
 
 
 def port() -> C.CDLL:
@@ -271,11 +293,14 @@ def ref_parse_config(text):
     return rc == 0, t
 
 
-def ref_run_command(command, config_text, out_dir, workers=1, seed=None):
-    rc = ref().ref_run_command(command.encode(), config_text.encode(), out_dir.encode(), workers,
+def ref_run_command(command, config_text, out_dir, workers=1, seed=None, lib=None):
+    """run_command (runner.cpp:437-452) of the CPU reference, or of ``lib``
+    (e.g. ``dropin()``: the same code with the solvers on the GPU)."""
+    L = lib or ref()
+    rc = L.ref_run_command(command.encode(), config_text.encode(), out_dir.encode(), workers,
                                0 if seed is None else 1, 0 if seed is None else seed)
     if rc < 0:
-        raise RuntimeError(ref().ref_last_error().decode())
+        raise RuntimeError(L.ref_last_error().decode())
     return rc
 
 
