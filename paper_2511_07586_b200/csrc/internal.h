@@ -27,7 +27,10 @@
 namespace mcsbr_int {
 
 constexpr int kStackSize = 96;  // >= 3 pushes per 4-wide level
-constexpr int kLeafMax = 4;
+#ifndef MCSBR_LEAF_MAX
+#define MCSBR_LEAF_MAX 2  // measured: 2 beats 1, 3, 4 on c1-c5 (fp64 triangle tests cost more than node visits)
+#endif
+constexpr int kLeafMax = MCSBR_LEAF_MAX;
 
 struct SceneView {
     const float4* nodes;

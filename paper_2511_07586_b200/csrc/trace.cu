@@ -51,6 +51,7 @@ struct FRay {
     float ix, iy, iz;     // 1/dir (fp32, zero components clamped)
     float oix, oiy, oiz;  // origin * inv, origin in the scene-centred frame
     double t_skip;       // parameter of the traversal origin along the fp64 ray
+    int oct;              // ray octant: bit a set iff inv component a < 0
 };
 
 // fp32 reciprocal of a direction component (relative error ~1e-7, covered by
@@ -88,7 +89,33 @@ __device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool o
     r.oix = __fmul_rn(__double2float_rn(ot.x), r.ix);
     r.oiy = __fmul_rn(__double2float_rn(ot.y), r.iy);
     r.oiz = __fmul_rn(__double2float_rn(ot.z), r.iz);
+    r.oct = (r.ix < 0.0f ? 1 : 0) | (r.iy < 0.0f ? 2 : 0) | (r.iz < 0.0f ? 4 : 0);
     return r;
+}
+
+// 3-input fp32 min / max (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// Slab test with the near / far planes already chosen by the ray octant
+// (the caller loads lo or hi per axis by address).  Because fma rounding is
+// monotonic and lo <= hi, the near-plane distance equals min(t_lo, t_hi) of
+// the symmetric form bit for bit, so culling is identical.
+__device__ __forceinline__ float slab_nf(const FRay& r, float nx, float fx, float ny, float fy, float nz,
+                                         float fz, float tmax) {
+    const float tn = fmax3(__fmaf_rn(nx, r.ix, -r.oix), __fmaf_rn(ny, r.iy, -r.oiy),
+                           fmaxf(__fmaf_rn(nz, r.iz, -r.oiz), 0.0f));
+    const float tf = fmin3(__fmaf_rn(fx, r.ix, -r.oix), __fmaf_rn(fy, r.iy, -r.oiy),
+                           fminf(__fmaf_rn(fz, r.iz, -r.oiz), tmax));
+    return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
 // slab test of one child box against [0, tmax]; returns entry distance or +inf
@@ -183,6 +210,7 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             // 4-wide node: 128 B, boxes SoA by axis (bvh.cu emit4_kernel)
             MCSBR_STAT(0);
             const float4* nd = S.nodes + 8ll * ref;
+#ifdef MCSBR_SLAB_MINMAX
             const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
             const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5), rf = __ldg(nd + 6), nc = __ldg(nd + 7);
             const int cnt = __float_as_int(nc.x);
@@ -191,6 +219,20 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             float t1 = slab(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmax);
             float t2 = cnt > 2 ? slab(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmax) : inf;
             float t3 = cnt > 3 ? slab(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmax) : inf;
+#else
+            // near planes at (lo | octant bit) per axis, far planes at the other
+            const int ox = r.oct & 1, oy = (r.oct >> 1) & 1, oz = (r.oct >> 2) & 1;
+            const float4 nx = __ldg(nd + ox), fx = __ldg(nd + (ox ^ 1));
+            const float4 ny = __ldg(nd + 2 + oy), fy = __ldg(nd + 2 + (oy ^ 1));
+            const float4 nz = __ldg(nd + 4 + oz), fz = __ldg(nd + 4 + (oz ^ 1));
+            const float4 rf = __ldg(nd + 6), nc = __ldg(nd + 7);
+            const int cnt = __float_as_int(nc.x);
+            const float inf = __int_as_float(0x7f800000);
+            float t0 = slab_nf(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
+            float t1 = slab_nf(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
+            float t2 = cnt > 2 ? slab_nf(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax) : inf;
+            float t3 = cnt > 3 ? slab_nf(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax) : inf;
+#endif
             int c0 = __float_as_int(rf.x), c1 = __float_as_int(rf.y), c2 = __float_as_int(rf.z),
                 c3 = __float_as_int(rf.w);
             // sort the 4 (entry, child) pairs: network (0,1)(2,3)(0,2)(1,3)(1,2)
