@@ -1,0 +1,50 @@
+"""One warm-up + one timed launch of an ISAR config (c4 or c5) for ncu, with
+the per-path counters that explain its cost.
+
+    python tools/profile_isar.py c4|c5 [--angles N]
+ncu: --set full -k regex:path_kernel -s 1 -c 1 (the second path_kernel launch).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import bench_configs as B  # noqa: E402
+import numpy as np  # noqa: E402
+
+import paper_2511_07586_b200 as M  # noqa: E402
+from paper_2511_07586_b200.geometry import airframe  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("config", choices=["c4", "c5"])
+ap.add_argument("--angles", type=int, default=8)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+if a.config == "c4":
+    sd, _ = airframe(200_000, seed=4)
+    cfg = M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, max_bounce=10, seed=4)
+    freqs, n_az, half, rays = np.linspace(9.5e9, 10.5e9, 64), 64, 3.0, 2e6
+else:
+    sd, _ = airframe(1_000_000, seed=5, dielectric_skin=True)
+    cfg = M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, max_bounce=24, seed=5,
+                     roulette=M.RouletteConfig(enabled=True, q=0.5, min_bounce=3))
+    freqs, n_az, half, rays = np.linspace(8e9, 12e9, 128), 128, 5.0, 16e6
+s = M.Scene(sd)
+lam = B.C0 / freqs[-1]
+az = np.linspace(-half, half, n_az)
+sel = az[np.linspace(0, n_az - 1, a.angles).round().astype(int)]
+excs = [M.monostatic_excitation(90.0, float(x)) for x in sel]
+spws = [B.spw_for(s, e, lam, rays) for e in excs]
+for _ in range(a.reps):
+    vals, st = M.estimate_batch(s, list(zip(excs, spws)), [[e] for e in excs], freqs, cfg)
+N = st.rays_launched
+print(json.dumps({"config": a.config, "angles": len(excs), "paths": N, "kernel_ms": st.kernel_ms,
+                  "paths_per_s": N / st.kernel_ms * 1e3,
+                  "segments_per_path": st.segments_traced / N,
+                  "occlusion_per_path": st.occlusion_queries / N,
+                  "contributions_per_path": st.contributions / N,
+                  "rays_per_bounce": list(st.rays_per_bounce[:12])}))
