@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -223,6 +224,11 @@ mcsbr_mc_config det_as_mc(const mcsbr_det_config* d) {
     return c;
 }
 
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
 constexpr uint64_t kPathStateBytes = 192;  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
 
 struct Job {
@@ -230,9 +236,9 @@ struct Job {
     std::vector<RxDev> rx;
     std::vector<double> k0;
     uint32_t n_rx = 1;
-    uint64_t total_tiles = 0;
-    uint32_t tile_entries = 0;
     uint64_t total_entries = 0;
+    int uniform_f = 0;
+    double kph0 = 0.0, kdph = 0.0;
 };
 
 // Plan all incidences of a batch for one shard.
@@ -286,17 +292,25 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
         }
     }
     job->total_entries = total;
-    // tile size: enough tiles for ~8 per warp, 64..4096 entries, multiple of 32
-    uint64_t t = total / (static_cast<uint64_t>(std::max(warps_hint, 1)) * 8);
-    t = (t + 31) / 32 * 32;
-    t = std::min<uint64_t>(std::max<uint64_t>(t, 64), 4096);
-    job->tile_entries = static_cast<uint32_t>(t);
-    uint64_t tiles = 0;
+    uint64_t g = 0;
     for (auto& d : job->inc) {
-        d.tile_begin = tiles;
-        tiles += (d.entry_end - d.entry_begin + t - 1) / t;
+        d.g_begin = g;
+        g += d.entry_end - d.entry_begin;
     }
-    job->total_tiles = tiles;
+    // uniform grid test of SweepAccumulator (farfield.cpp:87-104)
+    job->uniform_f = 0;
+    if (nf >= 2) {
+        const double df = freqs[1] - freqs[0];
+        bool uni = true;
+        for (uint32_t i = 1; i < nf; ++i)
+            if (std::abs((freqs[i] - freqs[i - 1]) - df) > 1e-6 * std::abs(df)) {
+                uni = false;
+                break;
+            }
+        job->uniform_f = uni ? 1 : 0;
+        job->kph0 = -2.0 * kPi * freqs[0] / kC;
+        job->kdph = -2.0 * kPi * df / kC;
+    }
     return MCSBR_OK;
 }
 
@@ -341,8 +355,15 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     p.sums = d_sums;
     p.counters = d_counters;
     p.tile_counter = s->tile.p;
-    p.total_tiles = job.total_tiles;
-    p.tile_entries = job.tile_entries;
+    p.total_entries = job.total_entries;
+    // scheduling knobs (A/B experiments only; the defaults are the product)
+    p.chunk_max = env_u32("MCSBR_CHUNK_MAX", 256);
+    p.chunk_min = env_u32("MCSBR_CHUNK_MIN", 32);
+    p.gss_div = env_u32("MCSBR_GSS", 16);
+    p.band_order = static_cast<int32_t>(env_u32("MCSBR_BAND", 1));
+    p.uniform_f = job.uniform_f;
+    p.kph0 = job.kph0;
+    p.kdph = job.kdph;
     fill_config(p, cfg);
     if (kernel_ms && !s->ev0) {
         CK(cudaEventCreate(&s->ev0), "cudaEventCreate");

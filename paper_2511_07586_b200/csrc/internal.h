@@ -58,7 +58,7 @@ struct IncDev {
     int32_t nu, nv;
     uint64_t entry_begin;     // this shard's entry range [begin, end)
     uint64_t entry_end;
-    uint64_t tile_begin;      // first global tile index of this incidence
+    uint64_t g_begin;         // index of entry_begin in the job's flattened entry space
     uint64_t _pad;
 };
 
@@ -95,9 +95,17 @@ struct TraceParams {
     int occlusion;
     double* sums;           // [n_inc][n_rx][nf][4] complex (re, im)
     unsigned long long* counters;
-    unsigned long long* tile_counter;
-    uint64_t total_tiles;
-    uint32_t tile_entries;
+    unsigned long long* tile_counter;  // global cursor over the flattened entry space
+    uint64_t total_entries;            // entries of all incidences (this shard)
+    uint32_t chunk_max;                // largest chunk a warp takes at once
+    uint32_t chunk_min;                // smallest chunk (multiple of 32)
+    uint32_t gss_div;                  // chunk = remaining / (gss_div * warps); 0 = always chunk_max
+    int32_t band_order;                // dispatch order of launch entries (trace.cu locate)
+    // uniform frequency grid (SweepAccumulator::uniform_, farfield.cpp:87-104):
+    // phase of frequency i is (kph0 + i * kdph) * s, kph0 = -2 pi f0 / c,
+    // kdph = -2 pi df / c, exactly the reference's operation order
+    int32_t uniform_f;
+    double kph0, kdph;
     // McConfig
     uint32_t spp;
     uint64_t seed;

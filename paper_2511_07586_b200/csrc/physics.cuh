@@ -104,6 +104,14 @@ __device__ __forceinline__ Cx phasor(double k0, double s) {
     sincos(-k0 * s, &sn, &cs);
     return {cs, sn};
 }
+// e^{la} (cos ph + j sin ph); la = 0 for the lossless model
+__device__ __forceinline__ Cx polar_la(double ph, double la) {
+    double sn, cs;
+    sincos(ph, &sn, &cs);
+    if (la == 0.0) return {cs, sn};
+    const double a = exp(la);
+    return {cs * a, sn * a};
+}
 __device__ __forceinline__ Cx phasor(double k0, Cx s) {
     double sn, cs;
     sincos(-k0 * s.re, &sn, &cs);

@@ -26,6 +26,8 @@
 // l, l+32, ... (fp64 phase, sincos) into its own slots, flushed with atomics
 // once per tile.
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <type_traits>
 
 #include "dmath.cuh"
@@ -408,14 +410,53 @@ __device__ __forceinline__ double draw(const TraceParams& P, const Path<NT>& s, 
     return philox_uniform(P.seed, s.key, static_cast<uint32_t>(bounce), static_cast<uint32_t>(purpose));
 }
 
+// A launch entry located on the strata grid (solver_mc.cpp:117-125):
+// entry = cell * spp + sample, cell = j * nu + i.
+struct Entry {
+    uint64_t entry;
+    uint32_t cell, sample, i, j;
+};
+
+// Dispatch order -> launch entry.  Warps take consecutive dispatch indices d.
+// Linear order: d is the entry itself.  Band order walks the strata grid in
+// bands of 4 rows, column by column, so a warp's 32 lanes get an 8 x 4 patch
+// of cells instead of a 32-cell line.  Both are bijections on
+// [0, nu*nv*spp): every entry, RNG key and contribution is unchanged; only
+// the order lanes take them in is.  32-bit index math (nu*nv < 2^32, like
+// the cell index of the reference's keys).
+__device__ __forceinline__ Entry locate(const TraceParams& P, const IncDev& I, uint64_t d) {
+    uint32_t cg, smp = 0;
+    if (P.spp == 1) {
+        cg = static_cast<uint32_t>(d);
+    } else {
+        cg = static_cast<uint32_t>(d / P.spp);
+        smp = static_cast<uint32_t>(d - static_cast<uint64_t>(cg) * P.spp);
+    }
+    const uint32_t nu = static_cast<uint32_t>(I.nu), nv = static_cast<uint32_t>(I.nv);
+    Entry e;
+    if (P.band_order) {
+        const uint32_t band = cg / (4u * nu);
+        const uint32_t r = cg - band * 4u * nu;
+        const uint32_t h = min(4u, nv - 4u * band);
+        const uint32_t col = h == 4u ? (r >> 2) : r / h;
+        e.i = col;
+        e.j = 4u * band + (r - col * h);
+    } else {
+        e.j = cg / nu;
+        e.i = cg - e.j * nu;
+    }
+    e.cell = e.j * nu + e.i;
+    e.sample = smp;
+    e.entry = static_cast<uint64_t>(e.cell) * P.spp + smp;
+    return e;
+}
+
 // sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
 template <typename NT>
 __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
-                                          uint64_t entry, Path<NT>& s) {
-    const uint32_t cell = static_cast<uint32_t>(entry / P.spp);
-    const uint32_t sample = static_cast<uint32_t>(entry % P.spp);
-    const uint32_t i = cell % static_cast<uint32_t>(I.nu);
-    const uint32_t j = cell / static_cast<uint32_t>(I.nu);
+                                          const Entry& en, Path<NT>& s) {
+    const uint32_t cell = en.cell, sample = en.sample, i = en.i, j = en.j;
+    const uint64_t entry = en.entry;
     double ju = 0.5, jv = 0.5;
     if (P.rng_mode == MCSBR_RNG_REFERENCE) {
         s.key = counter_prefix(P.seed, cell, sample);
@@ -538,13 +579,22 @@ enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
+// Instantiations whose shared memory already limits residency to 3 blocks per
+// SM (F > 1 per-warp accumulators, lossy state) may use the registers of 3.
+#ifndef MCSBR_SMEM_MIN_BLOCKS
+#define MCSBR_SMEM_MIN_BLOCKS 4
+#endif
+template <int kMode, bool kLossy>
+struct MinBlocks {
+    static constexpr int value = (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS : MCSBR_MIN_BLOCKS;
+};
 // kDet: the deterministic solver (solver_det.cpp:30-174) on the same engine:
 // midpoint launch (P.jitter = 0, spp = 1), no draws; at a two-branch hit the
 // reflect child continues in registers and the transmit child goes on the
 // lane's branch stack; a dead lane pops its own stack before it takes a new
 // entry, which reproduces the reference's depth-first, reflect-first order.
 template <int kMode, bool kDiel, bool kLossy, bool kDet>
-__global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams P) {
+__global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeSmem;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
@@ -554,6 +604,7 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
     // kernel.  Per block and bounce they stay far below 2^32.
     __shared__ unsigned int s_bounce[3 * 64];
     __shared__ double s_state[kSlotFields * kSlotThreads];
+    __shared__ unsigned long long s_sched[kSlotThreads / 32][4];
     for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) s_cnt[i] = 0;
     for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
@@ -580,32 +631,126 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
     uint32_t dev = 0, dpeak = 0;
     uint64_t dacc_peak = 0, dacc_push = 0, dblk = ~0ull;
 
-    for (;;) {
-        // ---- fetch a tile (warp-uniform) ----
-        unsigned long long tile = 0;
-        if (lane == 0) tile = atomicAdd(P.tile_counter, 1ull);
-        tile = __shfl_sync(kFull, tile, 0);
-        if (tile >= P.total_tiles) break;
-        // incidence of this tile: last a with tile_begin[a] <= tile
+    // Work distribution: a global cursor over the job's flattened entry space
+    // (incidence-major).  A warp takes a chunk with one atomicAdd; chunk sizes
+    // shrink as the work runs out (guided self-scheduling: remaining / (2 *
+    // warps), multiple of 32, in [32, chunk_max]) so the last chunks are small
+    // and the warps finish at nearly the same time.  A chunk may span
+    // incidences; it is processed as one sub-range per incidence.  The warp's
+    // phasor accumulators belong to one incidence and are flushed only when
+    // the warp moves to another one (and at the end), not per chunk, and a
+    // warp whose sub-range runs dry takes the next chunk without draining its
+    // lanes when that chunk continues the same incidence.
+    // The warp's scheduling state lives in shared memory (it is touched only
+    // when a sub-range runs dry), not in registers the traversal needs:
+    // q[0], q[1] = fetched, not yet started global range; q[2] = the cursor
+    // value the warp last saw (guides the chunk size; ~0 once exhausted).
+    volatile unsigned long long* q = s_sched[warp];
+    if (lane == 0) {
+        q[0] = 0;
+        q[1] = 0;
+        q[2] = 0;
+    }
+    __syncwarp();
+    auto fetch = [&]() {
+        const unsigned long long seen = q[2];
+        if (seen == ~0ull) return;
+        const uint64_t n_warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+        const uint64_t rem = P.total_entries > seen ? P.total_entries - seen : 0;
+        uint64_t c = P.gss_div ? rem / (P.gss_div * n_warps) : P.chunk_max;
+        c = (c + 31) & ~31ull;
+        c = c < P.chunk_min ? P.chunk_min : (c > P.chunk_max ? P.chunk_max : c);
+        if (lane == 0) {
+            const unsigned long long g = atomicAdd(P.tile_counter, static_cast<unsigned long long>(c));
+            if (g >= P.total_entries) {
+                q[2] = ~0ull;
+            } else {
+                q[2] = g + c;
+                q[0] = g;
+                q[1] = min(static_cast<uint64_t>(g + c), P.total_entries);
+            }
+        }
+        __syncwarp();
+    };
+    // incidence containing global entry g: last a with g_begin[a] <= g
+    auto find_inc = [&](uint64_t g) {
         uint32_t lo = 0, hi = P.n_inc;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (P.inc[mid].tile_begin <= tile) lo = mid; else hi = mid;
+            if (P.inc[mid].g_begin <= g) lo = mid; else hi = mid;
         }
-        const uint32_t a = lo;
+        return lo;
+    };
+    uint32_t cur_a = 0xffffffffu;  // incidence the accumulators hold (warp-uniform)
+    if (kRegAcc) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sl.set(kFAcc + k, 0.0);
+    }
+    // add the warp's accumulators into incidence cur_a's sums and clear them
+    auto flush = [&]() {
+        if (cur_a == 0xffffffffu) return;
+        if (kMode == kModeFan) {
+            const uint32_t rx = P.rx_index + static_cast<uint32_t>(lane);
+            if (rx < P.n_rx) {  // lane-owned receiver: nf == 1, no warp reduction
+                double* o = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + rx) * 8;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double v = sl.get(kFAcc + k);
+                    if (v != 0.0) atomicAdd(o + k, v);
+                    sl.set(kFAcc + k, 0.0);
+                }
+            }
+        } else if (kRegAcc) {
+            double* out = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + P.rx_index) * 8;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                double re = sl.get(kFAcc + 2 * ch), im = sl.get(kFAcc + 2 * ch + 1);
+                sl.set(kFAcc + 2 * ch, 0.0);
+                sl.set(kFAcc + 2 * ch + 1, 0.0);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    re += __shfl_xor_sync(kFull, re, o);
+                    im += __shfl_xor_sync(kFull, im, o);
+                }
+                if (lane == 0) {
+                    if (re != 0.0) atomicAdd(out + 2 * ch, re);
+                    if (im != 0.0) atomicAdd(out + 2 * ch + 1, im);
+                }
+            }
+        } else {
+            double* out = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + P.rx_index) * P.nf * 8;
+            __syncwarp();
+            for (uint32_t i = lane; i < P.nf * 8; i += 32) {
+                const double v = wacc[i];
+                if (v != 0.0) atomicAdd(out + i, v);
+                wacc[i] = 0.0;
+            }
+            __syncwarp();
+        }
+    };
+
+    for (;;) {
+        // ---- next sub-range (warp-uniform) ----
+        if (q[0] >= q[1]) fetch();
+        const uint64_t q0 = q[0], q1 = q[1];
+        if (q0 >= q1) break;
+        const uint32_t a = find_inc(q0);
         const IncDev& I = P.inc[a];
-        const uint64_t e_begin = I.entry_begin + (tile - I.tile_begin) * P.tile_entries;
-        const uint64_t e_end = min(e_begin + P.tile_entries, I.entry_end);
+        const uint64_t g_end_a = I.g_begin + (I.entry_end - I.entry_begin);
+        uint64_t cursor = I.entry_begin + (q0 - I.g_begin);  // warp-uniform
+        uint64_t e_end = I.entry_begin + (min(q1, g_end_a) - I.g_begin);
+        __syncwarp();
+        if (lane == 0) q[0] = min(q1, g_end_a);
+        __syncwarp();
+        if (a != cur_a) {
+            flush();
+            cur_a = a;
+        }
         // fan mode: lane l evaluates receiver rx_index + l (if it exists)
         const uint32_t my_rx = P.rx_index + (kMode == kModeFan ? static_cast<uint32_t>(lane) : 0u);
         const bool has_rx = my_rx < P.n_rx;
         const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + (has_rx ? my_rx : P.rx_index)];
-        uint64_t cursor = e_begin;  // warp-uniform
 
-        if (kRegAcc) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) sl.set(kFAcc + k, 0.0);
-        }
         bool alive = false;  // lane holds a path (possibly only its last occlusion query)
         bool pend = false;   // next query is the chi occlusion test of a contribution
         bool dying = false;  // the path ends once its pending occlusion test is done
@@ -629,11 +774,23 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
             }
             // ---- regenerate dead lanes from the tile ----
             const unsigned need = __ballot_sync(kFull, !alive);
+            if (need && cursor >= e_end) {
+                // sub-range dry: continue with the next chunk if it is the same incidence
+                if (q[0] >= q[1]) fetch();
+                const uint64_t n0 = q[0], n1 = q[1];
+                if (n0 < n1 && n0 >= I.g_begin && n0 < g_end_a) {
+                    cursor = I.entry_begin + (n0 - I.g_begin);
+                    e_end = I.entry_begin + (min(n1, g_end_a) - I.g_begin);
+                    __syncwarp();
+                    if (lane == 0) q[0] = min(n1, g_end_a);
+                    __syncwarp();
+                }
+            }
             if (need && cursor < e_end) {
                 const unsigned rank = __popc(need & ((1u << lane) - 1u));
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
-                    init_path(P, I, a, mine, s);
+                    init_path(P, I, a, locate(P, I, mine), s);
                     save_em(sl, s);
                     alive = true;
                     ++n_launched;
@@ -940,6 +1097,18 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                 // ---- phasor accumulation (farfield.cpp:130-146) ----
                 if (visible) acc_add(sl, amp, phasor(P.k0[0], s_path));
             } else {
+                // Uniform grids (the reference's own test, farfield.cpp:87-104):
+                // frequency i has phase (kph0 + i kdph) s.  Lane l evaluates
+                // frequency l directly and steps to l + 32, l + 64, ... with
+                // W = e^{-j 32 dk s}, which each contribution's own lane
+                // computes once before the broadcast.  Non-uniform grids
+                // evaluate every frequency directly (farfield.cpp:140-146).
+                // The 4-channel phasor sums use fused multiply-adds (their
+                // summation order already differs from the reference's).
+                const bool step32 = P.uniform_f && P.nf > 32;
+                Cx w32 = {1.0, 0.0};
+                if (visible && step32) w32 = polar_la(32.0 * (P.kdph * re_of(s_path)),
+                                                      -(32.0 * (P.kdph * im_of(s_path))));
                 unsigned vm = __ballot_sync(kFull, visible);
                 while (vm) {
                     const int src = __ffs(vm) - 1;
@@ -951,62 +1120,46 @@ __global__ void __launch_bounds__(128, MCSBR_MIN_BLOCKS) path_kernel(TraceParams
                         am[ch].im = shfl_d(amp[ch].im, src);
                     }
                     const NT sp = shfl_nt(s_path, src);
-                    for (uint32_t f = lane; f < P.nf; f += 32) {
-                        const Cx z = phasor(P.k0[f], sp);
+                    const Cx w = {shfl_d(w32.re, src), shfl_d(w32.im, src)};
+                    if (static_cast<uint32_t>(lane) >= P.nf) continue;  // no shuffles below
+                    Cx z;
+                    if (P.uniform_f) {
+                        const double ph0 = P.kph0 * re_of(sp), dph = P.kdph * re_of(sp);
+                        const double la0 = -(P.kph0 * im_of(sp)), dla = -(P.kdph * im_of(sp));
+                        z = polar_la(ph0 + static_cast<double>(lane) * dph,
+                                     la0 + static_cast<double>(lane) * dla);
+                    } else {
+                        z = phasor(P.k0[lane], sp);
+                    }
+                    for (uint32_t f = lane;;) {
                         double* slot = wacc + f * 8;
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
-                            const Cx v = am[ch] * z;
-                            slot[2 * ch] += v.re;
-                            slot[2 * ch + 1] += v.im;
+                            slot[2 * ch] = __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, slot[2 * ch]));
+                            slot[2 * ch + 1] =
+                                __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, slot[2 * ch + 1]));
+                        }
+                        f += 32;
+                        if (f >= P.nf) break;
+                        if (step32) {
+                            z = {__fma_rn(z.re, w.re, -z.im * w.im), __fma_rn(z.re, w.im, z.im * w.re)};
+                        } else {
+                            z = phasor(P.k0[f], sp);
                         }
                     }
                 }
             }
         }
 
-        if (kDet) {  // every root of the tile is finished
+        if (kDet) {  // every root of the sub-range is finished
             dacc_peak += dpeak;
             dpeak = 0;
             det_flush(P, dblk, dacc_peak, dacc_push);
             dacc_peak = dacc_push = 0;
             dblk = ~0ull;
         }
-        // ---- flush the tile's accumulators ----
-        double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
-        if (kMode == kModeFan) {
-            if (has_rx) {  // lane-owned receiver: nf == 1, no warp reduction
-                double* o = P.sums + (static_cast<size_t>(a) * P.n_rx + my_rx) * 8;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double v = sl.get(kFAcc + k);
-                    if (v != 0.0) atomicAdd(o + k, v);
-                }
-            }
-        } else if (kRegAcc) {
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                double re = sl.get(kFAcc + 2 * ch), im = sl.get(kFAcc + 2 * ch + 1);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    re += __shfl_xor_sync(kFull, re, o);
-                    im += __shfl_xor_sync(kFull, im, o);
-                }
-                if (lane == 0) {
-                    atomicAdd(out + 2 * ch, re);
-                    atomicAdd(out + 2 * ch + 1, im);
-                }
-            }
-        } else {
-            __syncwarp();
-            for (uint32_t i = lane; i < P.nf * 8; i += 32) {
-                const double v = wacc[i];
-                if (v != 0.0) atomicAdd(out + i, v);
-                wacc[i] = 0.0;
-            }
-            __syncwarp();
-        }
     }
+    flush();
 
     // ---- counters ----
     auto wsum = [](uint64_t v) {
@@ -1078,8 +1231,9 @@ static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
+    if (const char* v = std::getenv("MCSBR_BLOCKS_PER_SM")) per_sm = std::min(per_sm, std::max(1, std::atoi(v)));
     uint64_t blocks = static_cast<uint64_t>(device_sms) * per_sm;
-    const uint64_t max_blocks = (p.total_tiles + threads / 32 - 1) / (threads / 32);
+    const uint64_t max_blocks = (p.total_entries + 1023) / 1024;  // >= 8 entries per lane
     if (blocks > max_blocks) blocks = max_blocks;
     if (kDet && blocks * threads > p.det_threads) blocks = p.det_threads / threads;  // stack capacity
     if (blocks < 1) blocks = 1;

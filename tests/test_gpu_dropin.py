@@ -15,6 +15,7 @@ config -- CPU reference vs drop-in -- and the artifacts are compared:
 """
 import json
 import os
+import re
 
 import numpy as np
 import pytest
@@ -150,11 +151,19 @@ def test_isar_command(tmp_path):
     assert np.array_equal(ga[:, 0], gb[:, 0])  # down-range axis
     assert np.abs(ga[:, 1:] - gb[:, 1:]).max() < 1e-6
     pa, pb = _read(a, "isar.pgm", "rb"), _read(b, "isar.pgm", "rb")
-    assert len(pa) == len(pb)
-    hdr = pa.index(b"255\n") + 4
-    assert pa[:hdr].split(b"\n")[-3:] == pb[:hdr].split(b"\n")[-3:]  # size + maxval
-    xa = np.frombuffer(pa[hdr:], np.uint8).astype(int)
-    xb = np.frombuffer(pb[hdr:], np.uint8).astype(int)
+    ha, hb = pa.index(b"255\n") + 4, pb.index(b"255\n") + 4
+    la, lb = pa[:ha].split(b"\n"), pb[:hb].split(b"\n")
+    assert la[-3:] == lb[-3:]  # size + maxval
+    # comment lines carry full-precision doubles (dB window, extents): the
+    # sums agree to ~1e-15, so their printed digits may differ in the last place
+    num = re.compile(rb"-?\d+\.?\d*(?:e[-+]?\d+)?")
+    for ca, cb in zip(la[1:-3], lb[1:-3]):
+        assert num.sub(b"#", ca) == num.sub(b"#", cb)
+        assert np.allclose([float(x) for x in num.findall(ca)], [float(x) for x in num.findall(cb)],
+                           rtol=1e-9, atol=1e-9)
+    xa = np.frombuffer(pa[ha:], np.uint8).astype(int)
+    xb = np.frombuffer(pb[hb:], np.uint8).astype(int)
+    assert len(xa) == len(xb)
     assert np.abs(xa - xb).max() <= 1
     _compare_json(a, b, "manifest.json")
 
