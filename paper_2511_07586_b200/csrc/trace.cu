@@ -342,10 +342,23 @@ struct Path {
 // registers under the 128-register budget).  Accesses go through a volatile
 // pointer so the compiler re-reads the slot instead of keeping copies live.
 constexpr int kSlotThreads = 128;
-enum : int {
-    kFE0 = 0, kFE1 = 6, kFPhi = 12, kFProb = 13, kFWeight = 14, kFMedium = 15,
-    kFAmp = 16, kFSPath = 24, kFAcc = 25, kFPhiIm = 33, kFMediumIm = 34, kFSPathIm = 35,
-    kSlotFields = 36,
+// Slot layout per instantiation (field indices in doubles).  kPec: every
+// triangle has a PEC side, so a path never branches or leaves the ambient
+// medium -- prob stays exactly 1.0 and medium_n the ambient index, and the
+// two fields are not stored.  kLossy adds the imaginary parts; kRegAcc the
+// register-mode phasor sums.  Every 8 KB of shared memory per block costs
+// ~4-7% (measured) through the L1 capacity it takes: the PEC register-mode
+// slot (31 fields) keeps a block under 32 KB, so 4 blocks fit the 132 KB
+// shared-memory carve-out and leave ~124 KB of L1 per SM.
+template <bool kPec, bool kLossy, bool kRegAcc>
+struct Layout {
+    static constexpr int E0 = 0, E1 = 6, Phi = 12, Weight = 13, Amp = 14, SPath = 22;
+    static constexpr int Prob = 23, Medium = 24;            // !kPec only
+    static constexpr int Im0 = kPec ? 23 : 25;
+    static constexpr int PhiIm = Im0, MediumIm = Im0 + 1, SPathIm = Im0 + 2;  // kLossy only
+    static constexpr int Acc = Im0 + (kLossy ? 3 : 0);       // kRegAcc only
+    static constexpr int Fields = Acc + (kRegAcc ? 8 : 0);
+    static constexpr bool pec = kPec;
 };
 
 struct Slot {
@@ -378,29 +391,37 @@ __device__ __forceinline__ NT slot_get_nt(const Slot& sl, int f, int fim) {
     return make_nt<NT>(sl.get(f), std::is_same<NT, Cx>::value ? sl.get(fim) : 0.0);
 }
 
-template <typename NT>
+template <typename L, typename NT>
 __device__ __forceinline__ void save_em(const Slot& sl, const Path<NT>& s) {
-    sl.setv(kFE0, s.e0);
-    sl.setv(kFE1, s.e1);
-    slot_set_nt(sl, kFPhi, kFPhiIm, s.phi);
-    sl.set(kFProb, s.prob);
-    sl.set(kFWeight, s.weight);
-    slot_set_nt(sl, kFMedium, kFMediumIm, s.medium_n);
+    sl.setv(L::E0, s.e0);
+    sl.setv(L::E1, s.e1);
+    slot_set_nt(sl, L::Phi, L::PhiIm, s.phi);
+    sl.set(L::Weight, s.weight);
+    if (!L::pec) {
+        sl.set(L::Prob, s.prob);
+        slot_set_nt(sl, L::Medium, L::MediumIm, s.medium_n);
+    }
 }
 
-template <typename NT>
-__device__ __forceinline__ void load_em(const Slot& sl, Path<NT>& s) {
-    s.e0 = sl.getv(kFE0);
-    s.e1 = sl.getv(kFE1);
-    s.phi = slot_get_nt<NT>(sl, kFPhi, kFPhiIm);
-    s.prob = sl.get(kFProb);
-    s.weight = sl.get(kFWeight);
-    s.medium_n = slot_get_nt<NT>(sl, kFMedium, kFMediumIm);
+template <typename L, typename NT>
+__device__ __forceinline__ void load_em(const Slot& sl, Path<NT>& s, double ambient_n) {
+    s.e0 = sl.getv(L::E0);
+    s.e1 = sl.getv(L::E1);
+    s.phi = slot_get_nt<NT>(sl, L::Phi, L::PhiIm);
+    s.weight = sl.get(L::Weight);
+    if (L::pec) {
+        s.prob = 1.0;
+        s.medium_n = make_nt<NT>(ambient_n, 0.0);
+    } else {
+        s.prob = sl.get(L::Prob);
+        s.medium_n = slot_get_nt<NT>(sl, L::Medium, L::MediumIm);
+    }
 }
 
+template <int kAcc>
 __device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
 #pragma unroll
-    for (int ch = 0; ch < 4; ++ch) sl.setc(kFAcc + 2 * ch, sl.getc(kFAcc + 2 * ch) + am[ch] * z);
+    for (int ch = 0; ch < 4; ++ch) sl.setc(kAcc + 2 * ch, sl.getc(kAcc + 2 * ch) + am[ch] * z);
 }
 
 template <typename NT>
@@ -598,14 +619,17 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
     constexpr bool kRegAcc = kMode != kModeSmem;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
     extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
-    __shared__ unsigned long long s_cnt[kCntWords];
+    using L = Layout<!kDiel && !kLossy, kLossy, kRegAcc>;
+    constexpr int kFAcc = L::Acc;               // register-mode phasor sums
+    constexpr int kSlotFields = L::Fields;      // doubles per thread
+    __shared__ unsigned long long s_cnt[8];  // launched .. rounds (kCntLaunched..kCntRounds)
     // per-bounce counters as native 32-bit shared atomics (ATOMS.ADD); the
     // 64-bit shared atomicAdd is a CAS loop on sm_100 and cost ~20% of the
     // kernel.  Per block and bounce they stay far below 2^32.
     __shared__ unsigned int s_bounce[3 * 64];
     __shared__ double s_state[kSlotFields * kSlotThreads];
     __shared__ unsigned long long s_sched[kSlotThreads / 32][4];
-    for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < 8; i += blockDim.x) s_cnt[i] = 0;
     for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
     const Slot sl{s_state + threadIdx.x};
@@ -769,7 +793,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
             // ---- deterministic: a dead lane resumes its own pending branch ----
             if (kDet && !alive && dsp > 0) {
                 det_pop(P, gtid, --dsp, s);
-                save_em(sl, s);
+                save_em<L>(sl, s);
                 alive = true;
             }
             // ---- regenerate dead lanes from the tile ----
@@ -791,7 +815,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
                     init_path(P, I, a, locate(P, I, mine), s);
-                    save_em(sl, s);
+                    save_em<L>(sl, s);
                     alive = true;
                     ++n_launched;
                     if (kDet) {  // a new root ray (solver_det.cpp:72-82)
@@ -830,8 +854,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 visible = !hit;
                 if (visible) {  // the queued contribution's amplitudes come back from the slot
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) amp[ch] = sl.getc(kFAmp + 2 * ch);
-                    s_path = slot_get_nt<NT>(sl, kFSPath, kFSPathIm);
+                    for (int ch = 0; ch < 4; ++ch) amp[ch] = sl.getc(L::Amp + 2 * ch);
+                    s_path = slot_get_nt<NT>(sl, L::SPath, L::SPathIm);
                 }
                 if (dying) {
                     alive = false;
@@ -842,7 +866,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 if (!hit) {
                     alive = false;  // escaped
                 } else {
-                    load_em(sl, s);
+                    load_em<L>(sl, s, S.ambient_n);
                     const V3 point = s.origin + s.dir * t;
                     const HitInfo<NT> h = fill_hit<NT>(S, id, s.dir);
                     // advance (path_engine.cpp:17-21); complex in lossy media
@@ -1026,7 +1050,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                             }
                         }
                     }
-                    save_em(sl, s);
+                    save_em<L>(sl, s);
                 }
                 // ---- chi visibility (farfield.cpp:63-68): queue the occlusion query ----
                 if (candidate && kMode == kModeFan) {
@@ -1035,8 +1059,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                     if (P.occlusion) {
                         pend = true;
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) sl.setc(kFAmp + 2 * ch, amp[ch]);
-                        slot_set_nt(sl, kFSPath, kFSPathIm, s_path);
+                        for (int ch = 0; ch < 4; ++ch) sl.setc(L::Amp + 2 * ch, amp[ch]);
+                        slot_set_nt(sl, L::SPath, L::SPathIm, s_path);
                         if (!alive) {
                             alive = true;
                             dying = true;
@@ -1089,13 +1113,13 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         }
                         if (vis) {
                             ++n_contrib;
-                            acc_add(sl, am, phasor(P.k0[0], sp));
+                            acc_add<kFAcc>(sl, am, phasor(P.k0[0], sp));
                         }
                     }
                 }
             } else if (kRegAcc) {
                 // ---- phasor accumulation (farfield.cpp:130-146) ----
-                if (visible) acc_add(sl, amp, phasor(P.k0[0], s_path));
+                if (visible) acc_add<kFAcc>(sl, amp, phasor(P.k0[0], s_path));
             } else {
                 // Uniform grids (the reference's own test, farfield.cpp:87-104):
                 // frequency i has phase (kph0 + i kdph) s.  Lane l evaluates
@@ -1184,18 +1208,21 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
         atomicMax(&s_cnt[kCntRounds], static_cast<unsigned long long>(round_w));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) {
-        const int dst = i < 64 ? kCntRaysPerBounce + i : (i < 128 ? kCntRouletteCand + i - 64
-                                                                  : kCntRouletteSurv + i - 128);
-        s_cnt[dst] += s_bounce[i];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kCntWords; i += blockDim.x) {
-        const unsigned long long v = s_cnt[i];
+    for (int i = threadIdx.x; i < 8 + 3 * 64; i += blockDim.x) {
+        unsigned long long v;
+        int dst;
+        if (i < 8) {
+            v = s_cnt[i];
+            dst = i;
+        } else {
+            const int j = i - 8;
+            v = s_bounce[j];
+            dst = j < 64 ? kCntRaysPerBounce + j : (j < 128 ? kCntRouletteCand + j - 64 : kCntRouletteSurv + j - 128);
+        }
         if (!v) continue;
-        if (i == kCntFault) atomicOr(P.counters + i, v);
-        else if (i == kCntRounds) atomicMax(P.counters + i, v);
-        else atomicAdd(P.counters + i, v);
+        if (dst == kCntFault) atomicOr(P.counters + dst, v);
+        else if (dst == kCntRounds) atomicMax(P.counters + dst, v);
+        else atomicAdd(P.counters + dst, v);
     }
 }
 
@@ -1255,7 +1282,8 @@ static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int thre
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
     const int mode = (p.fan && !p.det) ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
-    const size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
+    size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
+    if (const char* v = std::getenv("MCSBR_EXTRA_SMEM")) smem += std::strtoul(v, nullptr, 10);  // A/B only
     // three physics instantiations: all-PEC (dielectric code compiled out),
     // the reference's lossless dielectric model (bit-exact), lossy media
     cudaError_t e = p.scene.lossy     ? launch_kind<true, true>(mode, p, device_sms, threads, smem, stream)

@@ -1,3 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 1500 python tools/ab.py --c2 --configs c1,c3,c4,c5 --reps 2 \
-  band= lin=,MCSBR_BAND=0 m128=,MCSBR_CHUNK_MAX=128 g32=,MCSBR_GSS=32 lin_m512=,MCSBR_BAND=0,MCSBR_CHUNK_MAX=512 s3=s3 old=old
+timeout 1500 python tools/ab.py --c2 --configs c1,c3,c4,c5 --reps 2 new= prev=prev
