@@ -100,6 +100,14 @@ struct mcsbr_scene {
     double ambient_n = 1.0;
     bool all_pec = false;  // every triangle has a PEC side (kernel specialisation)
     bool lossy = false;    // complex-permittivity transport
+    // deferred accumulation: contribution records per launched entry, learnt
+    // from the peak record count of earlier F > 1 jobs on this scene (read
+    // back asynchronously: peak_host is valid once peak_ev has completed)
+    double rec_ratio = 0.25;
+    unsigned long long* peak_host = nullptr;
+    cudaEvent_t peak_ev = nullptr;
+    uint64_t peak_entries = 0;
+    bool peak_pending = false;
     double* d_nim = nullptr;
     double* d_vtx = nullptr;
     uint4* d_tri = nullptr;
@@ -113,6 +121,7 @@ struct mcsbr_scene {
     DevBuf<double> sums;
     DevBuf<unsigned long long> counters;
     DevBuf<unsigned long long> tile;
+    DevBuf<double> recs;  // deferred-accumulation contribution records
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     SceneView view() const {
@@ -229,7 +238,25 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
     return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
 }
 
-constexpr uint64_t kPathStateBytes = 192;  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
+constexpr uint64_t kPathStateBytes = 192;
+constexpr uint64_t kRecCapMax = uint64_t{1} << 25;  // contribution records (96 B each): 3.2 GB
+
+// Fold the peak record count of the scene's previous F > 1 job (if its
+// readback has landed) into the records-per-entry estimate.
+void learn_rec_ratio(mcsbr_scene* s) {
+    if (!s->peak_host) {
+        if (cudaMallocHost(&s->peak_host, sizeof(unsigned long long)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->peak_ev, cudaEventDisableTiming) != cudaSuccess) {
+            s->peak_host = nullptr;
+            return;
+        }
+    }
+    if (!s->peak_pending || cudaEventQuery(s->peak_ev) != cudaSuccess) return;
+    s->peak_pending = false;
+    if (s->peak_entries == 0) return;
+    const double seen = static_cast<double>(*s->peak_host) / static_cast<double>(s->peak_entries);
+    s->rec_ratio = std::min(std::max(seen * 1.25, 1.0 / 64.0), 8.0);
+}  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
 
 struct Job {
     std::vector<IncDev> inc;
@@ -237,6 +264,15 @@ struct Job {
     std::vector<double> k0;
     uint32_t n_rx = 1;
     uint64_t total_entries = 0;
+    // launch groups [a0, a1) of incidences; IncDev::g_begin restarts at 0 in
+    // each.  F > 1 jobs are split into groups of <= kGroupEntries entries so a
+    // launch's contribution records fit the record buffer.
+    struct Group {
+        uint32_t a0, a1;
+        uint64_t entries;
+    };
+    std::vector<Group> groups;
+    uint64_t max_group_entries = 0;
     int uniform_f = 0;
     double kph0 = 0.0, kdph = 0.0;
 };
@@ -292,11 +328,32 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
         }
     }
     job->total_entries = total;
-    uint64_t g = 0;
-    for (auto& d : job->inc) {
-        d.g_begin = g;
-        g += d.entry_end - d.entry_begin;
+    // F > 1: the launch groups are sized so their records fit kRecCapMax
+    uint64_t group_cap = ~uint64_t{0};
+    if (nf > 1) {
+        learn_rec_ratio(const_cast<mcsbr_scene*>(s));
+        group_cap = std::max<uint64_t>(static_cast<uint64_t>(static_cast<double>(kRecCapMax) / s->rec_ratio),
+                                       uint64_t{1} << 20);
+        group_cap = env_u32("MCSBR_GROUP_ENTRIES", static_cast<uint32_t>(std::min<uint64_t>(group_cap, 0xffffffffu)));
     }
+    job->groups.clear();
+    job->max_group_entries = 0;
+    uint64_t g = 0;
+    uint32_t a0 = 0;
+    for (uint32_t a = 0; a < n_inc; ++a) {
+        IncDev& d = job->inc[a];
+        const uint64_t e = d.entry_end - d.entry_begin;
+        if (a > a0 && g + e > group_cap) {
+            job->groups.push_back({a0, a, g});
+            job->max_group_entries = std::max(job->max_group_entries, g);
+            a0 = a;
+            g = 0;
+        }
+        d.g_begin = g;
+        g += e;
+    }
+    job->groups.push_back({a0, n_inc, g});
+    job->max_group_entries = std::max(job->max_group_entries, g);
     // uniform grid test of SweepAccumulator (farfield.cpp:87-104)
     job->uniform_f = 0;
     if (nf >= 2) {
@@ -336,7 +393,18 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     CK(s->inc.reserve(job.inc.size()), "cudaMalloc(incidences)");
     CK(s->rx.reserve(job.rx.size()), "cudaMalloc(receivers)");
     CK(s->k0.reserve(nf), "cudaMalloc(k0)");
-    CK(s->tile.reserve(1), "cudaMalloc(tile counter)");
+    CK(s->tile.reserve(3), "cudaMalloc(tile counter)");  // entry cursor, record count, peak count
+    // deferred accumulation (F > 1): one 96-byte record per visible
+    // contribution; sized for one per launched path of the largest group
+    // (measured c4/c5: ~0.1 per path), overflow falls back to direct atomics
+    const bool defer = nf > 1;
+    uint64_t rec_cap = 0;
+    if (defer) {
+        rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1) + 4096;
+        rec_cap = std::min<uint64_t>(rec_cap, kRecCapMax);
+        rec_cap = env_u32("MCSBR_REC_CAP", static_cast<uint32_t>(rec_cap));
+        CK(s->recs.reserve(rec_cap * 12), "cudaMalloc(contribution records)");
+    }
     CK(cudaMemcpyAsync(s->inc.p, job.inc.data(), sizeof(IncDev) * job.inc.size(), cudaMemcpyHostToDevice,
                        stream), "upload incidences");
     CK(cudaMemcpyAsync(s->rx.p, job.rx.data(), sizeof(RxDev) * job.rx.size(), cudaMemcpyHostToDevice, stream),
@@ -345,17 +413,15 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
        "upload wavenumbers");
     TraceParams p = extra ? *extra : TraceParams{};
     p.scene = s->view();
-    p.inc = s->inc.p;
-    p.n_inc = static_cast<uint32_t>(job.inc.size());
     p.n_rx = job.n_rx;
-    p.rx = s->rx.p;
     p.k0 = s->k0.p;
     p.nf = nf;
     p.occlusion = occlusion;
-    p.sums = d_sums;
     p.counters = d_counters;
     p.tile_counter = s->tile.p;
-    p.total_entries = job.total_entries;
+    p.recs = defer ? s->recs.p : nullptr;
+    p.rec_count = s->tile.p + 1;
+    p.rec_cap = rec_cap;
     // scheduling knobs (A/B experiments only; the defaults are the product)
     p.chunk_max = env_u32("MCSBR_CHUNK_MAX", 256);
     p.chunk_min = env_u32("MCSBR_CHUNK_MIN", 32);
@@ -377,10 +443,27 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     const bool fan = job.n_rx > 1 && trace_fan_supported(nf);
     const uint32_t step = fan ? 32u : 1u;
     p.fan = fan ? 1 : 0;
+    if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
     for (uint32_t r = 0; r < job.n_rx; r += step) {
         p.rx_index = r;
-        CK(cudaMemsetAsync(s->tile.p, 0, sizeof(unsigned long long), stream), "reset tile counter");
-        CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
+        for (const Job::Group& gr : job.groups) {
+            p.inc = s->inc.p + gr.a0;
+            p.n_inc = gr.a1 - gr.a0;
+            p.inc_base = gr.a0;
+            p.rx = s->rx.p + static_cast<size_t>(gr.a0) * job.n_rx;
+            p.sums = d_sums + static_cast<size_t>(gr.a0) * job.n_rx * nf * 8;
+            p.total_entries = gr.entries;
+            CK(cudaMemsetAsync(s->tile.p, 0, 2 * sizeof(unsigned long long), stream), "reset tile counter");
+            CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
+            if (defer) CK(launch_accumulate(p, s->sms, stream, &g_launches), "accumulate launch");
+        }
+    }
+    if (defer && s->peak_host) {  // learn the record ratio for the next job
+        CK(cudaMemcpyAsync(s->peak_host, s->tile.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           stream), "peak record count");
+        CK(cudaEventRecord(s->peak_ev, stream), "cudaEventRecord");
+        s->peak_entries = job.max_group_entries;
+        s->peak_pending = true;
     }
     if (kernel_ms) {
         CK(cudaEventRecord(s->ev1, stream), "cudaEventRecord");
@@ -625,7 +708,10 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->sums.release();
     s->counters.release();
     s->tile.release();
+    s->recs.release();
     if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->peak_ev) cudaEventDestroy(s->peak_ev);
+    if (s->peak_host) cudaFreeHost(s->peak_host);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;

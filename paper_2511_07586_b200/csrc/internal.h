@@ -84,8 +84,9 @@ enum : int {
 
 struct TraceParams {
     SceneView scene;
-    const IncDev* inc;
+    const IncDev* inc;      // this launch's incidences (a group of the job)
     uint32_t n_inc;
+    uint32_t inc_base;      // job index of inc[0] (RNG keys, path log)
     uint32_t n_rx;          // receivers per incidence
     uint32_t rx_index;      // receiver traced by this launch (fan: the first of up to 32)
     int fan;                // bistatic fan mode (nf == 1)
@@ -94,6 +95,10 @@ struct TraceParams {
     uint32_t nf;
     int occlusion;
     double* sums;           // [n_inc][n_rx][nf][4] complex (re, im)
+    // deferred accumulation (F > 1): contribution records of this launch
+    double* recs;                      // [rec_cap][12]: amp[4], s (re, im), incidence
+    unsigned long long* rec_count;
+    uint64_t rec_cap;
     unsigned long long* counters;
     unsigned long long* tile_counter;  // global cursor over the flattened entry space
     uint64_t total_entries;            // entries of all incidences (this shard)
@@ -161,6 +166,8 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
 // trace.cu
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream,
                          uint64_t* launches);
+cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream,
+                              uint64_t* launches);
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,
                              const double* tmin, uint32_t n, int any_hit, double* t_out,
                              uint32_t* id_out, cudaStream_t stream);

@@ -583,11 +583,30 @@ __device__ __forceinline__ void det_flush(const TraceParams& P, uint64_t blk, ui
     atomicAdd(P.det_blocks + 2 * blk + 1, static_cast<unsigned long long>(push));
 }
 
+// e^{-j k_f s} for frequency f: on uniform grids the reference's phase
+// (kph0 + f kdph) s (farfield.cpp:131-139), else k0[f] directly (:140-146)
+template <typename NT>
+__device__ __forceinline__ Cx freq_phasor(const TraceParams& P, uint32_t f, NT s) {
+    if (P.uniform_f) {
+        const double ph0 = P.kph0 * re_of(s), dph = P.kdph * re_of(s);
+        const double la0 = -(P.kph0 * im_of(s)), dla = -(P.kdph * im_of(s));
+        return polar_la(ph0 + static_cast<double>(f) * dph, la0 + static_cast<double>(f) * dla);
+    }
+    return phasor(P.k0[f], s);
+}
+
+constexpr int kRecD2 = 6;  // contribution record: 6 double2 = 96 B (amp[4], s, incidence)
+
 // ---------------------------------------------------------------------------
 // the path kernel
 
 // Accumulation modes:
-//   kModeSmem  one receiver, F > 1: per-warp [F][4] shared-memory phasor sums
+//   kModeDefer one receiver, F > 1: every visible contribution (4 projected
+//              amplitudes, optical path, incidence) is appended to a record
+//              buffer in HBM; accumulate_kernel turns the records into the
+//              [F][4] phasor sums after the launch (deferred accumulation keeps
+//              the path kernel's shared memory -- and so its L1 -- free of
+//              per-warp [F][4] arrays).
 //   kModeReg   one receiver, F = 1: per-lane register sums, warp-reduced per tile
 //   kModeFan   a bistatic fan of up to 32 receivers per launch (P.rx_index is
 //              the first), F = 1: lane l owns receiver rx_index + l; every
@@ -595,13 +614,13 @@ __device__ __forceinline__ void det_flush(const TraceParams& P, uint64_t blk, ui
 //              its receiver's occlusion test and projection (a coherent
 //              32-ray bundle from one exit point), so paths are traced once
 //              per 32 receivers instead of once per receiver.
-enum { kModeSmem = 0, kModeReg = 1, kModeFan = 2 };
+enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2 };
 
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
 #endif
-// Instantiations whose shared memory already limits residency to 3 blocks per
-// SM (F > 1 per-warp accumulators, lossy state) may use the registers of 3.
+// (A/B knob) register budget of the deferred-accumulation and lossy
+// instantiations.
 #ifndef MCSBR_SMEM_MIN_BLOCKS
 #define MCSBR_SMEM_MIN_BLOCKS 4
 #endif
@@ -616,9 +635,8 @@ struct MinBlocks {
 // entry, which reproduces the reference's depth-first, reflect-first order.
 template <int kMode, bool kDiel, bool kLossy, bool kDet>
 __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_kernel(TraceParams P) {
-    constexpr bool kRegAcc = kMode != kModeSmem;
+    constexpr bool kRegAcc = kMode != kModeDefer;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
-    extern __shared__ double smem_acc[];  // kRegAcc ? unused : [warps][nf][4][2]
     using L = Layout<!kDiel && !kLossy, kLossy, kRegAcc>;
     constexpr int kFAcc = L::Acc;               // register-mode phasor sums
     constexpr int kSlotFields = L::Fields;      // doubles per thread
@@ -636,11 +654,6 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    double* wacc = kRegAcc ? nullptr : smem_acc + static_cast<size_t>(warp) * P.nf * 8;
-    if (!kRegAcc) {
-        for (uint32_t i = lane; i < P.nf * 8; i += 32) wacc[i] = 0.0;
-        __syncwarp();
-    }
     const SceneView& S = P.scene;
     uint32_t fault = 0;
     uint64_t n_launched = 0, n_contrib = 0, n_graze = 0, n_cap = 0, n_occ = 0;
@@ -741,15 +754,6 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                     if (im != 0.0) atomicAdd(out + 2 * ch + 1, im);
                 }
             }
-        } else {
-            double* out = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + P.rx_index) * P.nf * 8;
-            __syncwarp();
-            for (uint32_t i = lane; i < P.nf * 8; i += 32) {
-                const double v = wacc[i];
-                if (v != 0.0) atomicAdd(out + i, v);
-                wacc[i] = 0.0;
-            }
-            __syncwarp();
         }
     };
 
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 const unsigned rank = __popc(need & ((1u << lane) - 1u));
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
-                    init_path(P, I, a, locate(P, I, mine), s);
+                    init_path(P, I, a + P.inc_base, locate(P, I, mine), s);
                     save_em<L>(sl, s);
                     alive = true;
                     ++n_launched;
@@ -876,7 +880,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                     max_round = max(max_round, s.bounce);
                     // the deterministic solver counts segments that hit (solver_det.cpp:88-93)
                     if (kDet) atomicAdd(&s_bounce[min(s.bounce - 1, 63)], 1u);
-                    const bool logged = P.plog_tri && a == 0 && s.entry < P.plog_n;
+                    const bool logged = P.plog_tri && a + P.inc_base == 0 && s.entry < P.plog_n;
                     if (logged && static_cast<uint32_t>(s.bounce - 1) < P.plog_stride)
                         P.plog_tri[s.entry * P.plog_stride + (s.bounce - 1)] = id;
                     // branch_outcomes (path_engine.cpp:23-54)
@@ -1121,54 +1125,44 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 // ---- phasor accumulation (farfield.cpp:130-146) ----
                 if (visible) acc_add<kFAcc>(sl, amp, phasor(P.k0[0], s_path));
             } else {
-                // Uniform grids (the reference's own test, farfield.cpp:87-104):
-                // frequency i has phase (kph0 + i kdph) s.  Lane l evaluates
-                // frequency l directly and steps to l + 32, l + 64, ... with
-                // W = e^{-j 32 dk s}, which each contribution's own lane
-                // computes once before the broadcast.  Non-uniform grids
-                // evaluate every frequency directly (farfield.cpp:140-146).
-                // The 4-channel phasor sums use fused multiply-adds (their
-                // summation order already differs from the reference's).
-                const bool step32 = P.uniform_f && P.nf > 32;
-                Cx w32 = {1.0, 0.0};
-                if (visible && step32) w32 = polar_la(32.0 * (P.kdph * re_of(s_path)),
-                                                      -(32.0 * (P.kdph * im_of(s_path))));
-                unsigned vm = __ballot_sync(kFull, visible);
-                while (vm) {
-                    const int src = __ffs(vm) - 1;
-                    vm &= vm - 1;
-                    Cx am[4];
+                // ---- deferred accumulation: append the contribution record ----
+                const unsigned vm = __ballot_sync(kFull, visible);
+                if (vm) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(P.rec_count, static_cast<unsigned long long>(__popc(vm)));
+                    base = __shfl_sync(kFull, base, 0);
+                    const uint64_t slot = base + __popc(vm & ((1u << lane) - 1u));
+                    const bool stored = visible && slot < P.rec_cap;
+                    if (stored) {
+                        double2* r = reinterpret_cast<double2*>(P.recs) + slot * kRecD2;
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        am[ch].re = shfl_d(amp[ch].re, src);
-                        am[ch].im = shfl_d(amp[ch].im, src);
+                        for (int ch = 0; ch < 4; ++ch) r[ch] = make_double2(amp[ch].re, amp[ch].im);
+                        r[4] = make_double2(re_of(s_path), im_of(s_path));
+                        r[5] = make_double2(__longlong_as_double(static_cast<long long>(a)), 0.0);
                     }
-                    const NT sp = shfl_nt(s_path, src);
-                    const Cx w = {shfl_d(w32.re, src), shfl_d(w32.im, src)};
-                    if (static_cast<uint32_t>(lane) >= P.nf) continue;  // no shuffles below
-                    Cx z;
-                    if (P.uniform_f) {
-                        const double ph0 = P.kph0 * re_of(sp), dph = P.kdph * re_of(sp);
-                        const double la0 = -(P.kph0 * im_of(sp)), dla = -(P.kdph * im_of(sp));
-                        z = polar_la(ph0 + static_cast<double>(lane) * dph,
-                                     la0 + static_cast<double>(lane) * dla);
-                    } else {
-                        z = phasor(P.k0[lane], sp);
-                    }
-                    for (uint32_t f = lane;;) {
-                        double* slot = wacc + f * 8;
+                    // buffer full (the host sizes it so this is rare): the warp
+                    // adds each overflowing contribution straight into the sums,
+                    // lanes over frequencies
+                    unsigned om = __ballot_sync(kFull, visible && !stored);
+                    double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
+                    while (om) {
+                        const int src = __ffs(om) - 1;
+                        om &= om - 1;
+                        Cx am[4];
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
-                            slot[2 * ch] = __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, slot[2 * ch]));
-                            slot[2 * ch + 1] =
-                                __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, slot[2 * ch + 1]));
+                            am[ch].re = shfl_d(amp[ch].re, src);
+                            am[ch].im = shfl_d(amp[ch].im, src);
                         }
-                        f += 32;
-                        if (f >= P.nf) break;
-                        if (step32) {
-                            z = {__fma_rn(z.re, w.re, -z.im * w.im), __fma_rn(z.re, w.im, z.im * w.re)};
-                        } else {
-                            z = phasor(P.k0[f], sp);
+                        const NT sp = shfl_nt(s_path, src);
+                        for (uint32_t f = lane; f < P.nf; f += 32) {
+                            const Cx z = freq_phasor(P, f, sp);
+#pragma unroll
+                            for (int ch = 0; ch < 4; ++ch) {
+                                const Cx v = am[ch] * z;
+                                atomicAdd(out + f * 8 + 2 * ch, v.re);
+                                atomicAdd(out + f * 8 + 2 * ch + 1, v.im);
+                            }
                         }
                     }
                 }
@@ -1226,6 +1220,123 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// K4b: deferred phasor accumulation (SweepAccumulator::add, farfield.cpp:130-146)
+//
+// Each warp owns a contiguous span of contribution records (>= 512, so its
+// flushes cost < 1 atomic per record and channel) and keeps the [FPL][4]
+// complex sums of its 32 x FPL frequencies in registers: lane l holds
+// frequencies f_begin + l + 32 m.  Records are staged 32 at a time through
+// shared memory; for each, the staging lane precomputes the phase terms and
+// W = e^{-j 32 dk s} (one sincos per record), so an accumulating lane pays one
+// sincos per record for its first frequency and steps to the next with one
+// complex multiply.  Non-uniform grids evaluate every frequency directly.
+// Sums use fused multiply-adds (their order differs from the reference's
+// anyway); the records of one span are nearly always one incidence, and the
+// sums are flushed with fp64 atomics whenever the incidence changes.
+template <int FPL>
+__global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t f_begin) {
+    __shared__ double2 st[4][32][8];  // amp[4], (ph0, dph) | s, (la0, dla), W, incidence
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t n_all = *P.rec_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(P.rec_count + 1, n_all);  // peak for the host
+    const uint64_t n = min(n_all, P.rec_cap);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 4, gw = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
+    uint64_t span = ((n + nw - 1) / nw + 31) & ~31ull;
+    span = span < 512 ? 512 : span;
+    const uint32_t f_end = min(P.nf, f_begin + 32u * FPL);
+    const uint32_t f0 = f_begin + static_cast<uint32_t>(lane);
+    double acc[FPL][8];
+    const double2* recs = reinterpret_cast<const double2*>(P.recs);
+    for (uint64_t r0 = gw * span; r0 < n; r0 += nw * span) {
+        const uint64_t r1 = min(r0 + span, n);
+        uint32_t cur = 0xffffffffu;
+#pragma unroll
+        for (int m = 0; m < FPL; ++m)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[m][k] = 0.0;
+        auto flush = [&]() {
+            if (cur == 0xffffffffu) return;
+            double* out = P.sums + (static_cast<size_t>(cur) * P.n_rx + P.rx_index) * P.nf * 8;
+#pragma unroll
+            for (int m = 0; m < FPL; ++m) {
+                const uint32_t f = f0 + 32u * m;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (f < f_end && acc[m][k] != 0.0) atomicAdd(out + f * 8 + k, acc[m][k]);
+                    acc[m][k] = 0.0;
+                }
+            }
+        };
+        for (uint64_t rb = r0; rb < r1; rb += 32) {
+            const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(32), r1 - rb));
+            if (static_cast<uint32_t>(lane) < cnt) {
+                const double2* r = recs + (rb + lane) * kRecD2;
+                double2* t = st[warp][lane];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) t[ch] = __ldcs(r + ch);
+                const double2 sv = __ldcs(r + 4);
+                t[7] = __ldcs(r + 5);
+                if (P.uniform_f) {
+                    const double ph0 = P.kph0 * sv.x, dph = P.kdph * sv.x;
+                    const double la0 = -(P.kph0 * sv.y), dla = -(P.kdph * sv.y);
+                    t[4] = make_double2(ph0, dph);
+                    t[5] = make_double2(la0, dla);
+                    if (FPL > 1) {
+                        const Cx w = polar_la(32.0 * dph, 32.0 * dla);
+                        t[6] = make_double2(w.re, w.im);
+                    }
+                } else {
+                    t[4] = sv;
+                }
+            }
+            __syncwarp();
+            for (uint32_t j = 0; j < cnt; ++j) {
+                const double2* t = st[warp][j];
+                const uint32_t a = static_cast<uint32_t>(__double_as_longlong(t[7].x));
+                if (a != cur) {
+                    flush();
+                    cur = a;
+                }
+                if (f0 >= f_end) continue;
+                Cx am[4];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) am[ch] = {t[ch].x, t[ch].y};
+                Cx z, w = {1.0, 0.0};
+                const double2 t4 = t[4];
+                if (P.uniform_f) {
+                    const double2 t5 = t[5];
+                    z = polar_la(t4.x + static_cast<double>(f0) * t4.y, t5.x + static_cast<double>(f0) * t5.y);
+                    if (FPL > 1) w = {t[6].x, t[6].y};
+                } else {
+                    z = phasor(P.k0[f0], Cx{t4.x, t4.y});
+                }
+#pragma unroll
+                for (int m = 0; m < FPL; ++m) {
+                    const uint32_t f = f0 + 32u * m;
+                    if (f < f_end) {
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            acc[m][2 * ch] = __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, acc[m][2 * ch]));
+                            acc[m][2 * ch + 1] =
+                                __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
+                        }
+                        if (m + 1 < FPL && f + 32u < f_end) {
+                            if (P.uniform_f)
+                                z = {__fma_rn(z.re, w.re, -z.im * w.im), __fma_rn(z.re, w.im, z.im * w.re)};
+                            else
+                                z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        flush();
+    }
+}
+
 __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, const double* __restrict__ d,
                                  const double* __restrict__ tmin, uint32_t n, int any_hit,
                                  double* __restrict__ t_out, uint32_t* __restrict__ id_out) {
@@ -1273,16 +1384,31 @@ static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int thre
                                cudaStream_t stream) {
     if (p.det)  // one receiver per launch (the deterministic solver has no fan mode)
         return mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, true>(p, sms, threads, smem, stream)
-                                : launch_mode<kModeSmem, kDiel, kLossy, true>(p, sms, threads, smem, stream);
+                                : launch_mode<kModeDefer, kDiel, kLossy, true>(p, sms, threads, smem, stream);
     return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false>(p, sms, threads, smem, stream)
            : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false>(p, sms, threads, smem, stream)
-                              : launch_mode<kModeSmem, kDiel, kLossy, false>(p, sms, threads, smem, stream);
+                              : launch_mode<kModeDefer, kDiel, kLossy, false>(p, sms, threads, smem, stream);
+}
+
+// deferred accumulation of one path-kernel launch's records (F > 1)
+cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
+    const unsigned blocks = static_cast<unsigned>(device_sms) * 4;
+    const uint32_t fpl = p.nf <= 32 ? 1 : (p.nf <= 64 ? 2 : 4);
+    for (uint32_t fb = 0; fb < p.nf; fb += 32 * fpl) {
+        if (fpl == 1) accumulate_kernel<1><<<blocks, 128, 0, stream>>>(p, fb);
+        else if (fpl == 2) accumulate_kernel<2><<<blocks, 128, 0, stream>>>(p, fb);
+        else accumulate_kernel<4><<<blocks, 128, 0, stream>>>(p, fb);
+        if (launches) ++*launches;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
-    const int mode = (p.fan && !p.det) ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeSmem);
-    size_t smem = mode == kModeSmem ? static_cast<size_t>(threads / 32) * p.nf * 8 * sizeof(double) : 0;
+    const int mode = (p.fan && !p.det) ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeDefer);
+    size_t smem = 0;
     if (const char* v = std::getenv("MCSBR_EXTRA_SMEM")) smem += std::strtoul(v, nullptr, 10);  // A/B only
     // three physics instantiations: all-PEC (dielectric code compiled out),
     // the reference's lossless dielectric model (bit-exact), lossy media

@@ -309,3 +309,24 @@ def test_many_small_incidences_share_chunks():
         for e in excs:
             total += oracle_estimate(sd, e, freqs, cfg, contributions=False)["stats"].rays_launched
         assert st.rays_launched == total
+
+
+@pytest.mark.parametrize("knob", ["MCSBR_REC_CAP=64", "MCSBR_GROUP_ENTRIES=500"])
+def test_deferred_accumulation_overflow_and_groups(knob, monkeypatch):
+    """F > 1 sums are accumulated from contribution records after the launch.
+    A record buffer too small for the launch falls back to direct atomics,
+    and a job split into many launch groups (incidences x entries) gives the
+    same sums: both == the oracle per incidence."""
+    k, v = knob.split("=")
+    monkeypatch.setenv(k, v)
+    obj, mm = M.dihedral_grid(0.5, 8)
+    sd = M.load_scene(obj, mm)
+    s = M.Scene(sd)
+    cfg = M.McConfig(strata_per_wavelength=3, samples_per_stratum=1, max_bounce=4, seed=2)
+    excs = [M.monostatic_excitation(90.0, float(p)) for p in np.linspace(10.0, 80.0, 6)]
+    freqs = np.linspace(9e9, 11e9, 40)
+    vals, st = M.estimate_batch(s, [(e, 0.0) for e in excs], [[e] for e in excs], freqs, cfg)
+    for i, e in enumerate(excs):
+        ref = oracle_estimate(sd, e, freqs, cfg, contributions=False)
+        scale = max(np.max(np.abs(ref["values"])), 1e-300)
+        assert np.max(np.abs(vals[i, 0] - ref["values"])) <= 1e-9 * scale

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 1500 python tools/ab.py --c2 --configs c1,c3,c4,c5 --reps 2 new= prev=prev
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 120 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python tools/ab.py --configs c4,c5 --reps 3 new= prev=prev
