@@ -2,11 +2,12 @@
 
 One process per GPU (torch.distributed, NCCL over NVLink / NVSwitch).  Every
 rank holds a replica of the scene (uploaded + BVH built on its own GPU) and
-traces a disjoint launch-entry range of EVERY incidence,
+traces a disjoint range of EVERY incidence's launch entries,
 
     [entries * rank / world, entries * (rank + 1) / world)      (shard_range)
 
-(the same integer partition the C ABI applies in mcsbr_gpu_trace_device), so
+of the dispatch order (4-row bands of strata, trace.cu locate(); the same
+integer partition the C ABI applies in mcsbr_gpu_trace_device), so
 per-angle work is balanced and the counter-RNG keys (seed, cell, sample) --
 hence every path -- are independent of the GPU count.  The raw complex
 phasor sums ([n_inc][n_rx][nf][4] fp64) and the uint64 counters are then

@@ -1,9 +1,14 @@
 """Summarise ncu outputs into profiles/ (committed evidence).
 
-usage: python tools/ncu_summary.py <launches.csv> <full.ncu-rep> <round-tag>
-writes profiles/<tag>_launches.csv (kernel, count, total/mean ms, share),
-       profiles/<tag>_path_kernel.json (key metrics of the full capture),
-       profiles/path_kernel_dram.json (dram bytes per launch, read by bench.py)
+usage: python tools/ncu_summary.py <launches.csv|-> <full.ncu-rep> <round-tag> [name] [command]
+writes profiles/<tag>_launches.csv            (kernel, count, total/mean ms, share) unless '-'
+       profiles/<tag>_<name>.json             key metrics of the full capture (name default
+                                              'path_kernel' = the c2 bench workload)
+       profiles/path_kernel_dram.json         dram bytes per launch (read by bench.py; c2 only)
+
+The metrics answer the north star's question for the path kernel: achieved
+L2 / HBM GB/s, SM issue and the FP32 (fma), FP64 and SFU (xu) pipe
+utilisation against the B200's peaks, plus the stall mix.
 """
 import collections
 import csv
@@ -15,24 +20,27 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+name = sys.argv[4] if len(sys.argv) > 4 else "path_kernel"
+command = sys.argv[5] if len(sys.argv) > 5 else "python tools/profile_c2.py (c2 sweep, 2nd path_kernel launch)"
 prof = os.path.join(ROOT, "profiles")
 os.makedirs(prof, exist_ok=True)
 
-rows = [r for r in csv.reader(l for l in open(launches) if not l.startswith("=="))]
-hdr = rows[0]
-ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-tot = collections.defaultdict(float)
-cnt = collections.Counter()
-for r in rows[1:]:
-    if len(r) > vi:
-        k = r[ki].split("(")[0]
-        tot[k] += float(r[vi].replace(",", ""))
-        cnt[k] += 1
-allns = sum(tot.values())
-with open(os.path.join(prof, f"{tag}_launches.csv"), "w") as f:
-    f.write("kernel,launches,total_ms,mean_ms,share\n")
-    for k in sorted(tot, key=lambda k: -tot[k]):
-        f.write(f"{k},{cnt[k]},{tot[k] / 1e6:.4f},{tot[k] / cnt[k] / 1e6:.4f},{tot[k] / allns:.4f}\n")
+if launches != "-":
+    rows = [r for r in csv.reader(l for l in open(launches) if not l.startswith("=="))]
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for r in rows[1:]:
+        if len(r) > vi:
+            k = r[ki].split("(")[0]
+            tot[k] += float(r[vi].replace(",", ""))
+            cnt[k] += 1
+    allns = sum(tot.values())
+    with open(os.path.join(prof, f"{tag}_launches.csv"), "w") as f:
+        f.write("kernel,launches,total_ms,mean_ms,share\n")
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            f.write(f"{k},{cnt[k]},{tot[k] / 1e6:.4f},{tot[k] / cnt[k] / 1e6:.4f},{tot[k] / allns:.4f}\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
@@ -41,26 +49,42 @@ want = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
+    "dram__bytes.sum.per_second": "dram_bandwidth",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "lts__t_bytes.sum": "l2_bytes",
+    "lts__t_bytes.sum.per_second": "l2_bandwidth",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "l1tex__t_bytes.sum.per_second": "l1_bandwidth",
     "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
     "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "smsp_issue_active_pct",
     "sm__warps_active.avg.per_cycle_active": "warps_active_per_sm",
     "launch__registers_per_thread": "registers",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
+    "launch__shared_mem_per_block_static": "smem_static_per_block",
+    "launch__shared_mem_config_size": "smem_carveout",
     "smsp__inst_executed.sum": "warp_instructions",
     "smsp__thread_inst_executed_per_inst_executed.ratio": "simt_efficiency_threads",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fp32_fma_inst_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_inst_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "sfu_xu_inst_pct",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_inst_pct",
     "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum": "local_ld_sectors",
     "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum": "local_st_sectors",
-    "lts__t_bytes.sum": "l2_bytes",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
 }
-out = {"source": os.path.basename(rep), "command": "python tools/profile_c2.py (c2 sweep, 2nd path_kernel launch)"}
-for i, name in enumerate(h):
-    if name in want:
-        out[want[name]] = {"value": v[i], "unit": u[i]}
+out = {"source": os.path.basename(rep), "command": command}
+for i, key in enumerate(h):
+    if key in want:
+        out[want[key]] = {"value": v[i], "unit": u[i]}
+stalls = {k.split("stalled_")[1]: float(x.replace(",", "")) for k, x in zip(h, v)
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and "not_issued" not in k and x}
+tot_s = sum(stalls.values()) or 1.0
+out["stall_mix_pct"] = {k: round(100 * x / tot_s, 1) for k, x in sorted(stalls.items(), key=lambda kv: -kv[1])
+                        if 100 * x / tot_s >= 0.5}
 
 
 def to_bytes(x):
@@ -70,8 +94,9 @@ def to_bytes(x):
 
 dram = to_bytes(out["dram_read"]) + to_bytes(out["dram_write"])
 out["dram_bytes_per_launch"] = dram
-with open(os.path.join(prof, f"{tag}_path_kernel.json"), "w") as f:
+with open(os.path.join(prof, f"{tag}_{name}.json"), "w") as f:
     json.dump(out, f, indent=1)
-with open(os.path.join(prof, "path_kernel_dram.json"), "w") as f:
-    json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_path_kernel.json"}, f, indent=1)
+if name == "path_kernel":
+    with open(os.path.join(prof, "path_kernel_dram.json"), "w") as f:
+        json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_{name}.json"}, f, indent=1)
 print(json.dumps(out, indent=1))
