@@ -142,6 +142,7 @@ struct mcsbr_scene {
         s.center[1] = center[1];
         s.center[2] = center[2];
         s.skip_radius = radius * 1.01 + 1e-9;
+        s.margin_r = static_cast<float>(radius * 1.01 + 1e-9);
         return s;
     }
 };
@@ -678,7 +679,9 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
             return fail(e, "upload Im n");
     }
     const double lo3[3] = {lo.x, lo.y, lo.z}, hi3[3] = {hi.x, hi.y, hi.z};
-    const double box_pad = 1e-5 * r + 1e-30;
+    // boxes: outward-rounded fp64 AABBs; the pad only absorbs the fp64
+    // rounding of the centring (the slab test's margin lives on the ray)
+    const double box_pad = 1e-12 * r + 1e-30;
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
         return fail(e, "BVH build");
     g_launches += 7;

@@ -2,15 +2,16 @@
 // the BVH builder (bvh.cu) and the path kernel (trace.cu).
 //
 // Device memory layout of a scene (all arrays 16-byte aligned, SoA-by-record):
-//   nodes      BVH2, 64 B per node = 4 x float4:
-//                [0] (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)
-//                [1] (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
-//                [2] (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)
-//                [3] (ref0, ref1, -, -) as int bits; ref >= 0 inner node,
-//                    ref < 0 leaf: ~ref = (first << 3) | count (count <= 4)
+//   nodes      BVH4, 128 B per node = 8 x float4, child boxes SoA by axis:
+//                [0] lo.x of children 0..3   [1] hi.x   [2] lo.y   [3] hi.y
+//                [4] lo.z                    [5] hi.z
+//                [6] child refs as int bits: ref >= 0 inner node,
+//                    ref < 0 leaf: ~ref = (first << 3) | count (count <= MCSBR_LEAF_MAX)
+//                [7] (child count, -, -, -)
 //              child boxes are fp32 in a frame centred on the scene's
-//              bounding sphere, rounded outward from fp64 and padded by
-//              box_pad so the fp32 slab test can only over-accept.
+//              bounding sphere, the fp64 triangle boxes rounded outward (no
+//              padding): the slab test's rounding margin lives on the ray
+//              (trace.cu make_fray), so the fp32 descent can only over-accept.
 //   tri64      per leaf-ordered triangle 5 x double2 = 80 B:
 //                (a.x, a.y) (a.z, e1.x) (e1.y, e1.z) (e2.x, e2.y) (e2.z, id)
 //              e1 = b - a, e2 = c - a in fp64: exactly the values the
@@ -47,6 +48,7 @@ struct SceneView {
     const double* mat_nim;  // per material Im(n) (lossy scenes), else nullptr
     double center[3];  // bounding-sphere centre: origin of the fp32 box frame
     double skip_radius;  // bounding radius + margin (traversal origin advance)
+    float margin_r;      // bounding radius (fp32): scale of the slab-test ray margin
 };
 
 // Per incidence (one launch aperture), host-planned in fp64.

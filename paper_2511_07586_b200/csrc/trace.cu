@@ -51,29 +51,39 @@ __device__ __forceinline__ V3 ld3(const double* p) { return {p[0], p[1], p[2]}; 
 
 struct FRay {
     float ix, iy, iz;     // 1/dir (fp32, zero components clamped)
-    float oix, oiy, oiz;  // origin * inv, origin in the scene-centred frame
-    double t_skip;       // parameter of the traversal origin along the fp64 ray
+    float onx, ony, onz;  // origin * inv + margin: near planes  (t = plane * inv - on)
+    float ofx, ofy, ofz;  // origin * inv - margin: far planes
+    float tlo;            // lower end of the box interval (0, or t_min rounded down)
+    double t_skip;        // parameter of the traversal origin along the fp64 ray
     int oct;              // ray octant: bit a set iff inv component a < 0
 };
 
 // fp32 reciprocal of a direction component (relative error ~1e-7, covered by
-// the box padding); tiny components are clamped so no slab yields inf - inf.
+// the ray margin); tiny components are clamped so no slab yields inf - inf.
 __device__ __forceinline__ float safe_inv(double d) {
     const float f = __double2float_rn(d);
     const float a = fabsf(f) < 1e-12f ? copysignf(1e-12f, f) : f;
     return __frcp_rn(a);
 }
 
-// The fp32 boxes live in a frame centred on the scene's bounding sphere.  A
-// ray starting outside the sphere is advanced (for the box tests only) to a
-// conservative lower bound of its sphere entry, so every fp32 coordinate the
-// slab test sees is O(scene radius) and the rounding error stays far below
-// the box padding (build: box_pad = 1e-5 R).  The fp64 triangle test always
-// uses the untouched ray, so hits are exactly the reference's.
+// The fp32 boxes live in a frame centred on the scene's bounding sphere and
+// are the fp64 triangle boxes rounded outward (no padding): they contain
+// every triangle exactly.  The slab test's own rounding is covered by a
+// margin on the RAY, in t units, widening every slab by m |inv| on both
+// sides: m = 1e-6 R for rays that start on a surface (|origin| <= R in the
+// box frame; the worst-case error of t = plane * inv - origin * inv with
+// fp32-rounded origin, direction and reciprocal is < 5e-7 R |inv|), and
+// m = 1e-5 R for rays that start outside the bounding sphere, which are
+// advanced (for the box tests only) to a conservative lower bound of their
+// sphere entry so every fp32 coordinate is O(R).  Surface rays also cull by
+// t_min: a box the ray leaves (margin included) before t_min holds no
+// acceptable hit, which skips the flat-plate subtrees a reflected or
+// occlusion ray starts in.  The fp64 triangle test always uses the untouched
+// ray, so hits are exactly the reference's.
 // `outside`: the origin may lie outside the bounding sphere (launch rays and
 // the public intersect API); surface-to-surface and occlusion rays start on a
 // triangle, inside the sphere, and skip the advance.
-__device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool outside) {
+__device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool outside, double t_min) {
     FRay r;
     const V3 c = {S.center[0], S.center[1], S.center[2]};
     const V3 oc = o - c;
@@ -88,9 +98,18 @@ __device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool o
     r.ix = safe_inv(d.x);
     r.iy = safe_inv(d.y);
     r.iz = safe_inv(d.z);
-    r.oix = __fmul_rn(__double2float_rn(ot.x), r.ix);
-    r.oiy = __fmul_rn(__double2float_rn(ot.y), r.iy);
-    r.oiz = __fmul_rn(__double2float_rn(ot.z), r.iz);
+    const float m = S.margin_r * (outside ? 1e-5f : 1e-6f);
+    const float ox = __fmul_rn(__double2float_rn(ot.x), r.ix);
+    const float oy = __fmul_rn(__double2float_rn(ot.y), r.iy);
+    const float oz = __fmul_rn(__double2float_rn(ot.z), r.iz);
+    const float ex = __fmul_ru(m, fabsf(r.ix)), ey = __fmul_ru(m, fabsf(r.iy)), ez = __fmul_ru(m, fabsf(r.iz));
+    r.onx = __fadd_ru(ox, ex);
+    r.ony = __fadd_ru(oy, ey);
+    r.onz = __fadd_ru(oz, ez);
+    r.ofx = __fadd_rd(ox, -ex);
+    r.ofy = __fadd_rd(oy, -ey);
+    r.ofz = __fadd_rd(oz, -ez);
+    r.tlo = outside ? 0.0f : __double2float_rd(t_min * (1.0 - 1e-6));
     r.oct = (r.ix < 0.0f ? 1 : 0) | (r.iy < 0.0f ? 2 : 0) | (r.iz < 0.0f ? 4 : 0);
     return r;
 }
@@ -108,26 +127,15 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 }
 
 // Slab test with the near / far planes already chosen by the ray octant
-// (the caller loads lo or hi per axis by address).  Because fma rounding is
-// monotonic and lo <= hi, the near-plane distance equals min(t_lo, t_hi) of
-// the symmetric form bit for bit, so culling is identical.
+// (the caller loads lo or hi per axis by address): entry = max of the near
+// plane distances and tlo, exit = min of the far ones and tmax; returns the
+// entry distance or +inf.
 __device__ __forceinline__ float slab_nf(const FRay& r, float nx, float fx, float ny, float fy, float nz,
                                          float fz, float tmax) {
-    const float tn = fmax3(__fmaf_rn(nx, r.ix, -r.oix), __fmaf_rn(ny, r.iy, -r.oiy),
-                           fmaxf(__fmaf_rn(nz, r.iz, -r.oiz), 0.0f));
-    const float tf = fmin3(__fmaf_rn(fx, r.ix, -r.oix), __fmaf_rn(fy, r.iy, -r.oiy),
-                           fminf(__fmaf_rn(fz, r.iz, -r.oiz), tmax));
-    return tn <= tf ? tn : __int_as_float(0x7f800000);
-}
-
-// slab test of one child box against [0, tmax]; returns entry distance or +inf
-__device__ __forceinline__ float slab(const FRay& r, float lx, float hx, float ly, float hy, float lz,
-                                      float hz, float tmax) {
-    const float x0 = __fmaf_rn(lx, r.ix, -r.oix), x1 = __fmaf_rn(hx, r.ix, -r.oix);
-    const float y0 = __fmaf_rn(ly, r.iy, -r.oiy), y1 = __fmaf_rn(hy, r.iy, -r.oiy);
-    const float z0 = __fmaf_rn(lz, r.iz, -r.oiz), z1 = __fmaf_rn(hz, r.iz, -r.oiz);
-    const float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.0f));
-    const float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));
+    const float tn = fmax3(__fmaf_rn(nx, r.ix, -r.onx), __fmaf_rn(ny, r.iy, -r.ony),
+                           fmaxf(__fmaf_rn(nz, r.iz, -r.onz), r.tlo));
+    const float tf = fmin3(__fmaf_rn(fx, r.ix, -r.ofx), __fmaf_rn(fy, r.iy, -r.ofy),
+                           fminf(__fmaf_rn(fz, r.iz, -r.ofz), tmax));
     return tn <= tf ? tn : __int_as_float(0x7f800000);
 }
 
@@ -200,7 +208,7 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
         }
     } flush_{tstat};
 #endif
-    const FRay r = make_fray(S, o, d, outside);
+    const FRay r = make_fray(S, o, d, outside, t_min);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
     best_id = 0xffffffffu;
     float tmax = __int_as_float(0x7f800000);
@@ -212,16 +220,6 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             // 4-wide node: 128 B, boxes SoA by axis (bvh.cu emit4_kernel)
             MCSBR_STAT(0);
             const float4* nd = S.nodes + 8ll * ref;
-#ifdef MCSBR_SLAB_MINMAX
-            const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
-            const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5), rf = __ldg(nd + 6), nc = __ldg(nd + 7);
-            const int cnt = __float_as_int(nc.x);
-            const float inf = __int_as_float(0x7f800000);
-            float t0 = slab(r, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tmax);
-            float t1 = slab(r, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmax);
-            float t2 = cnt > 2 ? slab(r, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmax) : inf;
-            float t3 = cnt > 3 ? slab(r, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmax) : inf;
-#else
             // near planes at (lo | octant bit) per axis, far planes at the other
             const int ox = r.oct & 1, oy = (r.oct >> 1) & 1, oz = (r.oct >> 2) & 1;
             const float4 nx = __ldg(nd + ox), fx = __ldg(nd + (ox ^ 1));
@@ -234,7 +232,6 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             float t1 = slab_nf(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
             float t2 = cnt > 2 ? slab_nf(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax) : inf;
             float t3 = cnt > 3 ? slab_nf(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax) : inf;
-#endif
             int c0 = __float_as_int(rf.x), c1 = __float_as_int(rf.y), c2 = __float_as_int(rf.z),
                 c3 = __float_as_int(rf.w);
             // sort the 4 (entry, child) pairs: network (0,1)(2,3)(0,2)(1,3)(1,2)
