@@ -265,10 +265,11 @@ __global__ void emit4_kernel(int n, const int2* __restrict__ child, const int2* 
             ++cnt;
         }
     }
-    for (int k = cnt; k < 4; ++k) {  // unused slots: masked by the count in [7]
+    for (int k = cnt; k < 4; ++k) {  // unused slots: empty boxes, which every slab test misses
+        const float inf = __int_as_float(0x7f800000);
         ref[k] = 0;
-        lo[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        hi[k] = lo[k];
+        lo[k] = make_float4(inf, inf, inf, 0.f);
+        hi[k] = make_float4(-inf, -inf, -inf, 0.f);
     }
     float4* o = nodes + 8ll * idx4[i];
     o[0] = make_float4(lo[0].x, lo[1].x, lo[2].x, lo[3].x);

@@ -126,6 +126,18 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     return d;
 }
 
+// a * s + c for the pair (a0, a1): one FFMA2 (packed fp32x2, sm_100)
+__device__ __forceinline__ float2 ffma2(float a0, float a1, float s, float c) {
+    unsigned long long aa, ss, cc, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(ss) : "f"(s));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(cc) : "f"(c));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(ss), "l"(cc));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
+
 // Slab test with the near / far planes already chosen by the ray octant
 // (the caller loads lo or hi per axis by address): entry = max of the near
 // plane distances and tlo, exit = min of the far ones and tmax; returns the
@@ -220,42 +232,62 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             // 4-wide node: 128 B, boxes SoA by axis (bvh.cu emit4_kernel)
             MCSBR_STAT(0);
             const float4* nd = S.nodes + 8ll * ref;
-            // near planes at (lo | octant bit) per axis, far planes at the other
+            // near planes at (lo | octant bit) per axis, far planes at the other;
+            // unused child slots hold empty boxes (lo = +inf, hi = -inf) and
+            // always miss, so no child count is needed
             const int ox = r.oct & 1, oy = (r.oct >> 1) & 1, oz = (r.oct >> 2) & 1;
             const float4 nx = __ldg(nd + ox), fx = __ldg(nd + (ox ^ 1));
             const float4 ny = __ldg(nd + 2 + oy), fy = __ldg(nd + 2 + (oy ^ 1));
             const float4 nz = __ldg(nd + 4 + oz), fz = __ldg(nd + 4 + (oz ^ 1));
-            const float4 rf = __ldg(nd + 6), nc = __ldg(nd + 7);
-            const int cnt = __float_as_int(nc.x);
-            const float inf = __int_as_float(0x7f800000);
-            float t0 = slab_nf(r, nx.x, fx.x, ny.x, fy.x, nz.x, fz.x, tmax);
-            float t1 = slab_nf(r, nx.y, fx.y, ny.y, fy.y, nz.y, fz.y, tmax);
-            float t2 = cnt > 2 ? slab_nf(r, nx.z, fx.z, ny.z, fy.z, nz.z, fz.z, tmax) : inf;
-            float t3 = cnt > 3 ? slab_nf(r, nx.w, fx.w, ny.w, fy.w, nz.w, fz.w, tmax) : inf;
-            int c0 = __float_as_int(rf.x), c1 = __float_as_int(rf.y), c2 = __float_as_int(rf.z),
-                c3 = __float_as_int(rf.w);
-            // sort the 4 (entry, child) pairs: network (0,1)(2,3)(0,2)(1,3)(1,2)
-#define MCSBR_CSWAP(ta, ca, tb, cb)          \
-    if (tb < ta) {                           \
-        const float tt = ta; ta = tb; tb = tt; \
-        const int cc = ca; ca = cb; cb = cc;   \
+            const float4 rf = __ldg(nd + 6);
+            // plane distances two children at a time (FFMA2): [k].x child k, .y child k + 1
+            const float2 xn[2] = {ffma2(nx.x, nx.y, r.ix, -r.onx), ffma2(nx.z, nx.w, r.ix, -r.onx)};
+            const float2 yn[2] = {ffma2(ny.x, ny.y, r.iy, -r.ony), ffma2(ny.z, ny.w, r.iy, -r.ony)};
+            const float2 zn[2] = {ffma2(nz.x, nz.y, r.iz, -r.onz), ffma2(nz.z, nz.w, r.iz, -r.onz)};
+            const float2 xf[2] = {ffma2(fx.x, fx.y, r.ix, -r.ofx), ffma2(fx.z, fx.w, r.ix, -r.ofx)};
+            const float2 yf[2] = {ffma2(fy.x, fy.y, r.iy, -r.ofy), ffma2(fy.z, fy.w, r.iy, -r.ofy)};
+            const float2 zf[2] = {ffma2(fz.x, fz.y, r.iz, -r.ofz), ffma2(fz.z, fz.w, r.iz, -r.ofz)};
+            // sort keys: entry distance (>= 0, so its bits order like the
+            // float) with the child slot in the low 2 bits; a miss is >= +inf
+            uint32_t k[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int h = j >> 1;
+                const float a_n = (j & 1) ? xn[h].y : xn[h].x, b_n = (j & 1) ? yn[h].y : yn[h].x;
+                const float c_n = (j & 1) ? zn[h].y : zn[h].x;
+                const float a_f = (j & 1) ? xf[h].y : xf[h].x, b_f = (j & 1) ? yf[h].y : yf[h].x;
+                const float c_f = (j & 1) ? zf[h].y : zf[h].x;
+                const float tn = fmax3(a_n, b_n, fmaxf(c_n, r.tlo));
+                const float tf = fmin3(a_f, b_f, fminf(c_f, tmax));
+                k[j] = ((tn <= tf ? __float_as_uint(tn) : 0x7f800000u) & ~3u) | static_cast<uint32_t>(j);
+            }
+            // sorting network (0,1)(2,3)(0,2)(1,3)(1,2) on the keys: integer min / max
+#define MCSBR_KSWAP(a, b)               \
+    {                                   \
+        const uint32_t lo_ = min(a, b); \
+        b = max(a, b);                  \
+        a = lo_;                        \
     }
-            MCSBR_CSWAP(t0, c0, t1, c1)
-            MCSBR_CSWAP(t2, c2, t3, c3)
-            MCSBR_CSWAP(t0, c0, t2, c2)
-            MCSBR_CSWAP(t1, c1, t3, c3)
-            MCSBR_CSWAP(t1, c1, t2, c2)
-#undef MCSBR_CSWAP
-            if (t0 != inf) {
-                // visit the nearest now, push the others far-to-near
-                if (sp + 3 > kStackSize) {
-                    fault |= kFaultStack;
-                } else {
-                    if (t3 != inf) stack[sp++] = c3;
-                    if (t2 != inf) stack[sp++] = c2;
-                    if (t1 != inf) stack[sp++] = c1;
-                }
-                ref = c0;
+            MCSBR_KSWAP(k[0], k[1])
+            MCSBR_KSWAP(k[2], k[3])
+            MCSBR_KSWAP(k[0], k[2])
+            MCSBR_KSWAP(k[1], k[3])
+            MCSBR_KSWAP(k[1], k[2])
+#undef MCSBR_KSWAP
+            constexpr uint32_t kMiss = 0x7f800000u;
+            if (k[0] < kMiss) {
+                const int rc[4] = {__float_as_int(rf.x), __float_as_int(rf.y), __float_as_int(rf.z),
+                                   __float_as_int(rf.w)};
+                auto child = [&](uint32_t key) {
+                    const uint32_t j = key & 3u;
+                    return (j & 2u) ? ((j & 1u) ? rc[3] : rc[2]) : ((j & 1u) ? rc[1] : rc[0]);
+                };
+                // visit the nearest now, push the others far-to-near (the
+                // host bounds the tree depth so the stack cannot overflow)
+                if (k[3] < kMiss) stack[sp++] = child(k[3]);
+                if (k[2] < kMiss) stack[sp++] = child(k[2]);
+                if (k[1] < kMiss) stack[sp++] = child(k[1]);
+                ref = child(k[0]);
                 continue;
             }
         } else {
