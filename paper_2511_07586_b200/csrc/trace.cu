@@ -612,6 +612,36 @@ __device__ __forceinline__ void det_flush(const TraceParams& P, uint64_t blk, ui
     atomicAdd(P.det_blocks + 2 * blk + 1, static_cast<unsigned long long>(push));
 }
 
+// Add a warp's register-mode phasor sums (slot fields kAcc..kAcc+7) into
+// incidence a's sums and clear them.  Fan mode: lane l owns receiver
+// rx_index + l (nf == 1, no reduction); otherwise the warp reduces its 32
+// lanes and lane 0 adds.  Out of line: it runs once per incidence change and
+// its warp-collective shuffles would otherwise be inlined at every call site.
+template <bool kFan, int kAcc>
+__device__ __noinline__ void flush_sums(double* sums, uint32_t n_rx, uint32_t rx_index, volatile double* p,
+                                        uint32_t a, int lane) {
+    const Slot sl{p};
+    if (kFan) {
+        const uint32_t rx = rx_index + static_cast<uint32_t>(lane);
+        if (rx < n_rx) {
+            double* o = sums + (static_cast<size_t>(a) * n_rx + rx) * 8;
+            for (int k = 0; k < 8; ++k) {
+                const double v = sl.get(kAcc + k);
+                if (v != 0.0) atomicAdd(o + k, v);
+                sl.set(kAcc + k, 0.0);
+            }
+        }
+        return;
+    }
+    double* out = sums + (static_cast<size_t>(a) * n_rx + rx_index) * 8;
+    for (int k = 0; k < 8; ++k) {
+        double v = sl.get(kAcc + k);
+        sl.set(kAcc + k, 0.0);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (lane == 0 && v != 0.0) atomicAdd(out + k, v);
+    }
+}
+
 // e^{-j k_f s} for frequency f: on uniform grids the reference's phase
 // (kph0 + f kdph) s (farfield.cpp:131-139), else k0[f] directly (:140-146)
 template <typename NT>
@@ -754,36 +784,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
     }
     // add the warp's accumulators into incidence cur_a's sums and clear them
     auto flush = [&]() {
-        if (cur_a == 0xffffffffu) return;
-        if (kMode == kModeFan) {
-            const uint32_t rx = P.rx_index + static_cast<uint32_t>(lane);
-            if (rx < P.n_rx) {  // lane-owned receiver: nf == 1, no warp reduction
-                double* o = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + rx) * 8;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double v = sl.get(kFAcc + k);
-                    if (v != 0.0) atomicAdd(o + k, v);
-                    sl.set(kFAcc + k, 0.0);
-                }
-            }
-        } else if (kRegAcc) {
-            double* out = P.sums + (static_cast<size_t>(cur_a) * P.n_rx + P.rx_index) * 8;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                double re = sl.get(kFAcc + 2 * ch), im = sl.get(kFAcc + 2 * ch + 1);
-                sl.set(kFAcc + 2 * ch, 0.0);
-                sl.set(kFAcc + 2 * ch + 1, 0.0);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    re += __shfl_xor_sync(kFull, re, o);
-                    im += __shfl_xor_sync(kFull, im, o);
-                }
-                if (lane == 0) {
-                    if (re != 0.0) atomicAdd(out + 2 * ch, re);
-                    if (im != 0.0) atomicAdd(out + 2 * ch + 1, im);
-                }
-            }
-        }
+        if (kRegAcc && cur_a != 0xffffffffu)
+            flush_sums<kMode == kModeFan, kFAcc>(P.sums, P.n_rx, P.rx_index, sl.p, cur_a, lane);
     };
 
     for (;;) {
