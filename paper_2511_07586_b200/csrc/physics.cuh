@@ -234,4 +234,19 @@ __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs
     return cvreal(b.s_hat) * (es * co.t_s) + cvreal(b.p_out_t) * (ep * co.t_p);
 }
 
+// Real-field version for PEC hits (real coefficients r_s = -1, r_p = +1):
+// the complex version's real parts, operation for operation (its imaginary
+// parts are exactly +-0 there); only the reflected branch exists.
+__device__ inline V3 interface_transform(const V3& e, int branch, const Coeffs& co, const Basis& b,
+                                         uint32_t& fault) {
+    const V3 dir_in = cross(b.s_hat, b.p_in);
+    const double lim = 1e-9 * (1.0 + norm(e));
+    const double de = dot(e, dir_in);
+    if (de * de > lim * lim) fault |= kFaultTransverse;
+    const double es = dot(e, b.s_hat);
+    const double ep = dot(e, b.p_in);
+    if (branch == 0) return b.s_hat * (es * co.r_s.re) + b.p_out_r * (ep * co.r_p.re);
+    return b.s_hat * (es * co.t_s.re) + b.p_out_t * (ep * co.t_p.re);
+}
+
 }  // namespace mcsbr_dev

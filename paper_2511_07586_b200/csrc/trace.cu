@@ -348,11 +348,17 @@ __device__ __forceinline__ HitInfo<NT> fill_hit(const SceneView& S, uint32_t id,
 // per-path state (PathState, proj/include/mcsbr/path_engine.hpp:16-28)
 
 // NT = double: the reference model; NT = Cx: complex optical path / index
-// (lossy extension).
-template <typename NT>
+// (lossy extension).  EF = CV3: complex transverse fields; EF = V3 on the
+// PEC-only instantiation, where every field stays real: the initial
+// polarisations are real and the PEC coefficients (-1, +1) are real, so the
+// reference's complex arithmetic carries imaginary parts that are exactly
+// +-0 and real parts equal to this real arithmetic operation for operation
+// (x - (+-0) = x).  Outputs then agree with the reference under IEEE
+// equality; only the sign of some exactly-zero imaginary parts can differ.
+template <typename NT, typename EF = CV3>
 struct Path {
     V3 origin, dir;
-    CV3 e0, e1;
+    EF e0, e1;
     NT phi;
     double prob, weight;
     NT medium_n;
@@ -377,13 +383,16 @@ constexpr int kSlotThreads = 128;
 // two fields are not stored.  kLossy adds the imaginary parts; kRegAcc the
 // register-mode phasor sums.  Every 8 KB of shared memory per block costs
 // ~4-7% (measured) through the L1 capacity it takes: the PEC register-mode
-// slot (31 fields) keeps a block under 32 KB, so 4 blocks fit the 132 KB
-// shared-memory carve-out and leave ~124 KB of L1 per SM.
+// slot (real fields and amplitudes: 21 doubles) keeps a block at ~22 KB, so
+// 4 blocks fit the 100 KB shared-memory carve-out and leave ~156 KB of L1.
 template <bool kPec, bool kLossy, bool kRegAcc>
 struct Layout {
-    static constexpr int E0 = 0, E1 = 6, Phi = 12, Weight = 13, Amp = 14, SPath = 22;
-    static constexpr int Prob = 23, Medium = 24;            // !kPec only
-    static constexpr int Im0 = kPec ? 23 : 25;
+    static constexpr int EW = kPec ? 3 : 6;  // doubles per field vector (real / complex)
+    static constexpr int AW = kPec ? 1 : 2;  // doubles per projected amplitude
+    static constexpr int E0 = 0, E1 = EW, Phi = 2 * EW, Weight = Phi + 1, Amp = Weight + 1;
+    static constexpr int SPath = Amp + 4 * AW;
+    static constexpr int Prob = SPath + 1, Medium = SPath + 2;   // !kPec only
+    static constexpr int Im0 = kPec ? SPath + 1 : SPath + 3;
     static constexpr int PhiIm = Im0, MediumIm = Im0 + 1, SPathIm = Im0 + 2;  // kLossy only
     static constexpr int Acc = Im0 + (kLossy ? 3 : 0);       // kRegAcc only
     static constexpr int Fields = Acc + (kRegAcc ? 8 : 0);
@@ -407,6 +416,34 @@ struct Slot {
     }
 };
 
+__device__ __forceinline__ void slot_setv(const Slot& sl, int f, const CV3& v) { sl.setv(f, v); }
+__device__ __forceinline__ void slot_setv(const Slot& sl, int f, const V3& v) {
+    sl.set(f, v.x);
+    sl.set(f + 1, v.y);
+    sl.set(f + 2, v.z);
+}
+__device__ __forceinline__ void slot_getv(const Slot& sl, int f, CV3& v) { v = sl.getv(f); }
+__device__ __forceinline__ void slot_getv(const Slot& sl, int f, V3& v) { v = {sl.get(f), sl.get(f + 1), sl.get(f + 2)}; }
+// projected amplitude ch of a pending contribution (real on the PEC path)
+template <typename L>
+__device__ __forceinline__ void slot_set_amp(const Slot& sl, int ch, Cx a) {
+    if (L::pec) sl.set(L::Amp + ch, a.re);
+    else sl.setc(L::Amp + 2 * ch, a);
+}
+template <typename L>
+__device__ __forceinline__ Cx slot_get_amp(const Slot& sl, int ch) {
+    if (L::pec) return {sl.get(L::Amp + ch), 0.0};
+    return slot_get_amp<L>(sl, ch);
+}
+
+// EF helpers: a real vector as a field, the zero field, field norm
+template <typename EF> __device__ __forceinline__ EF ef_real(V3 v);
+template <> __device__ __forceinline__ CV3 ef_real<CV3>(V3 v) { return cvreal(v); }
+template <> __device__ __forceinline__ V3 ef_real<V3>(V3 v) { return v; }
+template <typename EF> __device__ __forceinline__ EF ef_zero();
+template <> __device__ __forceinline__ CV3 ef_zero<CV3>() { return cvzero(); }
+template <> __device__ __forceinline__ V3 ef_zero<V3>() { return {0.0, 0.0, 0.0}; }
+
 __device__ __forceinline__ void slot_set_nt(const Slot& sl, int f, int fim, double v) {
     (void)fim;
     sl.set(f, v);
@@ -420,10 +457,10 @@ __device__ __forceinline__ NT slot_get_nt(const Slot& sl, int f, int fim) {
     return make_nt<NT>(sl.get(f), std::is_same<NT, Cx>::value ? sl.get(fim) : 0.0);
 }
 
-template <typename L, typename NT>
-__device__ __forceinline__ void save_em(const Slot& sl, const Path<NT>& s) {
-    sl.setv(L::E0, s.e0);
-    sl.setv(L::E1, s.e1);
+template <typename L, typename NT, typename EF>
+__device__ __forceinline__ void save_em(const Slot& sl, const Path<NT, EF>& s) {
+    slot_setv(sl, L::E0, s.e0);
+    slot_setv(sl, L::E1, s.e1);
     slot_set_nt(sl, L::Phi, L::PhiIm, s.phi);
     sl.set(L::Weight, s.weight);
     if (!L::pec) {
@@ -432,10 +469,10 @@ __device__ __forceinline__ void save_em(const Slot& sl, const Path<NT>& s) {
     }
 }
 
-template <typename L, typename NT>
-__device__ __forceinline__ void load_em(const Slot& sl, Path<NT>& s, double ambient_n) {
-    s.e0 = sl.getv(L::E0);
-    s.e1 = sl.getv(L::E1);
+template <typename L, typename NT, typename EF>
+__device__ __forceinline__ void load_em(const Slot& sl, Path<NT, EF>& s, double ambient_n) {
+    slot_getv(sl, L::E0, s.e0);
+    slot_getv(sl, L::E1, s.e1);
     s.phi = slot_get_nt<NT>(sl, L::Phi, L::PhiIm);
     s.weight = sl.get(L::Weight);
     if (L::pec) {
@@ -453,8 +490,8 @@ __device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
     for (int ch = 0; ch < 4; ++ch) sl.setc(kAcc + 2 * ch, sl.getc(kAcc + 2 * ch) + am[ch] * z);
 }
 
-template <typename NT>
-__device__ __forceinline__ double draw(const TraceParams& P, const Path<NT>& s, uint64_t bounce,
+template <typename NT, typename EF>
+__device__ __forceinline__ double draw(const TraceParams& P, const Path<NT, EF>& s, uint64_t bounce,
                                        uint64_t purpose) {
     if (P.rng_mode == MCSBR_RNG_REFERENCE) return u53(counter_finish(s.key, bounce, purpose));
     return philox_uniform(P.seed, s.key, static_cast<uint32_t>(bounce), static_cast<uint32_t>(purpose));
@@ -502,9 +539,9 @@ __device__ __forceinline__ Entry locate(const TraceParams& P, const IncDev& I, u
 }
 
 // sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
-template <typename NT>
+template <typename NT, typename EF>
 __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
-                                          const Entry& en, Path<NT>& s) {
+                                          const Entry& en, Path<NT, EF>& s) {
     const uint32_t cell = en.cell, sample = en.sample, i = en.i, j = en.j;
     const uint64_t entry = en.entry;
     double ju = 0.5, jv = 0.5;
@@ -528,8 +565,8 @@ __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I,
     const V3 k = ld3(I.k_inc);
     s.origin = p;
     s.dir = k;
-    s.e0 = cvreal(ld3(I.pol_v));
-    s.e1 = cvreal(ld3(I.pol_h));
+    s.e0 = ef_real<EF>(ld3(I.pol_v));
+    s.e1 = ef_real<EF>(ld3(I.pol_h));
     s.phi = make_nt<NT>(P.scene.ambient_n * dot(k, p), 0.0);  // lossless ambient (validated)
     s.prob = 1.0;
     s.weight = 1.0;
@@ -552,8 +589,23 @@ __device__ __forceinline__ void project(const RxDev& R, const CV3& aj0, const CV
     amp[1] = dot(f1, rh);  // HH
 }
 
+// real fields (PEC path): the same projection in real arithmetic
+__device__ __forceinline__ void project(const RxDev& R, const V3& aj0, const V3& am0, const V3& aj1,
+                                        const V3& am1, Cx amp[4]) {
+    const V3 ks = ld3(R.k_s), rv = ld3(R.rx_v), rh = ld3(R.rx_h);
+    const V3 f0 = cross(ks, cross(ks, aj0)) + cross(ks, am0);
+    const V3 f1 = cross(ks, cross(ks, aj1)) + cross(ks, am1);
+    amp[0] = {dot(f0, rv), 0.0};  // VV
+    amp[3] = {dot(f0, rh), 0.0};  // HV
+    amp[2] = {dot(f1, rv), 0.0};  // VH
+    amp[1] = {dot(f1, rh), 0.0};  // HH
+}
+
 __device__ __forceinline__ void store_cv(double* p, const CV3& v) {
     p[0] = v.x.re; p[1] = v.x.im; p[2] = v.y.re; p[3] = v.y.im; p[4] = v.z.re; p[5] = v.z.im;
+}
+__device__ __forceinline__ void store_cv(double* p, const V3& v) {
+    p[0] = v.x; p[1] = 0.0; p[2] = v.y; p[3] = 0.0; p[4] = v.z; p[5] = 0.0;
 }
 
 __device__ __forceinline__ double shfl_d(double v, int src) {
@@ -561,6 +613,10 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
 }
 __device__ __forceinline__ double shfl_nt(double v, int src) { return shfl_d(v, src); }
 __device__ __forceinline__ Cx shfl_nt(Cx v, int src) { return {shfl_d(v.re, src), shfl_d(v.im, src)}; }
+__device__ __forceinline__ V3 shfl_ef(const V3& v, int src) { return {shfl_d(v.x, src), shfl_d(v.y, src), shfl_d(v.z, src)}; }
+__device__ __forceinline__ CV3 shfl_ef(const CV3& v, int src) {
+    return {shfl_nt(v.x, src), shfl_nt(v.y, src), shfl_nt(v.z, src)};
+}
 
 // ---------------------------------------------------------------------------
 // deterministic mode: per-thread branch stack in HBM, SoA over threads
@@ -572,26 +628,39 @@ __device__ __forceinline__ double& det_at(const TraceParams& P, uint64_t t, int 
     return P.det_stack[(static_cast<size_t>(f) * P.det_depth + d) * P.det_threads + t];
 }
 
-template <typename NT>
-__device__ __forceinline__ void det_push(const TraceParams& P, uint64_t t, int d, V3 o, V3 dir, const CV3& e0,
-                                         const CV3& e1, NT phi, NT n, int bounce) {
-    const double v[23] = {o.x, o.y, o.z, dir.x, dir.y, dir.z,
-                          e0.x.re, e0.x.im, e0.y.re, e0.y.im, e0.z.re, e0.z.im,
-                          e1.x.re, e1.x.im, e1.y.re, e1.y.im, e1.z.re, e1.z.im,
-                          re_of(phi), im_of(phi), re_of(n), im_of(n), static_cast<double>(bounce)};
+__device__ __forceinline__ void ef_store6(double* v, const CV3& e) {
+    v[0] = e.x.re; v[1] = e.x.im; v[2] = e.y.re; v[3] = e.y.im; v[4] = e.z.re; v[5] = e.z.im;
+}
+__device__ __forceinline__ void ef_store6(double* v, const V3& e) {
+    v[0] = e.x; v[1] = 0.0; v[2] = e.y; v[3] = 0.0; v[4] = e.z; v[5] = 0.0;
+}
+__device__ __forceinline__ void ef_load6(const double* v, CV3& e) { e = {{v[0], v[1]}, {v[2], v[3]}, {v[4], v[5]}}; }
+__device__ __forceinline__ void ef_load6(const double* v, V3& e) { e = {v[0], v[2], v[4]}; }
+
+template <typename NT, typename EF>
+__device__ __forceinline__ void det_push(const TraceParams& P, uint64_t t, int d, V3 o, V3 dir, const EF& e0,
+                                         const EF& e1, NT phi, NT n, int bounce) {
+    double v[23] = {o.x, o.y, o.z, dir.x, dir.y, dir.z};
+    ef_store6(v + 6, e0);
+    ef_store6(v + 12, e1);
+    v[18] = re_of(phi);
+    v[19] = im_of(phi);
+    v[20] = re_of(n);
+    v[21] = im_of(n);
+    v[22] = static_cast<double>(bounce);
 #pragma unroll
     for (int f = 0; f < 23; ++f) det_at(P, t, d, f) = v[f];
 }
 
-template <typename NT>
-__device__ __forceinline__ void det_pop(const TraceParams& P, uint64_t t, int d, Path<NT>& s) {
+template <typename NT, typename EF>
+__device__ __forceinline__ void det_pop(const TraceParams& P, uint64_t t, int d, Path<NT, EF>& s) {
     double v[23];
 #pragma unroll
     for (int f = 0; f < 23; ++f) v[f] = det_at(P, t, d, f);
     s.origin = {v[0], v[1], v[2]};
     s.dir = {v[3], v[4], v[5]};
-    s.e0 = {{v[6], v[7]}, {v[8], v[9]}, {v[10], v[11]}};
-    s.e1 = {{v[12], v[13]}, {v[14], v[15]}, {v[16], v[17]}};
+    ef_load6(v + 6, s.e0);
+    ef_load6(v + 12, s.e1);
     s.phi = make_nt<NT>(v[18], v[19]);
     s.medium_n = make_nt<NT>(v[20], v[21]);
     s.bounce = static_cast<int>(v[22]);
@@ -604,6 +673,7 @@ __device__ __forceinline__ double cvnorm(const CV3& v) {
     return sqrt((v.x.re * v.x.re + v.x.im * v.x.im) + (v.y.re * v.y.re + v.y.im * v.y.im) +
                 (v.z.re * v.z.re + v.z.im * v.z.im));
 }
+__device__ __forceinline__ double cvnorm(const V3& v) { return sqrt((v.x * v.x + v.y * v.y) + v.z * v.z); }
 
 // add a lane's stack accounting for one reference block (solver_det.cpp:127-132)
 __device__ __forceinline__ void det_flush(const TraceParams& P, uint64_t blk, uint64_t peak, uint64_t push) {
@@ -697,6 +767,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
     constexpr bool kRegAcc = kMode != kModeDefer;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
     using L = Layout<!kDiel && !kLossy, kLossy, kRegAcc>;
+    using EF = typename std::conditional<L::pec, V3, CV3>::type;  // field type
     constexpr int kFAcc = L::Acc;               // register-mode phasor sums
     constexpr int kSlotFields = L::Fields;      // doubles per thread
     __shared__ unsigned long long s_cnt[8];  // launched .. rounds (kCntLaunched..kCntRounds)
@@ -813,10 +884,10 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
         bool alive = false;  // lane holds a path (possibly only its last occlusion query)
         bool pend = false;   // next query is the chi occlusion test of a contribution
         bool dying = false;  // the path ends once its pending occlusion test is done
-        Path<NT> s;
+        Path<NT, EF> s;
         Cx amp[4];           // contribution: receiver-projected amplitudes (slot while pending)
         NT s_path{};         //               and net optical path
-        CV3 fj0, fm0, fj1, fm1;  // fan mode: the contribution's currents,
+        EF fj0, fm0, fj1, fm1;   // fan mode: the contribution's currents,
         NT fphi{};               // optical path
         V3 fpt = {0.0, 0.0, 0.0};  // and exit point, broadcast to the warp
 
@@ -889,7 +960,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 visible = !hit;
                 if (visible) {  // the queued contribution's amplitudes come back from the slot
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) amp[ch] = sl.getc(L::Amp + 2 * ch);
+                    for (int ch = 0; ch < 4; ++ch) amp[ch] = slot_get_amp<L>(sl, ch);
                     s_path = slot_get_nt<NT>(sl, L::SPath, L::SPathIm);
                 }
                 if (dying) {
@@ -930,10 +1001,10 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         const Coeffs co = pec ? coeffs_pec() : fresnel_any(n1, n2, cos_i, fault);
                         // ray geometry from the real parts (exact for the lossless model)
                         const Basis b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), !pec, fault);
-                        const CV3 er0 = interface_transform(s.e0, 0, co, b, fault);
-                        const CV3 er1 = interface_transform(s.e1, 0, co, b, fault);
+                        const EF er0 = interface_transform(s.e0, 0, co, b, fault);
+                        const EF er1 = interface_transform(s.e1, 0, co, b, fault);
                         const bool two = !pec && !co.tir;
-                        CV3 et0 = cvzero(), et1 = cvzero();
+                        EF et0 = ef_zero<EF>(), et1 = ef_zero<EF>();
                         if (two) {
                             et0 = interface_transform(s.e0, 1, co, b, fault);
                             et1 = interface_transform(s.e1, 1, co, b, fault);
@@ -944,12 +1015,12 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         candidate = !dark_exit && h.exterior_facing;
                         if (candidate) {
                             // meca_currents (farfield.cpp:11-45) for both pols
-                            CV3 j0, m0, j1, m1;
+                            EF j0, m0, j1, m1;
                             if (sc == 0) {
                                 j0 = cross(h.normal, cross(s.dir, s.e0) * s.medium_n) * 2.0;
                                 j1 = cross(h.normal, cross(s.dir, s.e1) * s.medium_n) * 2.0;
-                                m0 = cvzero();
-                                m1 = cvzero();
+                                m0 = ef_zero<EF>();
+                                m1 = ef_zero<EF>();
                             } else if (sc == 1) {
                                 j0 = cross(h.normal, (cross(s.dir, s.e0) + cross(b.dir_r, er0)) * s.medium_n);
                                 j1 = cross(h.normal, (cross(s.dir, s.e1) + cross(b.dir_r, er1)) * s.medium_n);
@@ -1094,7 +1165,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                     if (P.occlusion) {
                         pend = true;
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) sl.setc(L::Amp + 2 * ch, amp[ch]);
+                        for (int ch = 0; ch < 4; ++ch) slot_set_amp<L>(sl, ch, amp[ch]);
                         slot_set_nt(sl, L::SPath, L::SPathIm, s_path);
                         if (!alive) {
                             alive = true;
@@ -1121,16 +1192,9 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 while (fm) {
                     const int src = __ffs(fm) - 1;
                     fm &= fm - 1;
-                    CV3 c[4] = {fj0, fm0, fj1, fm1};
+                    EF c[4] = {fj0, fm0, fj1, fm1};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        c[k].x.re = shfl_d(c[k].x.re, src);
-                        c[k].x.im = shfl_d(c[k].x.im, src);
-                        c[k].y.re = shfl_d(c[k].y.re, src);
-                        c[k].y.im = shfl_d(c[k].y.im, src);
-                        c[k].z.re = shfl_d(c[k].z.re, src);
-                        c[k].z.im = shfl_d(c[k].z.im, src);
-                    }
+                    for (int k = 0; k < 4; ++k) c[k] = shfl_ef(c[k], src);
                     const NT ph = shfl_nt(fphi, src);
                     const V3 pt = {shfl_d(fpt.x, src), shfl_d(fpt.y, src), shfl_d(fpt.z, src)};
                     if (has_rx) {

@@ -108,3 +108,24 @@ def det_stats_vector(st):
                      st.cap_kills, st.peak_live_state_bytes, st.forced_stack_bytes,
                      st.state_bytes_per_ray, st.n_rounds] + list(st.rays_per_bounce[:32]),
                     dtype=np.uint64)
+
+
+def _zero_sign_free(x):
+    x = np.array(x, copy=True)
+    if x.dtype.kind == "f":
+        x[x == 0] = 0.0
+    return x
+
+
+def contribs_identical(a, b) -> bool:
+    """Contribution records bit for bit, every field, with one exception: the
+    sign of an exact zero is not compared (-0.0 == +0.0, IEEE equality).  The
+    PEC-only kernel carries the transverse fields in real arithmetic, where
+    the reference's complex arithmetic has imaginary parts of exactly +-0;
+    every nonzero value (and every integer) must still match bit for bit."""
+    if a.dtype != b.dtype or a.shape != b.shape:
+        return False
+    for name in a.dtype.names:
+        if _zero_sign_free(a[name]).tobytes() != _zero_sign_free(b[name]).tobytes():
+            return False
+    return True
