@@ -53,6 +53,7 @@ want = {
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
     "lts__t_bytes.sum": "l2_bytes",
     "lts__t_bytes.sum.per_second": "l2_bandwidth",
+    "lts__t_sectors.sum.per_second": "l2_sectors_per_second",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "l1tex__t_bytes.sum.per_second": "l1_bandwidth",
@@ -92,6 +93,11 @@ def to_bytes(x):
     return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(x["unit"], 1)
 
 
+if "l2_bandwidth" not in out and "l2_sectors_per_second" in out:  # 32-byte sectors
+    x = out["l2_sectors_per_second"]
+    per_ns = float(x["value"].replace(",", "")) * {"sector/ns": 1.0, "sector/us": 1e-3, "sector/s": 1e-9}.get(
+        x["unit"], float("nan"))
+    out["l2_bandwidth"] = {"value": f"{per_ns * 32:.3f}", "unit": "Gbyte/s"}
 dram = to_bytes(out["dram_read"]) + to_bytes(out["dram_write"])
 out["dram_bytes_per_launch"] = dram
 with open(os.path.join(prof, f"{tag}_{name}.json"), "w") as f:
