@@ -55,7 +55,9 @@ struct FRay {
     float ofx, ofy, ofz;  // origin * inv - margin: far planes
     float tlo;            // lower end of the box interval (0, or t_min rounded down)
     double t_skip;        // parameter of the traversal origin along the fp64 ray
-    int oct;              // ray octant: bit a set iff inv component a < 0
+    // byte offsets of the near-plane float4 of each axis inside a 128-byte
+    // node (16 * a + 16 iff inv component < 0); the far plane is at ^ 16
+    uint32_t offx, offy, offz;
 };
 
 // fp32 reciprocal of a direction component (relative error ~1e-7, covered by
@@ -110,7 +112,9 @@ __device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool o
     r.ofy = __fadd_rd(oy, -ey);
     r.ofz = __fadd_rd(oz, -ez);
     r.tlo = outside ? 0.0f : __double2float_rd(t_min * (1.0 - 1e-6));
-    r.oct = (r.ix < 0.0f ? 1 : 0) | (r.iy < 0.0f ? 2 : 0) | (r.iz < 0.0f ? 4 : 0);
+    r.offx = r.ix < 0.0f ? 16u : 0u;
+    r.offy = r.iy < 0.0f ? 48u : 32u;
+    r.offz = r.iz < 0.0f ? 80u : 64u;
     return r;
 }
 
@@ -235,10 +239,13 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             // near planes at (lo | octant bit) per axis, far planes at the other;
             // unused child slots hold empty boxes (lo = +inf, hi = -inf) and
             // always miss, so no child count is needed
-            const int ox = r.oct & 1, oy = (r.oct >> 1) & 1, oz = (r.oct >> 2) & 1;
-            const float4 nx = __ldg(nd + ox), fx = __ldg(nd + (ox ^ 1));
-            const float4 ny = __ldg(nd + 2 + oy), fy = __ldg(nd + 2 + (oy ^ 1));
-            const float4 nz = __ldg(nd + 4 + oz), fz = __ldg(nd + 4 + (oz ^ 1));
+            // nodes are 128-byte aligned: plane addresses are node | offset
+            // (near) and that ^ 16 (far), two logic ops per axis
+            const uint64_t nb = reinterpret_cast<uint64_t>(nd);
+            auto plane = [](uint64_t addr) { return __ldg(reinterpret_cast<const float4*>(addr)); };
+            const float4 nx = plane(nb | r.offx), fx = plane((nb | r.offx) ^ 16u);
+            const float4 ny = plane(nb | r.offy), fy = plane((nb | r.offy) ^ 16u);
+            const float4 nz = plane(nb | r.offz), fz = plane((nb | r.offz) ^ 16u);
             const float4 rf = __ldg(nd + 6);
             // plane distances two children at a time (FFMA2): [k].x child k, .y child k + 1
             const float2 xn[2] = {ffma2(nx.x, nx.y, r.ix, -r.onx), ffma2(nx.z, nx.w, r.ix, -r.onx)};

@@ -1,1 +1,2 @@
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:primary_kernel -s 1 -c 1 -o gpurun_out/c4_prim -f python tools/profile_isar.py c4 --angles 16 > gpurun_out/ncu_c4p.log 2>&1; echo "ncu rc=$?"
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python tools/ab.py --c2 --configs c1,c3,c4,c5 --reps 2 new= prev=prev 2>&1 | tail -3

@@ -23,6 +23,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("config", choices=["c4", "c5"])
 ap.add_argument("--angles", type=int, default=8)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--lossless", action="store_true", help="c5 skins with real permittivity (the reference's model)")
 a = ap.parse_args()
 if a.config == "c4":
     sd, _ = airframe(200_000, seed=4)
@@ -30,6 +31,8 @@ if a.config == "c4":
     freqs, n_az, half, rays = np.linspace(9.5e9, 10.5e9, 64), 64, 3.0, 2e6
 else:
     sd, _ = airframe(1_000_000, seed=5, dielectric_skin=True)
+    if a.lossless:
+        sd.eps_imag = None
     cfg = M.McConfig(strata_per_wavelength=10, samples_per_stratum=1, max_bounce=24, seed=5,
                      roulette=M.RouletteConfig(enabled=True, q=0.5, min_bounce=3))
     freqs, n_az, half, rays = np.linspace(8e9, 12e9, 128), 128, 5.0, 16e6
