@@ -1337,9 +1337,14 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
 // Sums use fused multiply-adds (their order differs from the reference's
 // anyway); the records of one span are nearly always one incidence, and the
 // sums are flushed with fp64 atomics whenever the incidence changes.
-template <int FPL>
+template <int FPL, bool kRealAmp>
 __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t f_begin) {
-    __shared__ double2 st[4][32][8];  // amp[4], (ph0, dph) | s, (la0, dla), W, incidence
+    // staged record: [0..3] amplitudes, [4] (ph0, dph) | s, [5] (la0, dla),
+    // [6] W = e^{-j 32 dk s}, [7] incidence.  (Measured and rejected: a
+    // per-record table of w^r, w^4q replacing the lane's sincos by two
+    // complex multiplies -- c5 +3.5%, the table doubles the shared memory.)
+    constexpr int kSt = 8;
+    __shared__ double2 st[4][32][kSt];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t n_all = *P.rec_count;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(P.rec_count + 1, n_all);  // peak for the host
@@ -1351,6 +1356,9 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
     const uint32_t f0 = f_begin + static_cast<uint32_t>(lane);
     double acc[FPL][8];
     const double2* recs = reinterpret_cast<const double2*>(P.recs);
+    auto cmul = [](Cx x, Cx y) { return Cx{__fma_rn(x.re, y.re, -x.im * y.im), __fma_rn(x.re, y.im, x.im * y.re)}; };
+    auto cx2 = [](double2 v) { return Cx{v.x, v.y}; };
+    auto d2 = [](Cx v) { return make_double2(v.re, v.im); };
     for (uint64_t r0 = gw * span; r0 < n; r0 += nw * span) {
         const uint64_t r1 = min(r0 + span, n);
         uint32_t cur = 0xffffffffu;
@@ -1385,10 +1393,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                     const double la0 = -(P.kph0 * sv.y), dla = -(P.kdph * sv.y);
                     t[4] = make_double2(ph0, dph);
                     t[5] = make_double2(la0, dla);
-                    if (FPL > 1) {
-                        const Cx w = polar_la(32.0 * dph, 32.0 * dla);
-                        t[6] = make_double2(w.re, w.im);
-                    }
+                    if (FPL > 1) t[6] = d2(polar_la(32.0 * dph, 32.0 * dla));
                 } else {
                     t[4] = sv;
                 }
@@ -1402,33 +1407,37 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                     cur = a;
                 }
                 if (f0 >= f_end) continue;
-                Cx am[4];
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) am[ch] = {t[ch].x, t[ch].y};
                 Cx z, w = {1.0, 0.0};
                 const double2 t4 = t[4];
                 if (P.uniform_f) {
                     const double2 t5 = t[5];
                     z = polar_la(t4.x + static_cast<double>(f0) * t4.y, t5.x + static_cast<double>(f0) * t5.y);
-                    if (FPL > 1) w = {t[6].x, t[6].y};
+                    if (FPL > 1) w = cx2(t[6]);
                 } else {
                     z = phasor(P.k0[f0], Cx{t4.x, t4.y});
                 }
+                Cx am[4];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) am[ch] = cx2(t[ch]);
 #pragma unroll
                 for (int m = 0; m < FPL; ++m) {
                     const uint32_t f = f0 + 32u * m;
                     if (f < f_end) {
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
-                            acc[m][2 * ch] = __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, acc[m][2 * ch]));
-                            acc[m][2 * ch + 1] =
-                                __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
+                            if (kRealAmp) {  // PEC scenes: the amplitudes are real
+                                acc[m][2 * ch] = __fma_rn(am[ch].re, z.re, acc[m][2 * ch]);
+                                acc[m][2 * ch + 1] = __fma_rn(am[ch].re, z.im, acc[m][2 * ch + 1]);
+                            } else {
+                                acc[m][2 * ch] =
+                                    __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, acc[m][2 * ch]));
+                                acc[m][2 * ch + 1] =
+                                    __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
+                            }
                         }
                         if (m + 1 < FPL && f + 32u < f_end) {
-                            if (P.uniform_f)
-                                z = {__fma_rn(z.re, w.re, -z.im * w.im), __fma_rn(z.re, w.im, z.im * w.re)};
-                            else
-                                z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
+                            if (P.uniform_f) z = cmul(z, w);
+                            else z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
                         }
                     }
                 }
@@ -1496,10 +1505,17 @@ static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int thre
 cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const unsigned blocks = static_cast<unsigned>(device_sms) * 4;
     const uint32_t fpl = p.nf <= 32 ? 1 : (p.nf <= 64 ? 2 : 4);
+    const bool real_amp = p.scene.all_pec && !p.scene.lossy;  // PEC paths carry real amplitudes
     for (uint32_t fb = 0; fb < p.nf; fb += 32 * fpl) {
-        if (fpl == 1) accumulate_kernel<1><<<blocks, 128, 0, stream>>>(p, fb);
-        else if (fpl == 2) accumulate_kernel<2><<<blocks, 128, 0, stream>>>(p, fb);
-        else accumulate_kernel<4><<<blocks, 128, 0, stream>>>(p, fb);
+        if (real_amp) {
+            if (fpl == 1) accumulate_kernel<1, true><<<blocks, 128, 0, stream>>>(p, fb);
+            else if (fpl == 2) accumulate_kernel<2, true><<<blocks, 128, 0, stream>>>(p, fb);
+            else accumulate_kernel<4, true><<<blocks, 128, 0, stream>>>(p, fb);
+        } else {
+            if (fpl == 1) accumulate_kernel<1, false><<<blocks, 128, 0, stream>>>(p, fb);
+            else if (fpl == 2) accumulate_kernel<2, false><<<blocks, 128, 0, stream>>>(p, fb);
+            else accumulate_kernel<4, false><<<blocks, 128, 0, stream>>>(p, fb);
+        }
         if (launches) ++*launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -118,7 +118,7 @@ def isar(name, sd, n_az, az_half, freqs, rays, cfg, gpu_angles, cpu, cpu_sd=None
     sel = az[np.linspace(0, n_az - 1, gpu_angles).round().astype(int)]
     excs = [M.monostatic_excitation(90.0, float(a)) for a in sel]
     spws = [spw_for(s, e, lam, rays) for e in excs]
-    vals, st = run_gpu(s, list(zip(excs, spws)), [[e] for e in excs], freqs, cfg, reps=1 if rays > 4e6 else 2)
+    vals, st = run_gpu(s, list(zip(excs, spws)), [[e] for e in excs], freqs, cfg, reps=2)
     per_angle_ms = st.kernel_ms / len(excs)
     out = {"config": name, "triangles": int(sd.n_triangles), "frequencies": len(freqs),
            "azimuths": n_az, "paths_per_angle": st.rays_launched / len(excs),
@@ -153,7 +153,7 @@ def c5(cpu):
         cpu_sd.eps_imag = None
     return isar("c5 airframe (~1M tris, seed 5), lossy 2-layer skins on wings/fin, ISAR 128 f "
                 "(8-12 GHz) x 128 az (+-5 deg), 16M paths/angle, RR, max 24", sd, 128, 5.0,
-                np.linspace(8e9, 12e9, 128), 16e6, cfg, 4, cpu, cpu_sd)
+                np.linspace(8e9, 12e9, 128), 16e6, cfg, 128, cpu, cpu_sd)
 
 
 def main():
