@@ -4,7 +4,9 @@
 //   1. prim_kernel      per triangle: fp64 AABB padded by box_pad and rounded
 //                       outward to fp32; 63-bit Morton code of the centroid.
 //   2. cub radix sort   (morton, id) pairs.
-//   3. karras_kernel    Karras (HPG 2012) binary radix tree over the sorted codes
+//   3. sah_split_kernel binned-SAH top-down build from the Morton order, one
+//                       block per node and level (default); fallback / MCSBR_BVH=lbvh:
+//      karras_kernel    Karras (HPG 2012) binary radix tree over the sorted codes
 //                       (ties broken by sort position), one thread per inner node.
 //   4. refit_kernel     bottom-up AABB union with one atomic flag per inner node.
 //   5. parity/scan/emit4  collapse to a 4-wide BVH: every inner node at even
@@ -22,6 +24,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -293,6 +297,233 @@ __global__ void depth_kernel(int n, const int* __restrict__ parent_inner, const 
     atomicMax(max_depth, static_cast<unsigned int>(d));
 }
 
+
+// ---------------------------------------------------------------------------
+// Binned-SAH top-down build (default; the Karras LBVH is the fallback).
+// One block per node of a level: centroid bounds, 16 bins per axis holding
+// counts and primitive boxes (shared atomics on order-preserving float
+// encodings), the SAH sweep A_L N_L + A_R N_R over the 15 bin boundaries of
+// each axis, then a stable block-wide partition of the node's index range.
+// Nodes split down to single triangles, so the output has the exact shape of
+// the Karras tree (n - 1 inner nodes, child / range / parent arrays, leaves
+// ~position in the final order) and the refit / collapse / emit stages run
+// unchanged; ranges stay contiguous because every split partitions its own
+// range.  The level loop runs on the host (one small readback per level).
+
+struct SahTask {
+    int first, count, node;
+};
+
+constexpr int kSahBins = 16;
+constexpr int kSahThreads = 256;
+
+__device__ __forceinline__ int fenc(float f) {  // int order == float order
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float fdec(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+__device__ __forceinline__ float half_area(float lx, float ly, float lz, float hx, float hy, float hz) {
+    const float dx = hx - lx, dy = hy - ly, dz = hz - lz;
+    return (dx < 0.f || dy < 0.f || dz < 0.f) ? 0.f : dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
+    const SahTask* __restrict__ tasks, const float4* __restrict__ blo, const float4* __restrict__ bhi,
+    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
+    int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ next,
+    int* __restrict__ next_count) {
+    __shared__ int s_cnt[3][kSahBins];
+    __shared__ int s_box[3][kSahBins][6];
+    __shared__ float s_red[2][3][kSahThreads / 32];
+    __shared__ float s_cmin[3], s_scale[3];
+    __shared__ float s_cost[3];
+    __shared__ int s_split[3], s_nl[3];
+    __shared__ int s_warp_l[kSahThreads / 32];
+    const SahTask t = tasks[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int end = t.first + t.count;
+    auto centroid = [&](uint32_t p, int a) {
+        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
+        const float lv = a == 0 ? l.x : (a == 1 ? l.y : l.z), hv = a == 0 ? h.x : (a == 1 ? h.y : h.z);
+        return 0.5f * (lv + hv);
+    };
+    // 1. centroid bounds
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = t.first + tid; i < end; i += kSahThreads) {
+        const uint32_t p = idx[i];
+        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
+        const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = fminf(mn[a], c[a]);
+            mx[a] = fmaxf(mx[a], c[a]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+        if (lane == 0) {
+            s_red[0][a][wid] = mn[a];
+            s_red[1][a][wid] = mx[a];
+        }
+    }
+    for (int i = tid; i < 3 * kSahBins; i += kSahThreads) {
+        const int a = i / kSahBins, b = i % kSahBins;
+        s_cnt[a][b] = 0;
+        s_box[a][b][0] = s_box[a][b][1] = s_box[a][b][2] = fenc(INFINITY);
+        s_box[a][b][3] = s_box[a][b][4] = s_box[a][b][5] = fenc(-INFINITY);
+    }
+    __syncthreads();
+    if (tid < 3) {
+        float lo = INFINITY, hi = -INFINITY;
+        for (int w = 0; w < kSahThreads / 32; ++w) {
+            lo = fminf(lo, s_red[0][tid][w]);
+            hi = fmaxf(hi, s_red[1][tid][w]);
+        }
+        s_cmin[tid] = lo;
+        s_scale[tid] = hi > lo ? (kSahBins * (1.0f - 1e-6f)) / (hi - lo) : 0.0f;
+    }
+    __syncthreads();
+    // 2. bins
+    for (int i = t.first + tid; i < end; i += kSahThreads) {
+        const uint32_t p = idx[i];
+        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
+        const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (s_scale[a] == 0.0f) continue;
+            const int b = min(kSahBins - 1, max(0, static_cast<int>((c[a] - s_cmin[a]) * s_scale[a])));
+            atomicAdd(&s_cnt[a][b], 1);
+            atomicMin(&s_box[a][b][0], fenc(l.x));
+            atomicMin(&s_box[a][b][1], fenc(l.y));
+            atomicMin(&s_box[a][b][2], fenc(l.z));
+            atomicMax(&s_box[a][b][3], fenc(h.x));
+            atomicMax(&s_box[a][b][4], fenc(h.y));
+            atomicMax(&s_box[a][b][5], fenc(h.z));
+        }
+    }
+    __syncthreads();
+    // 3. SAH sweep per axis
+    if (tid < 3) {
+        const int a = tid;
+        float best = INFINITY;
+        int split = -1, nl_best = 0;
+        if (s_scale[a] != 0.0f) {
+            float ra[kSahBins];
+            int rc[kSahBins];
+            float l0 = INFINITY, l1 = INFINITY, l2 = INFINITY, h0 = -INFINITY, h1 = -INFINITY, h2 = -INFINITY;
+            int n = 0;
+            for (int b = kSahBins - 1; b >= 1; --b) {  // suffix: bins b..15
+                n += s_cnt[a][b];
+                l0 = fminf(l0, fdec(s_box[a][b][0]));
+                l1 = fminf(l1, fdec(s_box[a][b][1]));
+                l2 = fminf(l2, fdec(s_box[a][b][2]));
+                h0 = fmaxf(h0, fdec(s_box[a][b][3]));
+                h1 = fmaxf(h1, fdec(s_box[a][b][4]));
+                h2 = fmaxf(h2, fdec(s_box[a][b][5]));
+                ra[b] = half_area(l0, l1, l2, h0, h1, h2);
+                rc[b] = n;
+            }
+            l0 = l1 = l2 = INFINITY;
+            h0 = h1 = h2 = -INFINITY;
+            n = 0;
+            for (int b = 0; b < kSahBins - 1; ++b) {  // prefix: bins 0..b | b+1..15
+                n += s_cnt[a][b];
+                l0 = fminf(l0, fdec(s_box[a][b][0]));
+                l1 = fminf(l1, fdec(s_box[a][b][1]));
+                l2 = fminf(l2, fdec(s_box[a][b][2]));
+                h0 = fmaxf(h0, fdec(s_box[a][b][3]));
+                h1 = fmaxf(h1, fdec(s_box[a][b][4]));
+                h2 = fmaxf(h2, fdec(s_box[a][b][5]));
+                if (n == 0 || rc[b + 1] == 0) continue;
+                const float cost = half_area(l0, l1, l2, h0, h1, h2) * n + ra[b + 1] * rc[b + 1];
+                if (cost < best) {
+                    best = cost;
+                    split = b + 1;
+                    nl_best = n;
+                }
+            }
+        }
+        s_cost[a] = best;
+        s_split[a] = split;
+        s_nl[a] = nl_best;
+    }
+    __syncthreads();
+    int axis = -1;
+    float best = INFINITY;
+    for (int a = 0; a < 3; ++a)
+        if (s_split[a] >= 0 && s_cost[a] < best) {
+            best = s_cost[a];
+            axis = a;
+        }
+    const int nl = axis >= 0 ? s_nl[axis] : t.count / 2;  // no usable split: median by position
+    const int split = axis >= 0 ? s_split[axis] : 0;
+    const float cmin = axis >= 0 ? s_cmin[axis] : 0.0f, scale = axis >= 0 ? s_scale[axis] : 0.0f;
+    // 4. stable partition of [first, end) into idx2, then back
+    int left_base = 0, right_base = 0;
+    for (int base = t.first; base < end; base += kSahThreads) {
+        const int i = base + tid;
+        bool valid = i < end, left = false;
+        uint32_t p = 0;
+        if (valid) {
+            p = idx[i];
+            if (axis >= 0) {
+                const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(p, axis) - cmin) * scale)));
+                left = b < split;
+            } else {
+                left = (i - t.first) < nl;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, valid && left);
+        const unsigned v = __ballot_sync(0xffffffffu, valid);
+        if (lane == 0) s_warp_l[wid] = __popc(m) | (__popc(v) << 16);
+        __syncthreads();
+        int wl = 0, wv = 0, tl = 0, tv = 0;
+        for (int w = 0; w < kSahThreads / 32; ++w) {
+            const int x = s_warp_l[w];
+            if (w < wid) {
+                wl += x & 0xffff;
+                wv += x >> 16;
+            }
+            tl += x & 0xffff;
+            tv += x >> 16;
+        }
+        if (valid) {
+            const unsigned below = (1u << lane) - 1u;
+            const int pl = wl + __popc(m & below);
+            const int pv = wv + __popc(v & below);
+            const int pos = left ? t.first + left_base + pl : t.first + nl + right_base + (pv - pl);
+            idx2[pos] = p;
+        }
+        left_base += tl;
+        right_base += tv - tl;
+        __syncthreads();
+    }
+    for (int i = t.first + tid; i < end; i += kSahThreads) idx[i] = idx2[i];
+    // 5. children
+    if (tid == 0) {
+        const int starts[2] = {t.first, t.first + nl}, sizes[2] = {nl, t.count - nl};
+        int enc[2];
+        for (int k = 0; k < 2; ++k) {
+            if (sizes[k] == 1) {
+                enc[k] = ~starts[k];
+                par_l[starts[k]] = t.node;
+            } else {
+                const int id = atomicAdd(node_counter, 1);
+                enc[k] = id;
+                par_i[id] = t.node;
+                next[atomicAdd(next_count, 1)] = SahTask{starts[k], sizes[k], id};
+            }
+        }
+        child[t.node] = make_int2(enc[0], enc[1]);
+        range[t.node] = make_int2(t.first, end - 1);
+    }
+}
+
 }  // namespace
 
 #define BVH_CHECK(x)                          \
@@ -317,6 +548,10 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     int *par_i = nullptr, *par_l = nullptr, *flags = nullptr;
     unsigned int* dmax = nullptr;
     unsigned int *is4 = nullptr, *idx4 = nullptr;
+    uint32_t* sidx = nullptr;         // SAH: the final triangle order
+    SahTask *tasks = nullptr, *tasks2 = nullptr;
+    int *node_counter = nullptr, *next_count = nullptr;
+    const uint32_t* order = nullptr;  // final leaf order (SAH or Morton)
     void* tmp = nullptr;
     void* scan_tmp = nullptr;
     size_t tmp_bytes = 0, scan_bytes = 0;
@@ -368,12 +603,59 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     BVH_CHECK(cudaMalloc(&tmp, tmp_bytes));
     BVH_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
                                               stream));
-    tri_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, ids_s, n_tri, out->tri64);
+    order = ids_s;
+    if (n > 1) {
+        // binned SAH from the Morton order (locality), unless MCSBR_BVH=lbvh or
+        // the tree comes out deeper than the traversal stack allows
+        const char* bvh_env = std::getenv("MCSBR_BVH");
+        bool sah = !(bvh_env && std::strcmp(bvh_env, "lbvh") == 0);
+        if (sah) {
+            BVH_CHECK(cudaMalloc(&sidx, sizeof(uint32_t) * n));
+            BVH_CHECK(cudaMalloc(&tasks, sizeof(SahTask) * (n / 2 + 1)));
+            BVH_CHECK(cudaMalloc(&tasks2, sizeof(SahTask) * (n / 2 + 1)));
+            BVH_CHECK(cudaMalloc(&node_counter, sizeof(int) * 2));
+            next_count = node_counter + 1;
+            BVH_CHECK(cudaMemcpyAsync(sidx, ids_s, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
+            const int one = 1;
+            const SahTask root{0, n, 0};
+            BVH_CHECK(cudaMemcpyAsync(node_counter, &one, sizeof(int), cudaMemcpyHostToDevice, stream));
+            BVH_CHECK(cudaMemcpyAsync(tasks, &root, sizeof(SahTask), cudaMemcpyHostToDevice, stream));
+            int h_tasks = 1;
+            while (h_tasks > 0) {
+                BVH_CHECK(cudaMemsetAsync(next_count, 0, sizeof(int), stream));
+                sah_split_kernel<<<h_tasks, kSahThreads, 0, stream>>>(tasks, blo, bhi, sidx, ids, child, range,
+                                                                      par_i, par_l, node_counter, tasks2,
+                                                                      next_count);
+                BVH_CHECK(cudaGetLastError());
+                BVH_CHECK(cudaMemcpyAsync(&h_tasks, next_count, sizeof(int), cudaMemcpyDeviceToHost, stream));
+                BVH_CHECK(cudaStreamSynchronize(stream));
+                SahTask* sw = tasks;
+                tasks = tasks2;
+                tasks2 = sw;
+            }
+            depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
+            BVH_CHECK(cudaGetLastError());
+            unsigned int md = 0;
+            BVH_CHECK(cudaMemcpyAsync(&md, dmax, sizeof(md), cudaMemcpyDeviceToHost, stream));
+            BVH_CHECK(cudaStreamSynchronize(stream));
+            if (3 * ((md + 1) / 2 + 1) > static_cast<unsigned>(kStackSize)) {
+                sah = false;  // too deep for the traversal stack: Karras tree instead
+                BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
+                BVH_CHECK(cudaMemsetAsync(par_i, 0xff, sizeof(int) * inner, stream));
+                BVH_CHECK(cudaMemsetAsync(par_l, 0xff, sizeof(int) * n, stream));
+            } else {
+                order = sidx;
+            }
+        }
+        if (!sah) {
+            karras_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(keys_s, n, child, range, par_i, par_l);
+            BVH_CHECK(cudaGetLastError());
+        }
+    }
+    tri_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, order, n_tri, out->tri64);
     BVH_CHECK(cudaGetLastError());
     if (n > 1) {
-        gather_boxes<<<G, B, 0, stream>>>(blo, bhi, ids_s, n, blo_s, bhi_s);
-        BVH_CHECK(cudaGetLastError());
-        karras_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(keys_s, n, child, range, par_i, par_l);
+        gather_boxes<<<G, B, 0, stream>>>(blo, bhi, order, n, blo_s, bhi_s);
         BVH_CHECK(cudaGetLastError());
         refit_kernel<<<G, B, 0, stream>>>(n, child, par_i, par_l, blo_s, bhi_s, ilo, ihi, flags);
         BVH_CHECK(cudaGetLastError());
@@ -385,8 +667,10 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         emit4_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, is4, idx4, ilo, ihi, blo_s,
                                                             bhi_s, out->nodes);
         BVH_CHECK(cudaGetLastError());
-        depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
-        BVH_CHECK(cudaGetLastError());
+        if (order != sidx) {  // (the SAH path measured its depth already)
+            depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
+            BVH_CHECK(cudaGetLastError());
+        }
     }
     BVH_CHECK(cudaEventRecord(e1, stream));
     {
@@ -428,6 +712,10 @@ done:
     cudaFree(idx4);
     cudaFree(tmp);
     cudaFree(scan_tmp);
+    cudaFree(sidx);
+    cudaFree(tasks);
+    cudaFree(tasks2);
+    cudaFree(node_counter);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (err != cudaSuccess) {
