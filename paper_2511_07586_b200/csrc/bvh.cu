@@ -314,7 +314,10 @@ struct SahTask {
     int first, count, node;
 };
 
-constexpr int kSahBins = 16;
+#ifndef MCSBR_SAH_BINS
+#define MCSBR_SAH_BINS 16
+#endif
+constexpr int kSahBins = MCSBR_SAH_BINS;
 constexpr int kSahThreads = 256;
 
 __device__ __forceinline__ int fenc(float f) {  // int order == float order
