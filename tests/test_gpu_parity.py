@@ -330,3 +330,32 @@ def test_deferred_accumulation_overflow_and_groups(knob, monkeypatch):
         ref = oracle_estimate(sd, e, freqs, cfg, contributions=False)
         scale = max(np.max(np.abs(ref["values"])), 1e-300)
         assert np.max(np.abs(vals[i, 0] - ref["values"])) <= 1e-9 * scale
+
+
+@pytest.mark.parametrize("builder", ["sah", "lbvh"])
+def test_both_bvh_builders_are_exact(builder, monkeypatch):
+    """The binned-SAH tree (default) and the Karras LBVH (fallback) only cull:
+    closest hits == brute force for 1e5 random rays, and a full estimate's
+    contributions are identical to the oracle, whichever tree traces them."""
+    if builder == "lbvh":
+        monkeypatch.setenv("MCSBR_BVH", "lbvh")
+    from paper_2511_07586_b200.geometry import airframe
+
+    sd, _ = airframe(6_000, seed=4)
+    s = M.Scene(sd)
+    info = s.bvh_info()
+    assert info["nodes"] > 0 and info["max_depth"] > 0
+    rng = np.random.default_rng(7)
+    o, d = _random_rays(rng, 100000, sd.bounding_radius * 2, sd)
+    t_min = np.zeros(len(o))
+    t, ids = s.intersect_batch(o, d, t_min)
+    hb = oracle.intersect("port", oracle.port_scene(sd), o, d, t_min, 1)
+    assert np.array_equal(ids, hb[:, 12].astype(np.uint32))
+    hit = ids != 0xFFFFFFFF
+    assert hit.sum() > 1000 and np.array_equal(t[hit], hb[hit, 0])
+    exc = M.monostatic_excitation(85.0, 10.0)
+    cfg = M.McConfig(strata_per_wavelength=1.0, samples_per_stratum=1, seed=4, max_bounce=10)
+    got = []
+    M.estimate(s, exc, [10e9], cfg, contributions_out=got)
+    ref = oracle_estimate(sd, exc, [10e9], cfg)
+    assert contribs_identical(sort_contribs(ref["contributions"]), got[0])
