@@ -185,7 +185,10 @@ int plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw
     out->nv = std::max(1, static_cast<int>(std::ceil(2.0 * out->half_v / target)));
     const double area = 4.0 * out->half_u * out->half_v;
     out->cell_area = area / (static_cast<double>(out->nu) * out->nv);
-    out->entries = static_cast<uint64_t>(out->nu * out->nv) * static_cast<uint64_t>(spp);
+    const uint64_t cells = static_cast<uint64_t>(out->nu) * static_cast<uint64_t>(out->nv);
+    if (cells >= (uint64_t{1} << 32))  // the device keys cells in 32 bits
+        return set_err(MCSBR_EINVAL, "build_strata: more than 2^32 strata per incidence");
+    out->entries = cells * static_cast<uint64_t>(spp);
     return MCSBR_OK;
 }
 
