@@ -240,9 +240,13 @@ __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs
 __device__ inline V3 interface_transform(const V3& e, int branch, const Coeffs& co, const Basis& b,
                                          uint32_t& fault) {
     const V3 dir_in = cross(b.s_hat, b.p_in);
-    const double lim = 1e-9 * (1.0 + norm(e));
+    // transversality guard: (1 + |e|)^2 >= 1 + |e|^2, so the square root is
+    // only needed when the cheap bound does not already clear the field
     const double de = dot(e, dir_in);
-    if (de * de > lim * lim) fault |= kFaultTransverse;
+    if (de * de > 1e-18 * (1.0 + dot(e, e))) {
+        const double lim = 1e-9 * (1.0 + norm(e));
+        if (de * de > lim * lim) fault |= kFaultTransverse;
+    }
     const double es = dot(e, b.s_hat);
     const double ep = dot(e, b.p_in);
     if (branch == 0) return b.s_hat * (es * co.r_s.re) + b.p_out_r * (ep * co.r_p.re);

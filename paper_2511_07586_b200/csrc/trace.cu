@@ -497,6 +497,17 @@ __device__ __forceinline__ void load_em(const Slot& sl, Path<NT, EF>& s, double 
     }
 }
 
+// real amplitudes (PEC path): am.im is 0, so (am * z) = (am.re z.re, am.re z.im)
+// up to the sign of zero
+template <int kAcc>
+__device__ __forceinline__ void acc_add_real(const Slot& sl, const Cx am[4], Cx z) {
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+        sl.set(kAcc + 2 * ch, sl.get(kAcc + 2 * ch) + am[ch].re * z.re);
+        sl.set(kAcc + 2 * ch + 1, sl.get(kAcc + 2 * ch + 1) + am[ch].re * z.im);
+    }
+}
+
 template <int kAcc>
 __device__ __forceinline__ void acc_add(const Slot& sl, const Cx am[4], Cx z) {
 #pragma unroll
@@ -608,6 +619,18 @@ __device__ __forceinline__ void project(const RxDev& R, const V3& aj0, const V3&
     const V3 ks = ld3(R.k_s), rv = ld3(R.rx_v), rh = ld3(R.rx_h);
     const V3 f0 = cross(ks, cross(ks, aj0)) + cross(ks, am0);
     const V3 f1 = cross(ks, cross(ks, aj1)) + cross(ks, am1);
+    amp[0] = {dot(f0, rv), 0.0};  // VV
+    amp[3] = {dot(f0, rh), 0.0};  // HV
+    amp[2] = {dot(f1, rv), 0.0};  // VH
+    amp[1] = {dot(f1, rh), 0.0};  // HH
+}
+
+// PEC hits have no magnetic current (sc == 0): the k_s x m term of the
+// projection is a zero vector and only flips signs of zeros, so it is skipped
+__device__ __forceinline__ void project_pec(const RxDev& R, const V3& aj0, const V3& aj1, Cx amp[4]) {
+    const V3 ks = ld3(R.k_s), rv = ld3(R.rx_v), rh = ld3(R.rx_h);
+    const V3 f0 = cross(ks, cross(ks, aj0));
+    const V3 f1 = cross(ks, cross(ks, aj1));
     amp[0] = {dot(f0, rv), 0.0};  // VV
     amp[3] = {dot(f0, rh), 0.0};  // HV
     amp[2] = {dot(f1, rv), 0.0};  // VH
@@ -1061,7 +1084,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                                 fphi = s.phi;
                                 fpt = point;
                             } else {
-                                project(R, j0, m0, j1, m1, amp);
+                                if constexpr (L::pec) project_pec(R, j0, j1, amp);  // m = 0 on PEC hits
+                                else project(R, j0, m0, j1, m1, amp);
                                 s_path = s.phi - dot(ld3(R.k_s), point);
                             }
                             if (scratch) {
@@ -1231,7 +1255,10 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 }
             } else if (kRegAcc) {
                 // ---- phasor accumulation (farfield.cpp:130-146) ----
-                if (visible) acc_add<kFAcc>(sl, amp, phasor(P.k0[0], s_path));
+                if (visible) {
+                    if constexpr (L::pec) acc_add_real<kFAcc>(sl, amp, phasor(P.k0[0], s_path));
+                    else acc_add<kFAcc>(sl, amp, phasor(P.k0[0], s_path));
+                }
             } else {
                 // ---- deferred accumulation: append the contribution record ----
                 const unsigned vm = __ballot_sync(kFull, visible);
