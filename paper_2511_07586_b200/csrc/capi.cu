@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -300,12 +301,35 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     job->k0.resize(nf);
     for (uint32_t f = 0; f < nf; ++f) job->k0[f] = 2.0 * kPi * freqs[f] / kC;
     uint64_t total = 0;
+    // launch rectangles: O(vertices) each, independent per incidence -> host
+    // threads when the batch is large (an azimuth sweep); a failing incidence
+    // is re-planned on this thread so the error message lands here
+    std::vector<mcsbr_launch_plan> plans(n_inc);
+    std::vector<int> prc(n_inc, MCSBR_OK);
+    auto plan_range = [&](uint32_t a0, uint32_t a1) {
+        for (uint32_t a = a0; a < a1; ++a) {
+            const double spw_a = incs[a].strata_per_wavelength > 0.0 ? incs[a].strata_per_wavelength
+                                                                       : cfg->strata_per_wavelength;
+            prc[a] = plan(s, incs[a].k_inc, cfg->launch_padding, spw_a, lambda_ref, cfg->samples_per_stratum,
+                          &plans[a]);
+        }
+    };
+    const uint64_t work = static_cast<uint64_t>(n_inc) * s->nv;
+    const uint32_t nthreads = work < 200000 ? 1u
+                              : std::min<uint32_t>(n_inc, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (nthreads <= 1) {
+        plan_range(0, n_inc);
+    } else {
+        std::vector<std::thread> pool;
+        for (uint32_t t = 0; t < nthreads; ++t)
+            pool.emplace_back(plan_range, n_inc * t / nthreads, n_inc * (t + 1) / nthreads);
+        for (auto& th : pool) th.join();
+    }
     for (uint32_t a = 0; a < n_inc; ++a) {
         const mcsbr_incidence& in = incs[a];
         const double spw = in.strata_per_wavelength > 0.0 ? in.strata_per_wavelength : cfg->strata_per_wavelength;
-        mcsbr_launch_plan lp;
-        rc = plan(s, in.k_inc, cfg->launch_padding, spw, lambda_ref, cfg->samples_per_stratum, &lp);
-        if (rc) return rc;
+        mcsbr_launch_plan lp = plans[a];
+        if (prc[a]) return plan(s, in.k_inc, cfg->launch_padding, spw, lambda_ref, cfg->samples_per_stratum, &lp);
         if (lp.entries == 0) return set_err(MCSBR_EINVAL, "estimate: empty strata grid");
         IncDev& d = job->inc[a];
         std::memset(&d, 0, sizeof(d));
