@@ -614,15 +614,18 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
         return set_err(MCSBR_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
     if (device < 0 || device >= ndev) return set_err(MCSBR_EINVAL, "scene_create: bad device index");
     CK(cudaSetDevice(device), "cudaSetDevice");
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-    if (prop.major < 10)
+    // two attributes, not cudaGetDeviceProperties (which costs ~1 ms per call)
+    int cc_major = 0, cc_minor = 0, n_sm = 0;
+    CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device), "cudaDeviceGetAttribute");
+    CK(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device), "cudaDeviceGetAttribute");
+    CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+    if (cc_major < 10)
         return set_err(MCSBR_ECUDA, "this library is built for sm_100a (B200); device is sm_" +
-                                        std::to_string(prop.major) + std::to_string(prop.minor));
+                                        std::to_string(cc_major) + std::to_string(cc_minor));
 
     auto* s = new mcsbr_scene();
     s->device = device;
-    s->sms = prop.multiProcessorCount;
+    s->sms = n_sm;
     s->nv = nv;
     s->nt = nt;
     s->nm = nm;
