@@ -454,7 +454,11 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     p.chunk_max = env_u32("MCSBR_CHUNK_MAX", 256);
     p.chunk_min = env_u32("MCSBR_CHUNK_MIN", 32);
     p.gss_div = env_u32("MCSBR_GSS", 16);
-    p.band_order = static_cast<int32_t>(env_u32("MCSBR_BAND", 1));
+    // band height of the launch-entry dispatch order (0 = linear; a power of two)
+    {
+        const uint32_t bh = env_u32("MCSBR_BAND", 4);
+        p.band_order = static_cast<int32_t>(bh & (bh - 1) ? 4 : bh);
+    }
     p.uniform_f = job.uniform_f;
     p.kph0 = job.kph0;
     p.kdph = job.kdph;

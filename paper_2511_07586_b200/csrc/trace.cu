@@ -546,12 +546,13 @@ __device__ __forceinline__ Entry locate(const TraceParams& P, const IncDev& I, u
     const uint32_t nu = static_cast<uint32_t>(I.nu), nv = static_cast<uint32_t>(I.nv);
     Entry e;
     if (P.band_order) {
-        const uint32_t band = cg / (4u * nu);
-        const uint32_t r = cg - band * 4u * nu;
-        const uint32_t h = min(4u, nv - 4u * band);
-        const uint32_t col = h == 4u ? (r >> 2) : r / h;
+        const uint32_t bh = static_cast<uint32_t>(P.band_order);  // band height (rows)
+        const uint32_t band = cg / (bh * nu);
+        const uint32_t r = cg - band * bh * nu;
+        const uint32_t h = min(bh, nv - bh * band);
+        const uint32_t col = h == bh ? (r >> (31 - __clz(bh))) : r / h;  // bh is a power of two
         e.i = col;
-        e.j = 4u * band + (r - col * h);
+        e.j = bh * band + (r - col * h);
     } else {
         e.j = cg / nu;
         e.i = cg - e.j * nu;
