@@ -356,6 +356,27 @@ def main():
     T = sd.n_triangles
     bq = 64 * math.ceil(math.log2(T / 4)) + 4 * 48  # SURVEY.md §8d traversal bytes per query
     queries = int(kst.segments_traced) + int(kst.occlusion_queries)
+    # accumulation roofline: C * R * (160 + 32 F) FP32-equivalent
+    # flops + C * R * F sincos per path against the FP32 / SFU peaks at the
+    # measured max clock (the kernel computes them in fp64: a lower bound on
+    # the work, so the fraction is an upper bound on the share)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            f_clk = float(json.load(f).get("sm_max_mhz", 1965.0)) * 1e6
+    except Exception:
+        f_clk = 1965.0e6
+    contribs = int(kst.contributions)
+    acc_flops = contribs * (160 + 32 * nf)
+    acc_sincos = contribs * nf
+    acc = {"model": "SURVEY.md 8d: C*R*(160+32F) FP32 flops + C*R*F sincos per path (F = 1, R = 1)",
+           "contributions_per_path": contribs / max(int(kst.rays_launched), 1),
+           "fp32_tflops": acc_flops / (kernel_ms / 1e3) / 1e12,
+           "fp32_peak_tflops": sm_count * 128 * 2 * f_clk / 1e12,
+           "sincos_per_s": acc_sincos / (kernel_ms / 1e3),
+           "sfu_peak_per_s": sm_count * 16 * f_clk}
+    acc["fp32_frac"] = acc["fp32_tflops"] / acc["fp32_peak_tflops"]
+    acc["sfu_frac"] = acc["sincos_per_s"] / acc["sfu_peak_per_s"]
     alg_bytes = queries * bq
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
@@ -451,6 +472,7 @@ def main():
                                  "from DRAM; the working set is cache-resident (see ncu), so frac > 1 "
                                  "means the kernel moves the model's bytes faster than HBM could"},
             "ncu": ncu,
+            "accumulation_roofline": acc,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks,
