@@ -319,6 +319,7 @@ struct SahTask {
 #endif
 constexpr int kSahBins = MCSBR_SAH_BINS;
 constexpr int kSahThreads = 256;
+constexpr int kSahSample = 16384;  // primitives sampled to choose the split of a large node
 
 __device__ __forceinline__ int fenc(float f) {  // int order == float order
     const int i = __float_as_int(f);
@@ -351,9 +352,12 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
         const float lv = a == 0 ? l.x : (a == 1 ? l.y : l.z), hv = a == 0 ? h.x : (a == 1 ? h.y : h.z);
         return 0.5f * (lv + hv);
     };
+    // large nodes (the top levels, one block each) choose their split from a
+    // strided sample of ~16 k primitives; the partition below counts exactly
+    const int stride = t.count > 4 * kSahSample ? t.count / kSahSample : 1;
     // 1. centroid bounds
     float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int i = t.first + tid; i < end; i += kSahThreads) {
+    for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
         const uint32_t p = idx[i];
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
         const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
     }
     __syncthreads();
     // 2. bins
-    for (int i = t.first + tid; i < end; i += kSahThreads) {
+    for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
         const uint32_t p = idx[i];
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
         const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
@@ -463,9 +467,27 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
             best = s_cost[a];
             axis = a;
         }
-    const int nl = axis >= 0 ? s_nl[axis] : t.count / 2;  // no usable split: median by position
+    int nl = axis >= 0 ? s_nl[axis] : t.count / 2;  // no usable split: median by position
     const int split = axis >= 0 ? s_split[axis] : 0;
     const float cmin = axis >= 0 ? s_cmin[axis] : 0.0f, scale = axis >= 0 ? s_scale[axis] : 0.0f;
+    if (stride > 1 && axis >= 0) {  // sampled: count the left side exactly
+        int c = 0;
+        for (int i = t.first + tid; i < end; i += kSahThreads) {
+            const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(idx[i], axis) - cmin) * scale)));
+            c += b < split;
+        }
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        __syncthreads();
+        if (lane == 0) s_warp_l[wid] = c;
+        __syncthreads();
+        nl = 0;
+        for (int w = 0; w < kSahThreads / 32; ++w) nl += s_warp_l[w];
+        __syncthreads();
+        if (nl == 0 || nl == t.count) {  // the sample's split separates nothing
+            axis = -1;
+            nl = t.count / 2;
+        }
+    }
     // 4. stable partition of [first, end) into idx2, then back
     int left_base = 0, right_base = 0;
     for (int base = t.first; base < end; base += kSahThreads) {
