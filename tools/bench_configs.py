@@ -52,15 +52,33 @@ def cpu_ref(sd, excs_spws, freqs, cfg, max_s=20.0):
     rs = oracle.ref_scene(sd)
     cores = os.cpu_count() or 1
     paths, secs, n = 0, 0.0, 0
+    cpu_ref.values = []
     for exc, spw in excs_spws:
         c = M.McConfig(**{**cfg.__dict__, "strata_per_wavelength": spw}).to_c()
         r = oracle.ref_estimate(rs, exc.to_c(), np.asarray(freqs, float), c, cores)
+        cpu_ref.values.append(r["values"])
         paths += r["stats"].rays_launched
         secs += r["stats"].wall_ms / 1e3
         n += 1
         if secs > max_s:
             break
     return paths, secs, n, cores
+
+
+def agreement(gpu, ref):
+    """GPU vs reference complex sweep values [4][nf] of one incidence: the
+    largest relative difference and the RMS dB difference of the co-pol
+    channels over the frequencies (same RNG stream: summation order only)."""
+    gpu, ref = np.asarray(gpu), np.asarray(ref)
+    rel = float(np.max(np.abs(gpu - ref)) / max(np.max(np.abs(ref)), 1e-300))
+    db = []
+    for ch in (M.VV, M.HH):
+        a, b = np.abs(gpu[ch]), np.abs(ref[ch])
+        ok = (a > 0) & (b > 0)
+        if ok.any():
+            db.append(20 * np.log10(a[ok] / b[ok]))
+    rms = float(np.sqrt(np.mean(np.concatenate(db) ** 2))) if db else 0.0
+    return {"max_rel_diff": rel, "rms_db_diff": rms}
 
 
 def c1(cpu):
@@ -77,7 +95,8 @@ def c1(cpu):
            "segments_per_path": st.segments_traced / st.rays_launched}
     if cpu:
         p, t, n, cores = cpu_ref(sd, [(exc, 30.0)], [10e9], cfg)
-        out["cpu_ref"] = {"paths_per_s": p / t, "cores": cores, "sample": "full config"}
+        out["cpu_ref"] = {"paths_per_s": p / t, "cores": cores, "sample": "full config",
+                          "gpu_vs_ref": agreement(vals[0, 0], cpu_ref.values[0])}
         out["speedup_kernel"] = out["gpu_paths_per_s"] / (p / t)
     return out
 
@@ -103,10 +122,12 @@ def c3(cpu, lossy=True):
         obj, mm = M.coated_sphere(subdivisions=5, lossless=True)
         sdl = M.load_scene(obj, mm)
         p, t, n, cores = cpu_ref(sdl, [(rx[180], 275.0)], [3e9], cfg)
+        gl = M.estimate(M.Scene(sdl), rx[180], [3e9], M.McConfig(**{**cfg.__dict__, "strata_per_wavelength": 275.0}))
         out["cpu_ref"] = {"path_receivers_per_s": p / t, "cores": cores,
                           "sample": "1 of 361 receivers (the reference re-traces per receiver), "
                                     "lossless skins (the reference has real eps only)",
-                          "sweep_s_extrapolated": t * 361}
+                          "sweep_s_extrapolated": t * 361,
+                          "gpu_vs_ref": agreement(gl.sweep.values, cpu_ref.values[0])}
         out["speedup_sweep"] = out["cpu_ref"]["sweep_s_extrapolated"] / (st.kernel_ms / 1e3)
     return out
 
@@ -131,6 +152,12 @@ def isar(name, sd, n_az, az_half, freqs, rays, cfg, gpu_angles, cpu, cpu_sd=None
                                  max_s=60.0)
         out["cpu_ref"] = {"paths_per_s": p / t, "cores": cores, "sample": f"{n} azimuth at full rays",
                           "sweep_s_extrapolated": t / n * n_az}
+        if cpu_sd is None:
+            out["cpu_ref"]["gpu_vs_ref"] = agreement(vals[0, 0], cpu_ref.values[0])
+        else:  # the reference has real permittivity only: compare the GPU's lossless twin
+            g2, _ = M.estimate_batch(M.Scene(cpu_sd), [(excs[0], spws[0])], [[excs[0]]], freqs, cfg)
+            out["cpu_ref"]["gpu_vs_ref"] = agreement(g2[0, 0], cpu_ref.values[0])
+            out["cpu_ref"]["gpu_vs_ref"]["note"] = "GPU run of the same scene with the reference's real permittivity"
         out["speedup_sweep"] = out["cpu_ref"]["sweep_s_extrapolated"] / out["gpu_sweep_s"]
     return out
 
