@@ -220,6 +220,36 @@ __device__ inline Basis sp_basis(V3 dir_in, V3 normal, double n1, double n2, boo
     return b;
 }
 
+// interface_transform's transversality guard alone (it does not depend on
+// the branch, so evaluating it once per field raises exactly the reference's
+// faults whichever branches are formed)
+__device__ __forceinline__ void transverse_guard(const CV3& e, const Basis& b, uint32_t& fault) {
+    const V3 dir_in = cross(b.s_hat, b.p_in);
+    const double lim = 1e-9 * (1.0 + norm(e));
+    if (cnorm2(dot(e, dir_in)) > lim * lim) fault |= kFaultTransverse;
+}
+__device__ __forceinline__ void transverse_guard(const V3& e, const Basis& b, uint32_t& fault) {
+    const V3 dir_in = cross(b.s_hat, b.p_in);
+    const double de = dot(e, dir_in);
+    if (de * de > 1e-18 * (1.0 + dot(e, e))) {
+        const double lim = 1e-9 * (1.0 + norm(e));
+        if (de * de > lim * lim) fault |= kFaultTransverse;
+    }
+}
+// the transformed field of one branch, without the guard
+__device__ __forceinline__ CV3 branch_field(const CV3& e, int branch, const Coeffs& co, const Basis& b) {
+    const Cx es = dot(e, b.s_hat);
+    const Cx ep = dot(e, b.p_in);
+    if (branch == 0) return cvreal(b.s_hat) * (es * co.r_s) + cvreal(b.p_out_r) * (ep * co.r_p);
+    return cvreal(b.s_hat) * (es * co.t_s) + cvreal(b.p_out_t) * (ep * co.t_p);
+}
+__device__ __forceinline__ V3 branch_field(const V3& e, int branch, const Coeffs& co, const Basis& b) {
+    const double es = dot(e, b.s_hat);
+    const double ep = dot(e, b.p_in);
+    if (branch == 0) return b.s_hat * (es * co.r_s.re) + b.p_out_r * (ep * co.r_p.re);
+    return b.s_hat * (es * co.t_s.re) + b.p_out_t * (ep * co.t_p.re);
+}
+
 // branch: 0 = reflect, 1 = transmit
 __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs& co,
                                           const Basis& b, uint32_t& fault) {

@@ -1038,13 +1038,23 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         const Coeffs co = pec ? coeffs_pec() : fresnel_any(n1, n2, cos_i, fault);
                         // ray geometry from the real parts (exact for the lossless model)
                         const Basis b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), !pec, fault);
-                        const EF er0 = interface_transform(s.e0, 0, co, b, fault);
-                        const EF er1 = interface_transform(s.e1, 0, co, b, fault);
                         const bool two = !pec && !co.tir;
-                        EF et0 = ef_zero<EF>(), et1 = ef_zero<EF>();
-                        if (two) {
-                            et0 = interface_transform(s.e0, 1, co, b, fault);
-                            et1 = interface_transform(s.e1, 1, co, b, fault);
+                        // The deterministic solver needs every branch's fields
+                        // at once; the Monte Carlo path forms only what the
+                        // contribution and the chosen branch use (fewer live
+                        // registers across the shading): identical values, and
+                        // the transversality guard raises the same faults.
+                        EF er0 = ef_zero<EF>(), er1 = ef_zero<EF>(), et0 = ef_zero<EF>(), et1 = ef_zero<EF>();
+                        if constexpr (kDet) {
+                            er0 = interface_transform(s.e0, 0, co, b, fault);
+                            er1 = interface_transform(s.e1, 0, co, b, fault);
+                            if (two) {
+                                et0 = interface_transform(s.e0, 1, co, b, fault);
+                                et1 = interface_transform(s.e1, 1, co, b, fault);
+                            }
+                        } else {
+                            transverse_guard(s.e0, b, fault);
+                            transverse_guard(s.e1, b, fault);
                         }
                         // scatter case + chi pre-checks (solver_mc.cpp:150-160)
                         const int sc = pec ? 0 : (h.near_is_ambient ? 1 : 2);
@@ -1059,11 +1069,19 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                                 m0 = ef_zero<EF>();
                                 m1 = ef_zero<EF>();
                             } else if (sc == 1) {
+                                if constexpr (!kDet) {
+                                    er0 = branch_field(s.e0, 0, co, b);
+                                    er1 = branch_field(s.e1, 0, co, b);
+                                }
                                 j0 = cross(h.normal, (cross(s.dir, s.e0) + cross(b.dir_r, er0)) * s.medium_n);
                                 j1 = cross(h.normal, (cross(s.dir, s.e1) + cross(b.dir_r, er1)) * s.medium_n);
                                 m0 = cross(s.e0 + er0, h.normal);
                                 m1 = cross(s.e1 + er1, h.normal);
                             } else {
+                                if constexpr (!kDet) {
+                                    et0 = branch_field(s.e0, 1, co, b);
+                                    et1 = branch_field(s.e1, 1, co, b);
+                                }
                                 const V3 n_out = -h.normal;
                                 j0 = cross(n_out, cross(b.dir_t, et0) * h.n_transmit);
                                 j1 = cross(n_out, cross(b.dir_t, et1) * h.n_transmit);
@@ -1167,15 +1185,14 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                                 }
                             }
                             if (logged && pick) P.plog_branch[s.entry] |= 1ull << (s.bounce - 1);
+                            const EF ne0 = branch_field(s.e0, pick, co, b), ne1 = branch_field(s.e1, pick, co, b);
+                            s.e0 = ne0;
+                            s.e1 = ne1;
                             if (pick == 0) {
                                 s.dir = b.dir_r;
-                                s.e0 = er0;
-                                s.e1 = er1;
                                 s.medium_n = n1;
                             } else {
                                 s.dir = b.dir_t;
-                                s.e0 = et0;
-                                s.e1 = et1;
                                 s.medium_n = n2;
                             }
                             s.prob *= pp;
