@@ -1036,8 +1036,12 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         const NT n1 = s.medium_n;
                         const NT n2 = pec ? n1 : h.n_transmit;
                         const Coeffs co = pec ? coeffs_pec() : fresnel_any(n1, n2, cos_i, fault);
-                        // ray geometry from the real parts (exact for the lossless model)
-                        const Basis b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), !pec, fault);
+                        // ray geometry from the real parts (exact for the lossless model);
+                        // a Monte Carlo PEC hit forms it only after its contribution,
+                        // which does not use it (shorter register live ranges)
+                        constexpr bool kLateBasis = L::pec && !kDet;
+                        Basis b;
+                        if constexpr (!kLateBasis) b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), !pec, fault);
                         const bool two = !pec && !co.tir;
                         // The deterministic solver needs every branch's fields
                         // at once; the Monte Carlo path forms only what the
@@ -1052,7 +1056,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                                 et0 = interface_transform(s.e0, 1, co, b, fault);
                                 et1 = interface_transform(s.e1, 1, co, b, fault);
                             }
-                        } else {
+                        } else if constexpr (!kLateBasis) {
                             transverse_guard(s.e0, b, fault);
                             transverse_guard(s.e1, b, fault);
                         }
@@ -1123,6 +1127,11 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                                          : ((static_cast<uint64_t>(s.cell) * P.spp + s.sample) << 8) |
                                                static_cast<uint64_t>(s.bounce & 0xff);
                             }
+                        }
+                        if constexpr (kLateBasis) {
+                            b = sp_basis(s.dir, h.normal, re_of(n1), re_of(n2), false, fault);
+                            transverse_guard(s.e0, b, fault);
+                            transverse_guard(s.e1, b, fault);
                         }
                         if (s.bounce >= P.max_bounce) {  // cap (solver_mc.cpp:176-179)
                             ++n_cap;
