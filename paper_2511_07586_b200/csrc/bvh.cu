@@ -560,28 +560,11 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
         }                                     \
     } while (0)
 
-// Build temporaries come from the stream-ordered allocator (no device-wide
-// synchronisation per allocation); the pool keeps up to 1 GB between builds.
-static void keep_pool(int device) {
-    static thread_local int done_for = -1;
-    if (done_for == device) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = uint64_t{1} << 30;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        done_for = device;
-    }
-}
-
 cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t n_tri,
                       const double scene_lo[3], const double scene_hi[3], const double center[3],
                       double box_pad, cudaStream_t stream, BvhBuildOut* out) {
     cudaError_t err = cudaSuccess;
     const int n = static_cast<int>(n_tri);
-    {
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) keep_pool(dev);
-    }
     uint64_t *keys = nullptr, *keys_s = nullptr;
     uint32_t *ids = nullptr, *ids_s = nullptr;
     float4 *blo = nullptr, *bhi = nullptr, *blo_s = nullptr, *bhi_s = nullptr;
@@ -611,26 +594,26 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     BVH_CHECK(cudaEventCreate(&e0));
     BVH_CHECK(cudaEventCreate(&e1));
     BVH_CHECK(cudaEventRecord(e0, stream));
-    BVH_CHECK(cudaMallocAsync(&keys, sizeof(uint64_t) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&keys_s, sizeof(uint64_t) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&ids, sizeof(uint32_t) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&ids_s, sizeof(uint32_t) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&blo, sizeof(float4) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&bhi, sizeof(float4) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&blo_s, sizeof(float4) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&bhi_s, sizeof(float4) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&ilo, sizeof(float4) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&ihi, sizeof(float4) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&child, sizeof(int2) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&range, sizeof(int2) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&par_i, sizeof(int) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&par_l, sizeof(int) * n, stream));
-    BVH_CHECK(cudaMallocAsync(&flags, sizeof(int) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&dmax, sizeof(unsigned int), stream));
-    BVH_CHECK(cudaMallocAsync(&is4, sizeof(unsigned int) * inner, stream));
-    BVH_CHECK(cudaMallocAsync(&idx4, sizeof(unsigned int) * inner, stream));
-    BVH_CHECK(cudaMalloc(&out->nodes, sizeof(float4) * 8 * inner));
-    BVH_CHECK(cudaMalloc(&out->tri64, sizeof(double2) * 5 * n));
+    BVH_CHECK(dev_malloc(&keys, sizeof(uint64_t) * n));
+    BVH_CHECK(dev_malloc(&keys_s, sizeof(uint64_t) * n));
+    BVH_CHECK(dev_malloc(&ids, sizeof(uint32_t) * n));
+    BVH_CHECK(dev_malloc(&ids_s, sizeof(uint32_t) * n));
+    BVH_CHECK(dev_malloc(&blo, sizeof(float4) * n));
+    BVH_CHECK(dev_malloc(&bhi, sizeof(float4) * n));
+    BVH_CHECK(dev_malloc(&blo_s, sizeof(float4) * n));
+    BVH_CHECK(dev_malloc(&bhi_s, sizeof(float4) * n));
+    BVH_CHECK(dev_malloc(&ilo, sizeof(float4) * inner));
+    BVH_CHECK(dev_malloc(&ihi, sizeof(float4) * inner));
+    BVH_CHECK(dev_malloc(&child, sizeof(int2) * inner));
+    BVH_CHECK(dev_malloc(&range, sizeof(int2) * inner));
+    BVH_CHECK(dev_malloc(&par_i, sizeof(int) * inner));
+    BVH_CHECK(dev_malloc(&par_l, sizeof(int) * n));
+    BVH_CHECK(dev_malloc(&flags, sizeof(int) * inner));
+    BVH_CHECK(dev_malloc(&dmax, sizeof(unsigned int)));
+    BVH_CHECK(dev_malloc(&is4, sizeof(unsigned int) * inner));
+    BVH_CHECK(dev_malloc(&idx4, sizeof(unsigned int) * inner));
+    BVH_CHECK(dev_malloc(&out->nodes, sizeof(float4) * 8 * inner));
+    BVH_CHECK(dev_malloc(&out->tri64, sizeof(double2) * 5 * n));
     BVH_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * inner, stream));
     BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
     BVH_CHECK(cudaMemsetAsync(par_i, 0xff, sizeof(int) * inner, stream));  // root parent = -1
@@ -642,7 +625,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     BVH_CHECK(cudaGetLastError());
     BVH_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
                                               stream));
-    BVH_CHECK(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    BVH_CHECK(dev_malloc(&tmp, tmp_bytes));
     BVH_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
                                               stream));
     order = ids_s;
@@ -652,10 +635,10 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         const char* bvh_env = std::getenv("MCSBR_BVH");
         bool sah = !(bvh_env && std::strcmp(bvh_env, "lbvh") == 0);
         if (sah) {
-            BVH_CHECK(cudaMallocAsync(&sidx, sizeof(uint32_t) * n, stream));
-            BVH_CHECK(cudaMallocAsync(&tasks, sizeof(SahTask) * (n / 2 + 1), stream));
-            BVH_CHECK(cudaMallocAsync(&tasks2, sizeof(SahTask) * (n / 2 + 1), stream));
-            BVH_CHECK(cudaMallocAsync(&node_counter, sizeof(int) * 2, stream));
+            BVH_CHECK(dev_malloc(&sidx, sizeof(uint32_t) * n));
+            BVH_CHECK(dev_malloc(&tasks, sizeof(SahTask) * (n / 2 + 1)));
+            BVH_CHECK(dev_malloc(&tasks2, sizeof(SahTask) * (n / 2 + 1)));
+            BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * 2));
             next_count = node_counter + 1;
             BVH_CHECK(cudaMemcpyAsync(sidx, ids_s, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
             const int one = 1;
@@ -704,7 +687,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         parity_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, range, par_i, is4);
         BVH_CHECK(cudaGetLastError());
         BVH_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, is4, idx4, n - 1, stream));
-        BVH_CHECK(cudaMallocAsync(&scan_tmp, scan_bytes, stream));
+        BVH_CHECK(dev_malloc(&scan_tmp, scan_bytes));
         BVH_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, is4, idx4, n - 1, stream));
         emit4_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, is4, idx4, ilo, ihi, blo_s,
                                                             bhi_s, out->nodes);
@@ -734,35 +717,35 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         out->build_ms = ms;
     }
 done:
-    if (keys) cudaFreeAsync(keys, stream);
-    if (keys_s) cudaFreeAsync(keys_s, stream);
-    if (ids) cudaFreeAsync(ids, stream);
-    if (ids_s) cudaFreeAsync(ids_s, stream);
-    if (blo) cudaFreeAsync(blo, stream);
-    if (bhi) cudaFreeAsync(bhi, stream);
-    if (blo_s) cudaFreeAsync(blo_s, stream);
-    if (bhi_s) cudaFreeAsync(bhi_s, stream);
-    if (ilo) cudaFreeAsync(ilo, stream);
-    if (ihi) cudaFreeAsync(ihi, stream);
-    if (child) cudaFreeAsync(child, stream);
-    if (range) cudaFreeAsync(range, stream);
-    if (par_i) cudaFreeAsync(par_i, stream);
-    if (par_l) cudaFreeAsync(par_l, stream);
-    if (flags) cudaFreeAsync(flags, stream);
-    if (dmax) cudaFreeAsync(dmax, stream);
-    if (is4) cudaFreeAsync(is4, stream);
-    if (idx4) cudaFreeAsync(idx4, stream);
-    if (tmp) cudaFreeAsync(tmp, stream);
-    if (scan_tmp) cudaFreeAsync(scan_tmp, stream);
-    if (sidx) cudaFreeAsync(sidx, stream);
-    if (tasks) cudaFreeAsync(tasks, stream);
-    if (tasks2) cudaFreeAsync(tasks2, stream);
-    if (node_counter) cudaFreeAsync(node_counter, stream);
+    dev_free(keys);
+    dev_free(keys_s);
+    dev_free(ids);
+    dev_free(ids_s);
+    dev_free(blo);
+    dev_free(bhi);
+    dev_free(blo_s);
+    dev_free(bhi_s);
+    dev_free(ilo);
+    dev_free(ihi);
+    dev_free(child);
+    dev_free(range);
+    dev_free(par_i);
+    dev_free(par_l);
+    dev_free(flags);
+    dev_free(dmax);
+    dev_free(is4);
+    dev_free(idx4);
+    dev_free(tmp);
+    dev_free(scan_tmp);
+    dev_free(sidx);
+    dev_free(tasks);
+    dev_free(tasks2);
+    dev_free(node_counter);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (err != cudaSuccess) {
-        cudaFree(out->nodes);
-        cudaFree(out->tri64);
+        dev_free(out->nodes);
+        dev_free(out->tri64);
         out->nodes = nullptr;
         out->tri64 = nullptr;
     }

@@ -19,11 +19,100 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 
 #include "internal.h"
 #include "mcsbr_gpu.h"
 
 using namespace mcsbr_int;
+
+// ---------------------------------------------------------------------------
+// caching device allocator (internal.h)
+namespace mcsbr_int {
+namespace {
+struct AllocCache {
+    std::mutex m;
+    std::unordered_map<void*, std::pair<int, size_t>> size_of;  // live and cached blocks
+    std::multimap<size_t, void*> free_blocks[64];               // per device: size -> block
+    size_t cached = 0;
+};
+AllocCache& alloc_cache() {
+    static AllocCache* c = new AllocCache();  // never destroyed (used during process exit)
+    return *c;
+}
+constexpr size_t kCacheLimit = size_t{4} << 30;
+size_t alloc_class(size_t n) {
+    n = n ? n : 1;
+    const size_t g = n >= (size_t{1} << 20) ? (size_t{1} << 16) : 256;  // 64 KB / 256 B granules
+    return (n + g - 1) / g * g;
+}
+}  // namespace
+
+cudaError_t dev_malloc(void** p, size_t bytes) {
+    *p = nullptr;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const size_t n = alloc_class(bytes);
+    AllocCache& c = alloc_cache();
+    {
+        std::lock_guard<std::mutex> g(c.m);
+        if (dev >= 0 && dev < 64) {
+            auto& fb = c.free_blocks[dev];
+            auto it = fb.lower_bound(n);
+            if (it != fb.end() && it->first <= 2 * n) {  // reuse a block at most twice the size
+                *p = it->second;
+                c.cached -= it->first;
+                fb.erase(it);
+                return cudaSuccess;
+            }
+        }
+    }
+    e = cudaMalloc(p, n);
+    if (e != cudaSuccess) {
+        // out of memory: hand the cache back to the driver and retry once
+        cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> g(c.m);
+            for (auto& kv : c.free_blocks[dev]) {
+                cudaFree(kv.second);
+                c.size_of.erase(kv.second);
+            }
+            c.cached = 0;
+            c.free_blocks[dev].clear();
+        }
+        e = cudaMalloc(p, n);
+        if (e != cudaSuccess) return e;
+    }
+    std::lock_guard<std::mutex> g(c.m);
+    c.size_of[*p] = {dev, n};
+    return cudaSuccess;
+}
+
+void dev_free(void* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();  // the block may be read by work still in flight
+    AllocCache& c = alloc_cache();
+    std::lock_guard<std::mutex> g(c.m);
+    auto it = c.size_of.find(p);
+    if (it == c.size_of.end()) {  // not ours
+        cudaFree(p);
+        return;
+    }
+    const int dev = it->second.first;
+    const size_t n = it->second.second;
+    if (dev < 0 || dev >= 64 || c.cached + n > kCacheLimit) {
+        c.size_of.erase(it);
+        cudaFree(p);
+        return;
+    }
+    c.free_blocks[dev].emplace(n, p);
+    c.cached += n;
+}
+
+}  // namespace mcsbr_int
 
 namespace {
 
@@ -74,15 +163,15 @@ struct DevBuf {
     size_t n = 0;
     cudaError_t reserve(size_t want) {
         if (want <= n) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         n = 0;
-        cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(want, 1));
+        cudaError_t e = dev_malloc(&p, sizeof(T) * std::max<size_t>(want, 1));
         if (e == cudaSuccess) n = want;
         return e;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         n = 0;
     }
@@ -418,10 +507,10 @@ void fill_config(TraceParams& p, const mcsbr_mc_config* cfg) {
 int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* cfg, int occlusion,
             double* d_sums, unsigned long long* d_counters, cudaStream_t stream, TraceParams* extra,
             float* kernel_ms) {
-    CK(s->inc.reserve(job.inc.size()), "cudaMalloc(incidences)");
-    CK(s->rx.reserve(job.rx.size()), "cudaMalloc(receivers)");
-    CK(s->k0.reserve(nf), "cudaMalloc(k0)");
-    CK(s->tile.reserve(3), "cudaMalloc(tile counter)");  // entry cursor, record count, peak count
+    CK(s->inc.reserve(job.inc.size()), "dev_malloc(incidences)");
+    CK(s->rx.reserve(job.rx.size()), "dev_malloc(receivers)");
+    CK(s->k0.reserve(nf), "dev_malloc(k0)");
+    CK(s->tile.reserve(3), "dev_malloc(tile counter)");  // entry cursor, record count, peak count
     // deferred accumulation (F > 1): one 96-byte record per visible
     // contribution; sized for one per launched path of the largest group
     // (measured c4/c5: ~0.1 per path), overflow falls back to direct atomics
@@ -431,7 +520,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1) + 4096;
         rec_cap = std::min<uint64_t>(rec_cap, kRecCapMax);
         rec_cap = env_u32("MCSBR_REC_CAP", static_cast<uint32_t>(rec_cap));
-        CK(s->recs.reserve(rec_cap * 12), "cudaMalloc(contribution records)");
+        CK(s->recs.reserve(rec_cap * 12), "dev_malloc(contribution records)");
     }
     CK(cudaMemcpyAsync(s->inc.p, job.inc.data(), sizeof(IncDev) * job.inc.size(), cudaMemcpyHostToDevice,
                        stream), "upload incidences");
@@ -690,10 +779,10 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     };
     if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(e, "cudaStreamCreate");
-    if ((e = cudaMalloc(&s->d_vtx, sizeof(double) * 3 * nv)) != cudaSuccess) return fail(e, "cudaMalloc(vertices)");
-    if ((e = cudaMalloc(&s->d_tri, sizeof(uint4) * nt)) != cudaSuccess) return fail(e, "cudaMalloc(triangles)");
-    if ((e = cudaMalloc(&s->d_info, sizeof(double2) * 2 * nt)) != cudaSuccess) return fail(e, "cudaMalloc(tri info)");
-    if ((e = cudaMalloc(&s->d_mat, sizeof(double2) * nm)) != cudaSuccess) return fail(e, "cudaMalloc(materials)");
+    if ((e = dev_malloc(&s->d_vtx, sizeof(double) * 3 * nv)) != cudaSuccess) return fail(e, "dev_malloc(vertices)");
+    if ((e = dev_malloc(&s->d_tri, sizeof(uint4) * nt)) != cudaSuccess) return fail(e, "dev_malloc(triangles)");
+    if ((e = dev_malloc(&s->d_info, sizeof(double2) * 2 * nt)) != cudaSuccess) return fail(e, "dev_malloc(tri info)");
+    if ((e = dev_malloc(&s->d_mat, sizeof(double2) * nm)) != cudaSuccess) return fail(e, "dev_malloc(materials)");
     if ((e = cudaMemcpyAsync(s->d_vtx, xyz, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice, s->stream)) !=
         cudaSuccess)
         return fail(e, "upload vertices");
@@ -707,7 +796,7 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
         cudaSuccess)
         return fail(e, "upload materials");
     if (s->lossy) {
-        if ((e = cudaMalloc(&s->d_nim, sizeof(double) * nm)) != cudaSuccess) return fail(e, "cudaMalloc(Im n)");
+        if ((e = dev_malloc(&s->d_nim, sizeof(double) * nm)) != cudaSuccess) return fail(e, "dev_malloc(Im n)");
         if ((e = cudaMemcpyAsync(s->d_nim, nim.data(), sizeof(double) * nm, cudaMemcpyHostToDevice, s->stream)) !=
             cudaSuccess)
             return fail(e, "upload Im n");
@@ -732,13 +821,13 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     if (!s) return;
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
-    cudaFree(s->d_vtx);
-    cudaFree(s->d_tri);
-    cudaFree(s->d_info);
-    cudaFree(s->d_mat);
-    cudaFree(s->d_nim);
-    cudaFree(s->bvh.nodes);
-    cudaFree(s->bvh.tri64);
+    dev_free(s->d_vtx);
+    dev_free(s->d_tri);
+    dev_free(s->d_info);
+    dev_free(s->d_mat);
+    dev_free(s->d_nim);
+    dev_free(s->bvh.nodes);
+    dev_free(s->bvh.tri64);
     s->inc.release();
     s->rx.release();
     s->k0.release();
@@ -788,10 +877,10 @@ int mcsbr_gpu_intersect(const mcsbr_scene* s, const double* o, const double* d, 
     uint32_t* d_id = nullptr;
     cudaError_t e = cudaSuccess;
     const size_t v3 = sizeof(double) * 3 * n;
-    if ((e = cudaMalloc(&d_o, v3)) == cudaSuccess && (e = cudaMalloc(&d_d, v3)) == cudaSuccess &&
-        (e = cudaMalloc(&d_t, sizeof(double) * n)) == cudaSuccess &&
-        (e = cudaMalloc(&d_to, sizeof(double) * n)) == cudaSuccess &&
-        (e = cudaMalloc(&d_id, sizeof(uint32_t) * n)) == cudaSuccess &&
+    if ((e = dev_malloc(&d_o, v3)) == cudaSuccess && (e = dev_malloc(&d_d, v3)) == cudaSuccess &&
+        (e = dev_malloc(&d_t, sizeof(double) * n)) == cudaSuccess &&
+        (e = dev_malloc(&d_to, sizeof(double) * n)) == cudaSuccess &&
+        (e = dev_malloc(&d_id, sizeof(uint32_t) * n)) == cudaSuccess &&
         (e = cudaMemcpyAsync(d_o, o, v3, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
         (e = cudaMemcpyAsync(d_d, d, v3, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
         (e = cudaMemcpyAsync(d_t, tmin, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream)) == cudaSuccess &&
@@ -802,11 +891,11 @@ int mcsbr_gpu_intersect(const mcsbr_scene* s, const double* o, const double* d, 
         ++g_launches;
         e = cudaStreamSynchronize(s->stream);
     }
-    cudaFree(d_o);
-    cudaFree(d_d);
-    cudaFree(d_t);
-    cudaFree(d_to);
-    cudaFree(d_id);
+    dev_free(d_o);
+    dev_free(d_d);
+    dev_free(d_t);
+    dev_free(d_to);
+    dev_free(d_id);
     if (e != cudaSuccess) return cuda_err(e, "intersect");
     return MCSBR_OK;
 }
@@ -844,8 +933,8 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     if (rc) return rc;
     if (det && (n_inc != 1 || n_rx != 1)) return set_err(MCSBR_EINVAL, "solve: one excitation per call");
     const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
-    CK(s->sums.reserve(nsum), "cudaMalloc(sums)");
-    CK(s->counters.reserve(kCntWords), "cudaMalloc(counters)");
+    CK(s->sums.reserve(nsum), "dev_malloc(sums)");
+    CK(s->counters.reserve(kCntWords), "dev_malloc(counters)");
     CK(cudaMemsetAsync(s->sums.p, 0, sizeof(double) * nsum, s->stream), "memset sums");
     CK(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kCntWords, s->stream), "memset counters");
     TraceParams extra{};
@@ -855,9 +944,9 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     if (contribs) {
         if (n_inc != 1 || n_rx != 1) return set_err(MCSBR_EINVAL, "contributions_out needs one incidence");
         const size_t scratch_n = static_cast<size_t>(s->sms) * 32 * 128;  // >= resident threads
-        CK(cudaMalloc(&d_out, sizeof(mcsbr_contribution) * std::max<uint64_t>(capacity, 1)), "cudaMalloc(contribs)");
-        CK(cudaMalloc(&d_scratch, sizeof(mcsbr_contribution) * scratch_n), "cudaMalloc(scratch)");
-        CK(cudaMalloc(&d_cnt, sizeof(unsigned long long)), "cudaMalloc(count)");
+        CK(dev_malloc(&d_out, sizeof(mcsbr_contribution) * std::max<uint64_t>(capacity, 1)), "dev_malloc(contribs)");
+        CK(dev_malloc(&d_scratch, sizeof(mcsbr_contribution) * scratch_n), "dev_malloc(scratch)");
+        CK(dev_malloc(&d_cnt, sizeof(unsigned long long)), "dev_malloc(count)");
         CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s->stream), "memset count");
         extra.contrib_out = d_out;
         extra.contrib_cap = capacity;
@@ -869,9 +958,9 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     unsigned long long* d_pbr = nullptr;
     if (plog && plog->n) {
         const size_t nt = plog->n * plog->stride;
-        CK(cudaMalloc(&d_ptri, sizeof(uint32_t) * nt), "cudaMalloc(plog)");
-        CK(cudaMalloc(&d_pterm, plog->n), "cudaMalloc(plog)");
-        CK(cudaMalloc(&d_pbr, sizeof(unsigned long long) * plog->n), "cudaMalloc(plog)");
+        CK(dev_malloc(&d_ptri, sizeof(uint32_t) * nt), "dev_malloc(plog)");
+        CK(dev_malloc(&d_pterm, plog->n), "dev_malloc(plog)");
+        CK(dev_malloc(&d_pbr, sizeof(unsigned long long) * plog->n), "dev_malloc(plog)");
         CK(cudaMemsetAsync(d_ptri, 0xff, sizeof(uint32_t) * nt, s->stream), "memset plog");
         CK(cudaMemsetAsync(d_pterm, 0, plog->n, s->stream), "memset plog");
         CK(cudaMemsetAsync(d_pbr, 0, sizeof(unsigned long long) * plog->n, s->stream), "memset plog");
@@ -890,17 +979,17 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         const uint32_t depth = static_cast<uint32_t>(det->max_bounce);
         stack_bytes = sizeof(double) * kDetFields * depth * threads;
         det_nblocks = (job.total_entries + det->block_size - 1) / static_cast<uint64_t>(det->block_size);
-        cudaError_t e0 = cudaMalloc(&d_stack, stack_bytes);
-        if (e0 == cudaSuccess) e0 = cudaMalloc(&d_blocks, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1));
+        cudaError_t e0 = dev_malloc(&d_stack, stack_bytes);
+        if (e0 == cudaSuccess) e0 = dev_malloc(&d_blocks, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1));
         if (e0 == cudaSuccess)
             e0 = cudaMemsetAsync(d_blocks, 0, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1), s->stream);
         if (e0 != cudaSuccess) {
-            cudaFree(d_stack);
-            cudaFree(d_blocks);
-            cudaFree(d_out);
-            cudaFree(d_scratch);
-            cudaFree(d_cnt);
-            return cuda_err(e0, "cudaMalloc(branch stacks)");
+            dev_free(d_stack);
+            dev_free(d_blocks);
+            dev_free(d_out);
+            dev_free(d_scratch);
+            dev_free(d_cnt);
+            return cuda_err(e0, "dev_malloc(branch stacks)");
         }
         extra.det = 1;
         extra.det_cutoff = det->amplitude_cutoff;
@@ -918,8 +1007,8 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
                                           cudaMemcpyDeviceToHost);
         if (e2 != cudaSuccess) rc = cuda_err(e2, "branch accounting readback");
     }
-    cudaFree(d_stack);
-    cudaFree(d_blocks);
+    dev_free(d_stack);
+    dev_free(d_blocks);
     if (rc == MCSBR_OK && plog && plog->n) {
         cudaError_t e2 = cudaMemcpy(plog->tri, d_ptri, sizeof(uint32_t) * plog->n * plog->stride,
                                     cudaMemcpyDeviceToHost);
@@ -928,13 +1017,13 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
             e2 = cudaMemcpy(plog->branch, d_pbr, sizeof(uint64_t) * plog->n, cudaMemcpyDeviceToHost);
         if (e2 != cudaSuccess) rc = cuda_err(e2, "path log readback");
     }
-    cudaFree(d_ptri);
-    cudaFree(d_pterm);
-    cudaFree(d_pbr);
+    dev_free(d_ptri);
+    dev_free(d_pterm);
+    dev_free(d_pbr);
     if (rc) {
-        cudaFree(d_out);
-        cudaFree(d_scratch);
-        cudaFree(d_cnt);
+        dev_free(d_out);
+        dev_free(d_scratch);
+        dev_free(d_cnt);
         return rc;
     }
     std::vector<double> raw(nsum);
@@ -954,9 +1043,9 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         });
         if (n_contribs) *n_contribs = ncol;
     }
-    cudaFree(d_out);
-    cudaFree(d_scratch);
-    cudaFree(d_cnt);
+    dev_free(d_out);
+    dev_free(d_scratch);
+    dev_free(d_cnt);
     if (e != cudaSuccess) return cuda_err(e, "estimate readback");
     rc = fault_check(cnt);
     if (rc) return rc;

@@ -148,6 +148,18 @@ constexpr int kDetFields = 24;  // origin 3, dir 3, e0 6, e1 6, phi 2, medium 2,
 // kernel's launch bound); launch_trace caps a det grid at the stack capacity
 #define MCSBR_DET_THREADS_PER_SM 512
 
+// capi.cu: caching device allocator.  Scene creation / destruction and the
+// BVH build allocate and free dozens of buffers; cudaMalloc / cudaFree cost
+// driver round trips (and, on a busy host, occasionally tens of ms), so
+// freed blocks are kept per device (bounded) and handed out again.  A free
+// synchronises the device first, so a cached block is never still in use.
+cudaError_t dev_malloc(void** p, size_t bytes);
+void dev_free(void* p);
+template <typename T>
+inline cudaError_t dev_malloc(T** p, size_t bytes) {
+    return dev_malloc(reinterpret_cast<void**>(p), bytes);
+}
+
 // bvh.cu
 struct BvhBuildOut {
     float4* nodes;
