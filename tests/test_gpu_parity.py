@@ -359,3 +359,28 @@ def test_both_bvh_builders_are_exact(builder, monkeypatch):
     M.estimate(s, exc, [10e9], cfg, contributions_out=got)
     ref = oracle_estimate(sd, exc, [10e9], cfg)
     assert contribs_identical(sort_contribs(ref["contributions"]), got[0])
+
+
+def test_scene_churn_reuses_device_memory_safely():
+    """Scenes of different sizes created and destroyed in turn (the caching
+    allocator hands freed blocks to the next scene): every estimate is
+    identical to a fresh process-level reference run of the same scene."""
+    cfg = M.McConfig(strata_per_wavelength=4, samples_per_stratum=1, max_bounce=4, seed=2)
+    exc = M.monostatic_excitation(90.0, 30.0)
+    scenes = []
+    for n in (8, 16, 4, 24):
+        obj, mm = M.dihedral_grid(0.5, n)
+        scenes.append(M.load_scene(obj, mm))
+    first = {}
+    for rep in range(3):
+        for i, sd in enumerate(scenes):
+            s = M.Scene(sd)
+            r = M.estimate(s, exc, [10e9], cfg)
+            s.close()
+            if rep == 0:
+                first[i] = r.sweep.values
+                ref = oracle_estimate(sd, exc, [10e9], cfg, contributions=False)
+                assert np.max(np.abs(ref["values"] - r.sweep.values)) <= 1e-9 * np.max(np.abs(ref["values"]))
+            else:
+                assert np.array_equal(first[i], r.sweep.values) or \
+                    np.max(np.abs(first[i] - r.sweep.values)) <= 1e-12 * np.max(np.abs(first[i]))
