@@ -274,32 +274,38 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
                 const float tf = fmin3(a_f, b_f, fminf(c_f, tmax));
                 k[j] = ((tn <= tf ? __float_as_uint(tn) : 0x7f800000u) & ~3u) | static_cast<uint32_t>(j);
             }
-            // sorting network (0,1)(2,3)(0,2)(1,3)(1,2) on the keys: integer min / max
+            constexpr uint32_t kMiss = 0x7f800000u;
+            const int rc[4] = {__float_as_int(rf.x), __float_as_int(rf.y), __float_as_int(rf.z),
+                               __float_as_int(rf.w)};
+            auto child = [&](uint32_t key) {
+                const uint32_t j = key & 3u;
+                return (j & 2u) ? ((j & 1u) ? rc[3] : rc[2]) : ((j & 1u) ? rc[1] : rc[0]);
+            };
+            const unsigned hm = (k[0] < kMiss ? 1u : 0u) | (k[1] < kMiss ? 2u : 0u) | (k[2] < kMiss ? 4u : 0u) |
+                                (k[3] < kMiss ? 8u : 0u);
+            if (hm && (hm & (hm - 1u)) == 0u) {  // exactly one child entered: no sort, no push
+                ref = child(static_cast<uint32_t>(__ffs(hm) - 1));
+                continue;
+            }
+            if (hm) {
+                // sorting network (0,1)(2,3)(0,2)(1,3)(1,2) on the keys: integer min / max
 #define MCSBR_KSWAP(a, b)               \
     {                                   \
         const uint32_t lo_ = min(a, b); \
         b = max(a, b);                  \
         a = lo_;                        \
     }
-            MCSBR_KSWAP(k[0], k[1])
-            MCSBR_KSWAP(k[2], k[3])
-            MCSBR_KSWAP(k[0], k[2])
-            MCSBR_KSWAP(k[1], k[3])
-            MCSBR_KSWAP(k[1], k[2])
+                MCSBR_KSWAP(k[0], k[1])
+                MCSBR_KSWAP(k[2], k[3])
+                MCSBR_KSWAP(k[0], k[2])
+                MCSBR_KSWAP(k[1], k[3])
+                MCSBR_KSWAP(k[1], k[2])
 #undef MCSBR_KSWAP
-            constexpr uint32_t kMiss = 0x7f800000u;
-            if (k[0] < kMiss) {
-                const int rc[4] = {__float_as_int(rf.x), __float_as_int(rf.y), __float_as_int(rf.z),
-                                   __float_as_int(rf.w)};
-                auto child = [&](uint32_t key) {
-                    const uint32_t j = key & 3u;
-                    return (j & 2u) ? ((j & 1u) ? rc[3] : rc[2]) : ((j & 1u) ? rc[1] : rc[0]);
-                };
                 // visit the nearest now, push the others far-to-near (the
                 // host bounds the tree depth so the stack cannot overflow)
                 if (k[3] < kMiss) stack[sp++] = child(k[3]);
                 if (k[2] < kMiss) stack[sp++] = child(k[2]);
-                if (k[1] < kMiss) stack[sp++] = child(k[1]);
+                stack[sp++] = child(k[1]);  // at least two entered
                 ref = child(k[0]);
                 continue;
             }
