@@ -23,6 +23,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -332,11 +333,11 @@ __device__ __forceinline__ float half_area(float lx, float ly, float lz, float h
     return (dx < 0.f || dy < 0.f || dz < 0.f) ? 0.f : dx * dy + dy * dz + dz * dx;
 }
 
-__global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
-    const SahTask* __restrict__ tasks, const float4* __restrict__ blo, const float4* __restrict__ bhi,
+__device__ __forceinline__ void sah_split(
+    const SahTask t, const float4* __restrict__ blo, const float4* __restrict__ bhi,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
-    int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ next,
-    int* __restrict__ next_count) {
+    int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
+    int* __restrict__ ready) {
     __shared__ int s_cnt[3][kSahBins];
     __shared__ int s_box[3][kSahBins][6];
     __shared__ float s_red[2][3][kSahThreads / 32];
@@ -344,7 +345,6 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
     __shared__ float s_cost[3];
     __shared__ int s_split[3], s_nl[3];
     __shared__ int s_warp_l[kSahThreads / 32];
-    const SahTask t = tasks[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int end = t.first + t.count;
     auto centroid = [&](uint32_t p, int a) {
@@ -537,15 +537,48 @@ __global__ void __launch_bounds__(kSahThreads) sah_split_kernel(
             if (sizes[k] == 1) {
                 enc[k] = ~starts[k];
                 par_l[starts[k]] = t.node;
-            } else {
+            } else {  // publish the child's task under its inner-node index
                 const int id = atomicAdd(node_counter, 1);
                 enc[k] = id;
                 par_i[id] = t.node;
-                next[atomicAdd(next_count, 1)] = SahTask{starts[k], sizes[k], id};
+                tasks[id] = SahTask{starts[k], sizes[k], id};
+                __threadfence();
+                atomicExch(ready + id, 1);
             }
         }
         child[t.node] = make_int2(enc[0], enc[1]);
         range[t.node] = make_int2(t.first, end - 1);
+    }
+}
+
+// Persistent build: every inner node is one task whose index is its node
+// id; co-resident blocks take ids 0, 1, 2, ... in order and wait until the
+// parent has published the task (a task's parent always has a smaller id and
+// is already being processed, so the waits always end).  One launch instead
+// of one launch plus a host round trip per tree level.
+__global__ void __launch_bounds__(kSahThreads) sah_build_kernel(
+    int n_inner, int* __restrict__ head, const float4* __restrict__ blo, const float4* __restrict__ bhi,
+    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
+    int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
+    int* __restrict__ ready) {
+    __shared__ int s_id;
+    __shared__ SahTask s_task;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int i = atomicAdd(head, 1);
+            if (i < n_inner) {
+                while (atomicAdd(ready + i, 0) == 0) __nanosleep(64);
+                __threadfence();
+                s_task.first = __ldcg(&tasks[i].first);
+                s_task.count = __ldcg(&tasks[i].count);
+                s_task.node = __ldcg(&tasks[i].node);
+            }
+            s_id = i;
+        }
+        __syncthreads();
+        if (s_id >= n_inner) break;
+        sah_split(s_task, blo, bhi, idx, idx2, child, range, par_i, par_l, node_counter, tasks, ready);
+        __syncthreads();
     }
 }
 
@@ -574,8 +607,8 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     unsigned int* dmax = nullptr;
     unsigned int *is4 = nullptr, *idx4 = nullptr;
     uint32_t* sidx = nullptr;         // SAH: the final triangle order
-    SahTask *tasks = nullptr, *tasks2 = nullptr;
-    int *node_counter = nullptr, *next_count = nullptr;
+    SahTask* tasks = nullptr;
+    int* node_counter = nullptr;
     const uint32_t* order = nullptr;  // final leaf order (SAH or Morton)
     void* tmp = nullptr;
     void* scan_tmp = nullptr;
@@ -636,27 +669,24 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         bool sah = !(bvh_env && std::strcmp(bvh_env, "lbvh") == 0);
         if (sah) {
             BVH_CHECK(dev_malloc(&sidx, sizeof(uint32_t) * n));
-            BVH_CHECK(dev_malloc(&tasks, sizeof(SahTask) * (n / 2 + 1)));
-            BVH_CHECK(dev_malloc(&tasks2, sizeof(SahTask) * (n / 2 + 1)));
-            BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * 2));
-            next_count = node_counter + 1;
+            BVH_CHECK(dev_malloc(&tasks, sizeof(SahTask) * inner));
+            BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * (inner + 2)));  // counter, head, ready[inner]
             BVH_CHECK(cudaMemcpyAsync(sidx, ids_s, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
-            const int one = 1;
-            const SahTask root{0, n, 0};
-            BVH_CHECK(cudaMemcpyAsync(node_counter, &one, sizeof(int), cudaMemcpyHostToDevice, stream));
-            BVH_CHECK(cudaMemcpyAsync(tasks, &root, sizeof(SahTask), cudaMemcpyHostToDevice, stream));
-            int h_tasks = 1;
-            while (h_tasks > 0) {
-                BVH_CHECK(cudaMemsetAsync(next_count, 0, sizeof(int), stream));
-                sah_split_kernel<<<h_tasks, kSahThreads, 0, stream>>>(tasks, blo, bhi, sidx, ids, child, range,
-                                                                      par_i, par_l, node_counter, tasks2,
-                                                                      next_count);
+            BVH_CHECK(cudaMemsetAsync(node_counter, 0, sizeof(int) * (inner + 2), stream));
+            {
+                const int init[3] = {1, 0, 1};  // next node id, head, ready[0]
+                const SahTask root{0, n, 0};
+                BVH_CHECK(cudaMemcpyAsync(node_counter, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+                BVH_CHECK(cudaMemcpyAsync(tasks, &root, sizeof(SahTask), cudaMemcpyHostToDevice, stream));
+                int dev = 0, sms = 148, per_sm = 1;
+                BVH_CHECK(cudaGetDevice(&dev));
+                BVH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                BVH_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sah_build_kernel, kSahThreads, 0));
+                const int grid = std::max(1, std::min(inner, sms * std::max(per_sm, 1)));  // co-resident
+                sah_build_kernel<<<grid, kSahThreads, 0, stream>>>(inner, node_counter + 1, blo, bhi, sidx, ids,
+                                                                   child, range, par_i, par_l, node_counter,
+                                                                   tasks, node_counter + 2);
                 BVH_CHECK(cudaGetLastError());
-                BVH_CHECK(cudaMemcpyAsync(&h_tasks, next_count, sizeof(int), cudaMemcpyDeviceToHost, stream));
-                BVH_CHECK(cudaStreamSynchronize(stream));
-                SahTask* sw = tasks;
-                tasks = tasks2;
-                tasks2 = sw;
             }
             depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
             BVH_CHECK(cudaGetLastError());
@@ -739,7 +769,6 @@ done:
     dev_free(scan_tmp);
     dev_free(sidx);
     dev_free(tasks);
-    dev_free(tasks2);
     dev_free(node_counter);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
