@@ -384,3 +384,40 @@ def test_scene_churn_reuses_device_memory_safely():
             else:
                 assert np.array_equal(first[i], r.sweep.values) or \
                     np.max(np.abs(first[i] - r.sweep.values)) <= 1e-12 * np.max(np.abs(first[i]))
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_rank_shards_add_up_to_the_full_sweep(world):
+    """Every rank's shard (mcsbr_gpu_trace_device with rank / world) traced on
+    this one GPU in turn: the shards' raw sums and counters add up to the
+    single-launch sweep -- the multi-GPU partition on the real kernel (the
+    NCCL all-reduce is the same sum)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2511_07586_b200 import _abi as A
+    from paper_2511_07586_b200 import distributed as D
+
+    obj, mm = M.dihedral_grid(0.5, 8)
+    s = M.Scene(M.load_scene(obj, mm))
+    cfg = M.McConfig(strata_per_wavelength=5, samples_per_stratum=2, max_bounce=4, seed=2)
+    excs = [M.monostatic_excitation(90.0, p) for p in (5.0, 30.0, 45.0, 85.0)]
+    freqs = np.linspace(9.5e9, 10.5e9, 3)
+    full, st_full = M.estimate_batch(s, [(e, 0.0) for e in excs], [[e] for e in excs], freqs, cfg)
+    n = len(excs)
+    inc = (A.Incidence * n)(*[e.incidence(0.0) for e in excs])
+    rx = (A.Receiver * n)(*[e.receiver() for e in excs])
+    c = cfg.to_c()
+    dev = torch.device("cuda", 0)
+    sums = torch.zeros(n * len(freqs) * 8, dtype=torch.float64, device=dev)
+    counters = torch.zeros(A.MCSBR_COUNTER_WORDS, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for rank in range(world):
+        A.check(A.lib().mcsbr_gpu_trace_device(
+            s.handle, inc, n, rx, 1, 1, freqs.ctypes.data_as(C.POINTER(C.c_double)), len(freqs), C.byref(c),
+            rank, world, C.c_void_p(sums.data_ptr()), C.c_void_p(counters.data_ptr()),
+            C.c_void_p(stream.cuda_stream)))
+    vals, st = D.allreduce_finalize(sums, counters, freqs, n)
+    assert st.rays_launched == st_full.rays_launched and st.contributions == st_full.contributions
+    assert np.max(np.abs(vals.reshape(n, 1, 4, len(freqs)) - full)) <= 1e-10 * np.max(np.abs(full))
