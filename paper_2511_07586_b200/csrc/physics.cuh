@@ -225,13 +225,17 @@ __device__ inline Basis sp_basis(V3 dir_in, V3 normal, double n1, double n2, boo
 // faults whichever branches are formed)
 __device__ __forceinline__ void transverse_guard(const CV3& e, const Basis& b, uint32_t& fault) {
     const V3 dir_in = cross(b.s_hat, b.p_in);
-    const double lim = 1e-9 * (1.0 + norm(e));
-    if (cnorm2(dot(e, dir_in)) > lim * lim) fault |= kFaultTransverse;
+    // (1 + |e|)^2 >= 1 + |e|^2 (halved for rounding): the square root only when this bound does not clear it
+    const double de2 = cnorm2(dot(e, dir_in));
+    if (de2 > 0.5e-18 * (1.0 + (cnorm2(e.x) + cnorm2(e.y) + cnorm2(e.z)))) {
+        const double lim = 1e-9 * (1.0 + norm(e));
+        if (de2 > lim * lim) fault |= kFaultTransverse;
+    }
 }
 __device__ __forceinline__ void transverse_guard(const V3& e, const Basis& b, uint32_t& fault) {
     const V3 dir_in = cross(b.s_hat, b.p_in);
     const double de = dot(e, dir_in);
-    if (de * de > 1e-18 * (1.0 + dot(e, e))) {
+    if (de * de > 0.5e-18 * (1.0 + dot(e, e))) {
         const double lim = 1e-9 * (1.0 + norm(e));
         if (de * de > lim * lim) fault |= kFaultTransverse;
     }
@@ -240,28 +244,23 @@ __device__ __forceinline__ void transverse_guard(const V3& e, const Basis& b, ui
 __device__ __forceinline__ CV3 branch_field(const CV3& e, int branch, const Coeffs& co, const Basis& b) {
     const Cx es = dot(e, b.s_hat);
     const Cx ep = dot(e, b.p_in);
-    if (branch == 0) return cvreal(b.s_hat) * (es * co.r_s) + cvreal(b.p_out_r) * (ep * co.r_p);
-    return cvreal(b.s_hat) * (es * co.t_s) + cvreal(b.p_out_t) * (ep * co.t_p);
+    const bool r = branch == 0;  // operands selected, one copy of the arithmetic
+    return vmul(b.s_hat, es * (r ? co.r_s : co.t_s)) + vmul(r ? b.p_out_r : b.p_out_t, ep * (r ? co.r_p : co.t_p));
 }
 __device__ __forceinline__ V3 branch_field(const V3& e, int branch, const Coeffs& co, const Basis& b) {
     const double es = dot(e, b.s_hat);
     const double ep = dot(e, b.p_in);
-    if (branch == 0) return b.s_hat * (es * co.r_s.re) + b.p_out_r * (ep * co.r_p.re);
-    return b.s_hat * (es * co.t_s.re) + b.p_out_t * (ep * co.t_p.re);
+    const bool r = branch == 0;
+    return b.s_hat * (es * (r ? co.r_s.re : co.t_s.re)) + (r ? b.p_out_r : b.p_out_t) * (ep * (r ? co.r_p.re : co.t_p.re));
 }
 
 // branch: 0 = reflect, 1 = transmit
 __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs& co,
                                           const Basis& b, uint32_t& fault) {
-    // Transversality guard (the reference throws DomainError).  Only the fault
-    // flag depends on it, so it is evaluated on squares: |x|^2 > (1e-9 (1+|e|))^2.
-    const V3 dir_in = cross(b.s_hat, b.p_in);
-    const double lim = 1e-9 * (1.0 + norm(e));
-    if (cnorm2(dot(e, dir_in)) > lim * lim) fault |= kFaultTransverse;
-    const Cx es = dot(e, b.s_hat);
-    const Cx ep = dot(e, b.p_in);
-    if (branch == 0) return cvreal(b.s_hat) * (es * co.r_s) + cvreal(b.p_out_r) * (ep * co.r_p);
-    return cvreal(b.s_hat) * (es * co.t_s) + cvreal(b.p_out_t) * (ep * co.t_p);
+    // transversality guard (the reference throws DomainError); only the fault
+    // flag depends on it
+    transverse_guard(e, b, fault);
+    return branch_field(e, branch, co, b);
 }
 
 // Real-field version for PEC hits (real coefficients r_s = -1, r_p = +1):
@@ -269,18 +268,8 @@ __device__ inline CV3 interface_transform(const CV3& e, int branch, const Coeffs
 // parts are exactly +-0 there); only the reflected branch exists.
 __device__ inline V3 interface_transform(const V3& e, int branch, const Coeffs& co, const Basis& b,
                                          uint32_t& fault) {
-    const V3 dir_in = cross(b.s_hat, b.p_in);
-    // transversality guard: (1 + |e|)^2 >= 1 + |e|^2, so the square root is
-    // only needed when the cheap bound does not already clear the field
-    const double de = dot(e, dir_in);
-    if (de * de > 1e-18 * (1.0 + dot(e, e))) {
-        const double lim = 1e-9 * (1.0 + norm(e));
-        if (de * de > lim * lim) fault |= kFaultTransverse;
-    }
-    const double es = dot(e, b.s_hat);
-    const double ep = dot(e, b.p_in);
-    if (branch == 0) return b.s_hat * (es * co.r_s.re) + b.p_out_r * (ep * co.r_p.re);
-    return b.s_hat * (es * co.t_s.re) + b.p_out_t * (ep * co.t_p.re);
+    transverse_guard(e, b, fault);
+    return branch_field(e, branch, co, b);
 }
 
 }  // namespace mcsbr_dev

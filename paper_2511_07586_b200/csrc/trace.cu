@@ -1072,31 +1072,40 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                         candidate = !dark_exit && h.exterior_facing;
                         if (candidate) {
                             // meca_currents (farfield.cpp:11-45) for both pols
-                            EF j0, m0, j1, m1;
+                            // The three cases share one copy of the arithmetic
+                            // (operands selected per lane, so a warp mixing PEC,
+                            // ambient-side and exiting hits runs it once):
+                            //   sc 0: j = n x ((d x e) n1) 2,              m = 0
+                            //   sc 1: j = n x ((d x e + d_r x e_r) n1),    m = (e + e_r) x n
+                            //   sc 2: j = n_o x ((d_t x e_t) n2),          m = e_t x n_o, n_o = -n
+                            // each the reference's expression operation for operation.
+                            const bool ex = sc == 2;
+                            EF f0 = ef_zero<EF>(), f1 = ef_zero<EF>();  // e_r (sc 1) / e_t (sc 2)
+                            if (sc != 0) {
+                                if constexpr (kDet) {
+                                    f0 = ex ? et0 : er0;
+                                    f1 = ex ? et1 : er1;
+                                } else {
+                                    f0 = branch_field(s.e0, ex ? 1 : 0, co, b);
+                                    f1 = branch_field(s.e1, ex ? 1 : 0, co, b);
+                                }
+                            }
+                            const V3 nrm = ex ? -h.normal : h.normal;
+                            const V3 dj = ex ? b.dir_t : s.dir;
+                            const NT nj = ex ? h.n_transmit : s.medium_n;
+                            EF x0 = cross(dj, ex ? f0 : s.e0), x1 = cross(dj, ex ? f1 : s.e1);
+                            if (sc == 1) {
+                                x0 = x0 + cross(b.dir_r, f0);
+                                x1 = x1 + cross(b.dir_r, f1);
+                            }
+                            EF j0 = cross(nrm, x0 * nj), j1 = cross(nrm, x1 * nj);
+                            EF m0 = ef_zero<EF>(), m1 = ef_zero<EF>();
                             if (sc == 0) {
-                                j0 = cross(h.normal, cross(s.dir, s.e0) * s.medium_n) * 2.0;
-                                j1 = cross(h.normal, cross(s.dir, s.e1) * s.medium_n) * 2.0;
-                                m0 = ef_zero<EF>();
-                                m1 = ef_zero<EF>();
-                            } else if (sc == 1) {
-                                if constexpr (!kDet) {
-                                    er0 = branch_field(s.e0, 0, co, b);
-                                    er1 = branch_field(s.e1, 0, co, b);
-                                }
-                                j0 = cross(h.normal, (cross(s.dir, s.e0) + cross(b.dir_r, er0)) * s.medium_n);
-                                j1 = cross(h.normal, (cross(s.dir, s.e1) + cross(b.dir_r, er1)) * s.medium_n);
-                                m0 = cross(s.e0 + er0, h.normal);
-                                m1 = cross(s.e1 + er1, h.normal);
+                                j0 = j0 * 2.0;
+                                j1 = j1 * 2.0;
                             } else {
-                                if constexpr (!kDet) {
-                                    et0 = branch_field(s.e0, 1, co, b);
-                                    et1 = branch_field(s.e1, 1, co, b);
-                                }
-                                const V3 n_out = -h.normal;
-                                j0 = cross(n_out, cross(b.dir_t, et0) * h.n_transmit);
-                                j1 = cross(n_out, cross(b.dir_t, et1) * h.n_transmit);
-                                m0 = cross(et0, n_out);
-                                m1 = cross(et1, n_out);
+                                m0 = cross(ex ? f0 : s.e0 + f0, nrm);
+                                m1 = cross(ex ? f1 : s.e1 + f1, nrm);
                             }
                             // make_contribution (farfield.cpp:70-85)
                             const double cos_n = fabs(dot(s.dir, h.normal));
