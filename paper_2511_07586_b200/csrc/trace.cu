@@ -97,9 +97,12 @@ __device__ __forceinline__ FRay make_fray(const SceneView& S, V3 o, V3 d, bool o
     const V3 oc = o - c;
     r.t_skip = 0.0;
     if (outside) {
-        const double dd = dot(d, d);
+        // (b - R' |d|) / |d|^2 = y (b y - R'), y = 1/|d| (rsqrt, ~1 ulp): the
+        // advance only has to stay below the sphere entry, and R' = 1.01 R
+        // leaves 0.01 R / |d| of slack for the rounding (|b| << 1e13 R)
+        const double y = rsqrt(dot(d, d));
         const double b = -dot(oc, d);
-        const double skip = (b - S.skip_radius * sqrt(dd)) / dd;
+        const double skip = y * (b * y - S.skip_radius);
         r.t_skip = skip > 0.0 ? skip : 0.0;
     }
     const V3 ot = oc + d * r.t_skip;
@@ -572,7 +575,7 @@ __device__ __forceinline__ Entry locate(const TraceParams& P, const IncDev& I, u
 // sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
 template <typename NT, typename EF>
 __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
-                                          const Entry& en, Path<NT, EF>& s) {
+                                          const Entry& en, Path<NT, EF>& s, const volatile double* rcp) {
     const uint32_t cell = en.cell, sample = en.sample, i = en.i, j = en.j;
     const uint64_t entry = en.entry;
     double ju = 0.5, jv = 0.5;
@@ -589,8 +592,17 @@ __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I,
             jv = philox_uniform(P.seed, s.key, 0, kLaunchV);
         }
     }
-    const double su = -1.0 + 2.0 * (static_cast<double>(i) + ju) / I.nu;
-    const double sv = -1.0 + 2.0 * (static_cast<double>(j) + jv) / I.nv;
+    // -1 + 2 (i + ju) / nu, the quotient from the incidence's shared
+    // reciprocals rcp[0], rcp[1] (div_by: identical to '/')
+    const double pu = 2.0 * (static_cast<double>(i) + ju), pv = 2.0 * (static_cast<double>(j) + jv);
+    bool ok = true;
+    double qu = mcsbr_dev::div_by(pu, I.nu, rcp[0], ok), qv = mcsbr_dev::div_by(pv, I.nv, rcp[1], ok);
+    if (!ok) {
+        qu = pu / I.nu;
+        qv = pv / I.nv;
+    }
+    const double su = -1.0 + qu;
+    const double sv = -1.0 + qv;
     const V3 c = ld3(I.center), u = ld3(I.u), v = ld3(I.v);
     const V3 p = (c + u * (su * I.half_u)) + v * (sv * I.half_v);
     const V3 k = ld3(I.k_inc);
@@ -820,6 +832,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
     __shared__ unsigned int s_bounce[3 * 64];
     __shared__ double s_state[kSlotFields * kSlotThreads];
     __shared__ unsigned long long s_sched[kSlotThreads / 32][4];
+    __shared__ double s_rcp[kSlotThreads / 32][2];  // reciprocals of the incidence's nu, nv (init_path)
     for (int i = threadIdx.x; i < 8; i += blockDim.x) s_cnt[i] = 0;
     for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
@@ -913,7 +926,11 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
         uint64_t cursor = I.entry_begin + (q0 - I.g_begin);  // warp-uniform
         uint64_t e_end = I.entry_begin + (min(q1, g_end_a) - I.g_begin);
         __syncwarp();
-        if (lane == 0) q[0] = min(q1, g_end_a);
+        if (lane == 0) {
+            q[0] = min(q1, g_end_a);
+            s_rcp[warp][0] = mcsbr_dev::rcp_seed(I.nu);
+            s_rcp[warp][1] = mcsbr_dev::rcp_seed(I.nv);
+        }
         __syncwarp();
         if (a != cur_a) {
             flush();
@@ -963,7 +980,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_k
                 const unsigned rank = __popc(need & ((1u << lane) - 1u));
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
-                    init_path(P, I, a + P.inc_base, locate(P, I, mine), s);
+                    init_path(P, I, a + P.inc_base, locate(P, I, mine), s, s_rcp[warp]);
                     save_em<L>(sl, s);
                     alive = true;
                     ++n_launched;
