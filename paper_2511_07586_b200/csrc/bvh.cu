@@ -345,6 +345,8 @@ __device__ __forceinline__ void sah_split(
     __shared__ float s_cost[3];
     __shared__ int s_split[3], s_nl[3];
     __shared__ int s_warp_l[kSahThreads / 32];
+    __shared__ float s_ra[3][kSahBins];  // sweep: suffix areas / counts per axis
+    __shared__ int s_rc[3][kSahBins];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int end = t.first + t.count;
     auto centroid = [&](uint32_t p, int a) {
@@ -420,8 +422,8 @@ __device__ __forceinline__ void sah_split(
         float best = INFINITY;
         int split = -1, nl_best = 0;
         if (s_scale[a] != 0.0f) {
-            float ra[kSahBins];
-            int rc[kSahBins];
+            float* ra = s_ra[a];
+            int* rc = s_rc[a];
             float l0 = INFINITY, l1 = INFINITY, l2 = INFINITY, h0 = -INFINITY, h1 = -INFINITY, h2 = -INFINITY;
             int n = 0;
             for (int b = kSahBins - 1; b >= 1; --b) {  // suffix: bins b..15
@@ -556,7 +558,7 @@ __device__ __forceinline__ void sah_split(
 // parent has published the task (a task's parent always has a smaller id and
 // is already being processed, so the waits always end).  One launch instead
 // of one launch plus a host round trip per tree level.
-__global__ void __launch_bounds__(kSahThreads) sah_build_kernel(
+__global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
     int n_inner, int* __restrict__ head, const float4* __restrict__ blo, const float4* __restrict__ bhi,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
