@@ -502,8 +502,14 @@ def estimate_batch(scene: Scene, incidences: list, receivers: list, frequencies,
     freqs = np.ascontiguousarray(np.asarray(frequencies, dtype=np.float64).reshape(-1))
     n_inc = len(incidences)
     n_rx = len(receivers[0]) if receivers else 0
-    inc_arr = (A.Incidence * n_inc)(*[e.incidence(spw) for e, spw in incidences])
-    rx_arr = (A.Receiver * (n_inc * n_rx))(*[r.receiver() for rl in receivers for r in rl])
+    # the C structs are plain doubles: pack them with numpy (one array per
+    # call instead of a ctypes object per incidence / receiver)
+    inc_np = np.array([(*e.k_inc, *e.pol_v, *e.pol_h, spw) for e, spw in incidences],
+                      dtype=np.float64).reshape(n_inc, 10)
+    rx_np = np.array([(*r.k_scatter, *r.rx_v, *r.rx_h) for rl in receivers for r in rl],
+                     dtype=np.float64).reshape(n_inc * n_rx, 9)
+    inc_arr = (A.Incidence * n_inc).from_buffer(inc_np)
+    rx_arr = (A.Receiver * (n_inc * n_rx)).from_buffer(rx_np)
     values = np.zeros((n_inc, n_rx, 4, len(freqs), 2), dtype=np.float64)
     st = A.Stats()
     cfg = config.to_c()
