@@ -311,8 +311,10 @@ __global__ void depth_kernel(int n, const int* __restrict__ parent_inner, const 
 // unchanged; ranges stay contiguous because every split partitions its own
 // range.  The level loop runs on the host (one small readback per level).
 
+// flip: the range's primitives are in idx (0) or idx2 (1); a block task
+// partitions into the other buffer, so no copy-back pass
 struct SahTask {
-    int first, count, node;
+    int first, count, node, flip;
 };
 
 #ifndef MCSBR_SAH_BINS
@@ -333,11 +335,190 @@ __device__ __forceinline__ float half_area(float lx, float ly, float lz, float h
     return (dx < 0.f || dy < 0.f || dz < 0.f) ? 0.f : dx * dy + dy * dz + dz * dx;
 }
 
+// Subtrees of at most kWarpBuild primitives are built by ONE warp, start to
+// finish, instead of one block-wide task per inner node (a small task's block
+// time is all barriers and global round trips: ~80% of the build's stall
+// samples).  Lane l holds one primitive; per node and axis the members are
+// ranked by centroid (ties by lane), the boxes gathered in that order, and
+// prefix / suffix bound scans give the exact SAH cost of every object split
+// A_L N_L + A_R N_R; the cheapest (axis, position) wins and the members are
+// permuted into that order, so each child is again a contiguous lane range.
+// Node ids come from the top of the id space (`down` counts down) and are
+// marked 2 in `ready`, which tells the persistent loop that no published
+// task remains above them.
+#ifdef MCSBR_SAH_PROF
+// build profile (A/B builds only): per phase, clock cycles summed over tasks
+// by each block's thread 0; [0] = waiting for a task, [8] = tasks, [9] = sum of counts
+__device__ unsigned long long g_sah_prof[10];
+#define SAHP0() long long sahp_t = clock64()
+#define SAHP(k)                                                                       \
+    do {                                                                              \
+        if (threadIdx.x == 0) {                                                       \
+            const long long now = clock64();                                          \
+            atomicAdd(&g_sah_prof[k], static_cast<unsigned long long>(now - sahp_t)); \
+            sahp_t = now;                                                             \
+        }                                                                             \
+    } while (0)
+#else
+#define SAHP0() (void)0
+#define SAHP(k) (void)0
+#endif
+constexpr int kWarpBuild = 32;
+
+__device__ __forceinline__ float wscan_min_up(float v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const float w = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = fminf(v, w);
+    }
+    return v;
+}
+__device__ __forceinline__ float wscan_max_up(float v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const float w = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = fmaxf(v, w);
+    }
+    return v;
+}
+__device__ __forceinline__ float wscan_min_down(float v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const float w = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = fminf(v, w);
+    }
+    return v;
+}
+__device__ __forceinline__ float wscan_max_down(float v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const float w = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = fmaxf(v, w);
+    }
+    return v;
+}
+
+__device__ __noinline__ void warp_subtree(int first, int count, int root, const float4* __restrict__ blo,
+                                          const float4* __restrict__ bhi, const uint32_t* src_buf,
+                                          uint32_t* __restrict__ idx, int2* __restrict__ child, int2* __restrict__ range,
+                                          int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ down,
+                                          int* __restrict__ ready, volatile int* stk) {
+    constexpr unsigned F = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    uint32_t p = 0;
+    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, c[3] = {0.f, 0.f, 0.f};
+    if (lane < count) {
+        p = src_buf[first + lane];
+        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
+        lo[0] = l.x; lo[1] = l.y; lo[2] = l.z;
+        hi[0] = h.x; hi[1] = h.y; hi[2] = h.z;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) c[k] = 0.5f * (lo[k] + hi[k]);
+    }
+    int sp = 1;
+    if (lane == 0) {
+        stk[0] = 0;
+        stk[1] = count;
+        stk[2] = root;
+    }
+    __syncwarp();
+    while (sp > 0) {
+        --sp;
+        const int b = stk[3 * sp], cnt = stk[3 * sp + 1], id = stk[3 * sp + 2];
+        __syncwarp();
+        const bool mem = lane >= b && lane < b + cnt;
+        float best = INFINITY;
+        int best_k = cnt / 2, best_src = lane;  // (no finite cost: split by position)
+#pragma unroll 1
+        for (int a = 0; a < 3; ++a) {
+            const float ca = a == 0 ? c[0] : (a == 1 ? c[1] : c[2]);
+            int rank = 0;
+            for (int k = b; k < b + cnt; ++k) {
+                const float ck = __shfl_sync(F, ca, k);
+                rank += (ck < ca || (ck == ca && k < lane)) ? 1 : 0;
+            }
+            int src = lane;  // member that lands on position `lane` of the sorted order
+            for (int r = 0; r < cnt; ++r) {
+                const unsigned m = __ballot_sync(F, mem && rank == r);
+                if (lane == b + r) src = __ffs(m) - 1;
+            }
+            float sl[3], sh[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                sl[k] = __shfl_sync(F, lo[k], src);
+                sh[k] = __shfl_sync(F, hi[k], src);
+                if (!mem) {
+                    sl[k] = INFINITY;
+                    sh[k] = -INFINITY;
+                }
+            }
+            float pl[3], ph[3], rl[3], rh[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                pl[k] = wscan_min_up(sl[k], lane);
+                ph[k] = wscan_max_up(sh[k], lane);
+                rl[k] = __shfl_down_sync(F, wscan_min_down(sl[k], lane), 1);
+                rh[k] = __shfl_down_sync(F, wscan_max_down(sh[k], lane), 1);
+            }
+            float cost = INFINITY;
+            if (lane >= b && lane < b + cnt - 1) {  // left = positions b..lane
+                const int nl = lane - b + 1;
+                cost = half_area(pl[0], pl[1], pl[2], ph[0], ph[1], ph[2]) * nl +
+                       half_area(rl[0], rl[1], rl[2], rh[0], rh[1], rh[2]) * (cnt - nl);
+            }
+            float bc = cost;
+            int bk = lane;
+            for (int o = 16; o > 0; o >>= 1) {
+                const float oc = __shfl_xor_sync(F, bc, o);
+                const int ok = __shfl_xor_sync(F, bk, o);
+                if (oc < bc || (oc == bc && ok < bk)) {
+                    bc = oc;
+                    bk = ok;
+                }
+            }
+            if (bc < best) {
+                best = bc;
+                best_k = bk - b + 1;
+                best_src = src;
+            }
+        }
+        // members into the chosen order (non-members keep their lane)
+        p = __shfl_sync(F, p, best_src);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = __shfl_sync(F, lo[k], best_src);
+            hi[k] = __shfl_sync(F, hi[k], best_src);
+            c[k] = __shfl_sync(F, c[k], best_src);
+        }
+        if (lane == 0) {
+            int enc[2];
+            for (int sd = 0; sd < 2; ++sd) {
+                const int bs = sd ? b + best_k : b, cs = sd ? cnt - best_k : best_k;
+                if (cs == 1) {
+                    enc[sd] = ~(first + bs);
+                    par_l[first + bs] = id;
+                } else {
+                    const int cid = atomicSub(down, 1) - 1;
+                    enc[sd] = cid;
+                    par_i[cid] = id;
+                    atomicExch(ready + cid, 2);
+                    stk[3 * sp] = bs;
+                    stk[3 * sp + 1] = cs;
+                    stk[3 * sp + 2] = cid;
+                    ++sp;
+                }
+            }
+            child[id] = make_int2(enc[0], enc[1]);
+            range[id] = make_int2(first + b, first + b + cnt - 1);
+        }
+        sp = __shfl_sync(F, sp, 0);
+        __syncwarp();
+    }
+    if (lane < count) idx[first + lane] = p;
+}
+
 __device__ __forceinline__ void sah_split(
     const SahTask t, const float4* __restrict__ blo, const float4* __restrict__ bhi,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
-    int* __restrict__ ready) {
+    int* __restrict__ ready, int* __restrict__ down) {
+    SAHP0();
     __shared__ int s_cnt[3][kSahBins];
     __shared__ int s_box[3][kSahBins][6];
     __shared__ float s_red[2][3][kSahThreads / 32];
@@ -349,6 +530,8 @@ __device__ __forceinline__ void sah_split(
     __shared__ int s_rc[3][kSahBins];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int end = t.first + t.count;
+    const uint32_t* in = t.flip ? idx2 : idx;
+    uint32_t* out = t.flip ? idx : idx2;
     auto centroid = [&](uint32_t p, int a) {
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
         const float lv = a == 0 ? l.x : (a == 1 ? l.y : l.z), hv = a == 0 ? h.x : (a == 1 ? h.y : h.z);
@@ -360,7 +543,7 @@ __device__ __forceinline__ void sah_split(
     // 1. centroid bounds
     float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
-        const uint32_t p = idx[i];
+        const uint32_t p = in[i];
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
         const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
 #pragma unroll
@@ -397,9 +580,10 @@ __device__ __forceinline__ void sah_split(
         s_scale[tid] = hi > lo ? (kSahBins * (1.0f - 1e-6f)) / (hi - lo) : 0.0f;
     }
     __syncthreads();
+    SAHP(1);
     // 2. bins
     for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
-        const uint32_t p = idx[i];
+        const uint32_t p = in[i];
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
         const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
 #pragma unroll
@@ -416,6 +600,7 @@ __device__ __forceinline__ void sah_split(
         }
     }
     __syncthreads();
+    SAHP(2);
     // 3. SAH sweep per axis
     if (tid < 3) {
         const int a = tid;
@@ -462,6 +647,7 @@ __device__ __forceinline__ void sah_split(
         s_nl[a] = nl_best;
     }
     __syncthreads();
+    SAHP(3);
     int axis = -1;
     float best = INFINITY;
     for (int a = 0; a < 3; ++a)
@@ -472,32 +658,17 @@ __device__ __forceinline__ void sah_split(
     int nl = axis >= 0 ? s_nl[axis] : t.count / 2;  // no usable split: median by position
     const int split = axis >= 0 ? s_split[axis] : 0;
     const float cmin = axis >= 0 ? s_cmin[axis] : 0.0f, scale = axis >= 0 ? s_scale[axis] : 0.0f;
-    if (stride > 1 && axis >= 0) {  // sampled: count the left side exactly
-        int c = 0;
-        for (int i = t.first + tid; i < end; i += kSahThreads) {
-            const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(idx[i], axis) - cmin) * scale)));
-            c += b < split;
-        }
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        __syncthreads();
-        if (lane == 0) s_warp_l[wid] = c;
-        __syncthreads();
-        nl = 0;
-        for (int w = 0; w < kSahThreads / 32; ++w) nl += s_warp_l[w];
-        __syncthreads();
-        if (nl == 0 || nl == t.count) {  // the sample's split separates nothing
-            axis = -1;
-            nl = t.count / 2;
-        }
-    }
-    // 4. stable partition of [first, end) into idx2, then back
+    SAHP(4);
+    // 4. partition of [first, end) from `in` into `out`: the left side from
+    // `first` up in order, the right side from `end - 1` down, so one pass
+    // needs no left count (a sampled split's exact count falls out of it)
     int left_base = 0, right_base = 0;
     for (int base = t.first; base < end; base += kSahThreads) {
         const int i = base + tid;
         bool valid = i < end, left = false;
         uint32_t p = 0;
         if (valid) {
-            p = idx[i];
+            p = in[i];
             if (axis >= 0) {
                 const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(p, axis) - cmin) * scale)));
                 left = b < split;
@@ -523,27 +694,40 @@ __device__ __forceinline__ void sah_split(
             const unsigned below = (1u << lane) - 1u;
             const int pl = wl + __popc(m & below);
             const int pv = wv + __popc(v & below);
-            const int pos = left ? t.first + left_base + pl : t.first + nl + right_base + (pv - pl);
-            idx2[pos] = p;
+            const int pos = left ? t.first + left_base + pl : end - 1 - (right_base + (pv - pl));
+            out[pos] = p;
         }
         left_base += tl;
         right_base += tv - tl;
         __syncthreads();
     }
-    for (int i = t.first + tid; i < end; i += kSahThreads) idx[i] = idx2[i];
-    // 5. children
+    nl = left_base;
+    if (nl == 0 || nl == t.count) nl = t.count / 2;  // a sampled split that separates nothing: by position
+    SAHP(5);
+    // 5. children: single primitives are leaves, small ranges are built by
+    // warps 0 / 1 of this block right away, the rest are published as tasks
+    __shared__ SahTask s_sub[2];
+    __shared__ int s_stk[2][3 * kWarpBuild];
     if (tid == 0) {
         const int starts[2] = {t.first, t.first + nl}, sizes[2] = {nl, t.count - nl};
         int enc[2];
         for (int k = 0; k < 2; ++k) {
-            if (sizes[k] == 1) {
+            s_sub[k].count = 0;
+            if (sizes[k] == 1) {  // a leaf: its primitive goes to the final order (idx)
                 enc[k] = ~starts[k];
                 par_l[starts[k]] = t.node;
+                if (out != idx) idx[starts[k]] = out[starts[k]];
+            } else if (sizes[k] <= kWarpBuild) {
+                const int id = atomicSub(down, 1) - 1;
+                enc[k] = id;
+                par_i[id] = t.node;
+                atomicExch(ready + id, 2);
+                s_sub[k] = SahTask{starts[k], sizes[k], id, 0};
             } else {  // publish the child's task under its inner-node index
                 const int id = atomicAdd(node_counter, 1);
                 enc[k] = id;
                 par_i[id] = t.node;
-                tasks[id] = SahTask{starts[k], sizes[k], id};
+                tasks[id] = SahTask{starts[k], sizes[k], id, t.flip ^ 1};
                 __threadfence();
                 atomicExch(ready + id, 1);
             }
@@ -551,6 +735,12 @@ __device__ __forceinline__ void sah_split(
         child[t.node] = make_int2(enc[0], enc[1]);
         range[t.node] = make_int2(t.first, end - 1);
     }
+    __syncthreads();
+    SAHP(6);
+    if (wid < 2 && s_sub[wid].count >= 2)
+        warp_subtree(s_sub[wid].first, s_sub[wid].count, s_sub[wid].node, blo, bhi, out, idx, child, range, par_i,
+                     par_l, down, ready, s_stk[wid]);
+    SAHP(7);
 }
 
 // Persistent build: every inner node is one task whose index is its node
@@ -562,24 +752,40 @@ __global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
     int n_inner, int* __restrict__ head, const float4* __restrict__ blo, const float4* __restrict__ bhi,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
-    int* __restrict__ ready) {
+    int* __restrict__ ready, int* __restrict__ down) {
     __shared__ int s_id;
     __shared__ SahTask s_task;
     for (;;) {
         if (threadIdx.x == 0) {
-            const int i = atomicAdd(head, 1);
+#ifdef MCSBR_SAH_PROF
+            const long long w0 = clock64();
+#endif
+            int i = atomicAdd(head, 1);
             if (i < n_inner) {
-                while (atomicAdd(ready + i, 0) == 0) __nanosleep(64);
-                __threadfence();
-                s_task.first = __ldcg(&tasks[i].first);
-                s_task.count = __ldcg(&tasks[i].count);
-                s_task.node = __ldcg(&tasks[i].node);
+                int r;
+                while ((r = atomicAdd(ready + i, 0)) == 0) __nanosleep(64);
+                if (r == 2) {
+                    i = n_inner;  // a warp-built node: every id from here up is one
+                } else {
+                    __threadfence();
+                    s_task.first = __ldcg(&tasks[i].first);
+                    s_task.count = __ldcg(&tasks[i].count);
+                    s_task.node = __ldcg(&tasks[i].node);
+                    s_task.flip = __ldcg(&tasks[i].flip);
+                }
             }
             s_id = i;
+#ifdef MCSBR_SAH_PROF
+            atomicAdd(&g_sah_prof[0], static_cast<unsigned long long>(clock64() - w0));
+            if (i < n_inner) {
+                atomicAdd(&g_sah_prof[8], 1ull);
+                atomicAdd(&g_sah_prof[9], static_cast<unsigned long long>(s_task.count));
+            }
+#endif
         }
         __syncthreads();
         if (s_id >= n_inner) break;
-        sah_split(s_task, blo, bhi, idx, idx2, child, range, par_i, par_l, node_counter, tasks, ready);
+        sah_split(s_task, blo, bhi, idx, idx2, child, range, par_i, par_l, node_counter, tasks, ready, down);
         __syncthreads();
     }
 }
@@ -672,12 +878,13 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         if (sah) {
             BVH_CHECK(dev_malloc(&sidx, sizeof(uint32_t) * n));
             BVH_CHECK(dev_malloc(&tasks, sizeof(SahTask) * inner));
-            BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * (inner + 2)));  // counter, head, ready[inner]
+            BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * (inner + 3)));  // counter, head, ready[inner], down
             BVH_CHECK(cudaMemcpyAsync(sidx, ids_s, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
             BVH_CHECK(cudaMemsetAsync(node_counter, 0, sizeof(int) * (inner + 2), stream));
+            BVH_CHECK(cudaMemcpyAsync(node_counter + inner + 2, &inner, sizeof(int), cudaMemcpyHostToDevice, stream));
             {
                 const int init[3] = {1, 0, 1};  // next node id, head, ready[0]
-                const SahTask root{0, n, 0};
+                const SahTask root{0, n, 0, 0};
                 BVH_CHECK(cudaMemcpyAsync(node_counter, init, sizeof(init), cudaMemcpyHostToDevice, stream));
                 BVH_CHECK(cudaMemcpyAsync(tasks, &root, sizeof(SahTask), cudaMemcpyHostToDevice, stream));
                 int dev = 0, sms = 148, per_sm = 1;
@@ -687,11 +894,24 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                 const int grid = std::max(1, std::min(inner, sms * std::max(per_sm, 1)));  // co-resident
                 sah_build_kernel<<<grid, kSahThreads, 0, stream>>>(inner, node_counter + 1, blo, bhi, sidx, ids,
                                                                    child, range, par_i, par_l, node_counter,
-                                                                   tasks, node_counter + 2);
+                                                                   tasks, node_counter + 2, node_counter + inner + 2);
                 BVH_CHECK(cudaGetLastError());
             }
             depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
             BVH_CHECK(cudaGetLastError());
+#ifdef MCSBR_SAH_PROF
+            {
+                unsigned long long pr[10];
+                BVH_CHECK(cudaMemcpyFromSymbolAsync(pr, g_sah_prof, sizeof(pr), 0, cudaMemcpyDeviceToHost, stream));
+                BVH_CHECK(cudaStreamSynchronize(stream));
+                std::fprintf(stderr, "sah prof n=%d tasks=%llu prims=%llu | wait %.3g bounds %.3g bins %.3g sweep %.3g "
+                             "select %.3g partition %.3g children %.3g warpbuild %.3g (Mcycles, summed over blocks)\n",
+                             n, pr[8], pr[9], pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[4] * 1e-6,
+                             pr[5] * 1e-6, pr[6] * 1e-6, pr[7] * 1e-6);
+                const unsigned long long z[10] = {};
+                BVH_CHECK(cudaMemcpyToSymbolAsync(g_sah_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, stream));
+            }
+#endif
             unsigned int md = 0;
             BVH_CHECK(cudaMemcpyAsync(&md, dmax, sizeof(md), cudaMemcpyDeviceToHost, stream));
             BVH_CHECK(cudaStreamSynchronize(stream));
