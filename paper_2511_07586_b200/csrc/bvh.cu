@@ -662,43 +662,64 @@ __device__ __forceinline__ void sah_split(
     // 4. partition of [first, end) from `in` into `out`: the left side from
     // `first` up in order, the right side from `end - 1` down, so one pass
     // needs no left count (a sampled split's exact count falls out of it)
+    // kPU sub-chunks of 256 per iteration: their loads issued together and
+    // one barrier pair per iteration (a top-level node's partition is the
+    // build's critical path)
+    constexpr int kPU = 4;
+    __shared__ int s_wl[kPU][kSahThreads / 32];
     int left_base = 0, right_base = 0;
-    for (int base = t.first; base < end; base += kSahThreads) {
-        const int i = base + tid;
-        bool valid = i < end, left = false;
-        uint32_t p = 0;
-        if (valid) {
-            p = in[i];
-            if (axis >= 0) {
-                const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(p, axis) - cmin) * scale)));
-                left = b < split;
-            } else {
-                left = (i - t.first) < nl;
+    for (int base = t.first; base < end; base += kPU * kSahThreads) {
+        uint32_t p[kPU];
+        bool valid[kPU], left[kPU];
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            const int i = base + j * kSahThreads + tid;
+            valid[j] = i < end;
+            p[j] = valid[j] ? in[i] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            const int i = base + j * kSahThreads + tid;
+            left[j] = false;
+            if (valid[j]) {
+                if (axis >= 0) {
+                    const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(p[j], axis) - cmin) * scale)));
+                    left[j] = b < split;
+                } else {
+                    left[j] = (i - t.first) < nl;
+                }
             }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, valid && left);
-        const unsigned v = __ballot_sync(0xffffffffu, valid);
-        if (lane == 0) s_warp_l[wid] = __popc(m) | (__popc(v) << 16);
+        unsigned m[kPU], v[kPU];
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            m[j] = __ballot_sync(0xffffffffu, valid[j] && left[j]);
+            v[j] = __ballot_sync(0xffffffffu, valid[j]);
+            if (lane == 0) s_wl[j][wid] = __popc(m[j]) | (__popc(v[j]) << 16);
+        }
         __syncthreads();
-        int wl = 0, wv = 0, tl = 0, tv = 0;
-        for (int w = 0; w < kSahThreads / 32; ++w) {
-            const int x = s_warp_l[w];
-            if (w < wid) {
-                wl += x & 0xffff;
-                wv += x >> 16;
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            int wl = 0, wv = 0, tl = 0, tv = 0;
+            for (int w = 0; w < kSahThreads / 32; ++w) {
+                const int x = s_wl[j][w];
+                if (w < wid) {
+                    wl += x & 0xffff;
+                    wv += x >> 16;
+                }
+                tl += x & 0xffff;
+                tv += x >> 16;
             }
-            tl += x & 0xffff;
-            tv += x >> 16;
+            if (valid[j]) {
+                const unsigned below = (1u << lane) - 1u;
+                const int pl = wl + __popc(m[j] & below);
+                const int pv = wv + __popc(v[j] & below);
+                const int pos = left[j] ? t.first + left_base + pl : end - 1 - (right_base + (pv - pl));
+                out[pos] = p[j];
+            }
+            left_base += tl;
+            right_base += tv - tl;
         }
-        if (valid) {
-            const unsigned below = (1u << lane) - 1u;
-            const int pl = wl + __popc(m & below);
-            const int pv = wv + __popc(v & below);
-            const int pos = left ? t.first + left_base + pl : end - 1 - (right_base + (pv - pl));
-            out[pos] = p;
-        }
-        left_base += tl;
-        right_base += tv - tl;
         __syncthreads();
     }
     nl = left_base;
