@@ -322,7 +322,14 @@ struct SahTask {
 #endif
 constexpr int kSahBins = MCSBR_SAH_BINS;
 constexpr int kSahThreads = 256;
-constexpr int kSahSample = 16384;  // primitives sampled to choose the split of a large node
+#ifndef MCSBR_SAH_SAMPLE
+#define MCSBR_SAH_SAMPLE 4096
+#endif
+#ifndef MCSBR_SAH_SAMPLE_X
+#define MCSBR_SAH_SAMPLE_X 2
+#endif
+constexpr int kSahSample = MCSBR_SAH_SAMPLE;  // primitives sampled to choose the split of a large node
+constexpr int kSahSampleFrom = MCSBR_SAH_SAMPLE_X * kSahSample;  // ... of more than this many
 
 __device__ __forceinline__ int fenc(float f) {  // int order == float order
     const int i = __float_as_int(f);
@@ -539,7 +546,7 @@ __device__ __forceinline__ void sah_split(
     };
     // large nodes (the top levels, one block each) choose their split from a
     // strided sample of ~16 k primitives; the partition below counts exactly
-    const int stride = t.count > 4 * kSahSample ? t.count / kSahSample : 1;
+    const int stride = t.count > kSahSampleFrom ? t.count / kSahSample : 1;
     // 1. centroid bounds
     float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
