@@ -1,11 +1,13 @@
-// K1: LBVH builder on the GPU (replaces Scene::build_bvh, proj/src/geometry.cpp:68-144,
+// K1: BVH builder on the GPU (replaces Scene::build_bvh, proj/src/geometry.cpp:68-144,
 // a single-threaded fp64 median split).
 //
 //   1. prim_kernel      per triangle: fp64 AABB padded by box_pad and rounded
 //                       outward to fp32; 63-bit Morton code of the centroid.
 //   2. cub radix sort   (morton, id) pairs.
-//   3. sah_split_kernel binned-SAH top-down build from the Morton order, one
-//                       block per node and level (default); fallback / MCSBR_BVH=lbvh:
+//   3. sah_build_kernel binned-SAH top-down build from the Morton order, one
+//                       persistent launch: block tasks for nodes of > 32
+//                       triangles, one warp per smaller subtree (default);
+//                       fallback / MCSBR_BVH=lbvh:
 //      karras_kernel    Karras (HPG 2012) binary radix tree over the sorted codes
 //                       (ties broken by sort position), one thread per inner node.
 //   4. refit_kernel     bottom-up AABB union with one atomic flag per inner node.
@@ -301,15 +303,16 @@ __global__ void depth_kernel(int n, const int* __restrict__ parent_inner, const 
 
 // ---------------------------------------------------------------------------
 // Binned-SAH top-down build (default; the Karras LBVH is the fallback).
-// One block per node of a level: centroid bounds, 16 bins per axis holding
-// counts and primitive boxes (shared atomics on order-preserving float
-// encodings), the SAH sweep A_L N_L + A_R N_R over the 15 bin boundaries of
-// each axis, then a stable block-wide partition of the node's index range.
-// Nodes split down to single triangles, so the output has the exact shape of
-// the Karras tree (n - 1 inner nodes, child / range / parent arrays, leaves
-// ~position in the final order) and the refit / collapse / emit stages run
-// unchanged; ranges stay contiguous because every split partitions its own
-// range.  The level loop runs on the host (one small readback per level).
+// A node of more than kWarpBuild primitives is a block task: centroid bounds,
+// 16 bins per axis holding counts and primitive boxes (shared atomics on
+// order-preserving float encodings), the SAH sweep A_L N_L + A_R N_R over the
+// 15 bin boundaries of each axis, then a block-wide partition of the node's
+// range into the other index buffer.  Smaller nodes are built to the leaves
+// by one warp (warp_subtree).  Nodes split down to single triangles, so the
+// output has the exact shape of the Karras tree (n - 1 inner nodes, child /
+// range / parent arrays, leaves ~position in the final order) and the refit /
+// collapse / emit stages run unchanged; ranges stay contiguous because every
+// split partitions its own range.  One persistent launch (sah_build_kernel).
 
 // flip: the range's primitives are in idx (0) or idx2 (1); a block task
 // partitions into the other buffer, so no copy-back pass
