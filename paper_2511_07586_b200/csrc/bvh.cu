@@ -374,6 +374,7 @@ __device__ unsigned long long g_sah_prof[10];
 #define SAHP(k) (void)0
 #endif
 constexpr int kWarpBuild = 32;
+constexpr int kStkScr = 3 * kWarpBuild;  // per-warp scratch: node stack, then 32 ints of scatter space
 
 __device__ __forceinline__ float wscan_min_up(float v, int lane) {
     for (int o = 1; o < 32; o <<= 1) {
@@ -443,11 +444,12 @@ __device__ __noinline__ void warp_subtree(int first, int count, int root, const 
                 const float ck = __shfl_sync(F, ca, k);
                 rank += (ck < ca || (ck == ca && k < lane)) ? 1 : 0;
             }
-            int src = lane;  // member that lands on position `lane` of the sorted order
-            for (int r = 0; r < cnt; ++r) {
-                const unsigned m = __ballot_sync(F, mem && rank == r);
-                if (lane == b + r) src = __ffs(m) - 1;
-            }
+            // member that lands on position `lane` of the sorted order (the
+            // ranks are a permutation of the members: scatter, then gather)
+            if (mem) stk[kStkScr + b + rank] = lane;
+            __syncwarp();
+            const int src = mem ? stk[kStkScr + lane] : lane;
+            __syncwarp();
             float sl[3], sh[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -738,7 +740,7 @@ __device__ __forceinline__ void sah_split(
     // 5. children: single primitives are leaves, small ranges are built by
     // warps 0 / 1 of this block right away, the rest are published as tasks
     __shared__ SahTask s_sub[2];
-    __shared__ int s_stk[2][3 * kWarpBuild];
+    __shared__ int s_stk[2][kStkScr + 32];
     if (tid == 0) {
         const int starts[2] = {t.first, t.first + nl}, sizes[2] = {nl, t.count - nl};
         int enc[2];
