@@ -808,9 +808,15 @@ enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_SMEM_MIN_BLOCKS
 #define MCSBR_SMEM_MIN_BLOCKS 4
 #endif
-template <int kMode, bool kLossy>
+// (A/B knob) register budget of the PEC register-mode / fan instantiations
+#ifndef MCSBR_PEC_MIN_BLOCKS
+#define MCSBR_PEC_MIN_BLOCKS 5  // c1 -5%, c2 -0.1% against 4 (96 registers, 5 blocks/SM)
+#endif
+template <int kMode, bool kDiel, bool kLossy>
 struct MinBlocks {
-    static constexpr int value = (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS : MCSBR_MIN_BLOCKS;
+    static constexpr int value = (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS
+                                 : !kDiel               ? MCSBR_PEC_MIN_BLOCKS
+                                                        : MCSBR_MIN_BLOCKS;
 };
 // kDet: the deterministic solver (solver_det.cpp:30-174) on the same engine:
 // midpoint launch (P.jitter = 0, spp = 1), no draws; at a two-branch hit the
@@ -818,7 +824,7 @@ struct MinBlocks {
 // lane's branch stack; a dead lane pops its own stack before it takes a new
 // entry, which reproduces the reference's depth-first, reflect-first order.
 template <int kMode, bool kDiel, bool kLossy, bool kDet>
-__global__ void __launch_bounds__(128, (MinBlocks<kMode, kLossy>::value)) path_kernel(TraceParams P) {
+__global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value)) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeDefer;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
     using L = Layout<!kDiel && !kLossy, kLossy, kRegAcc>;
