@@ -808,15 +808,15 @@ enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_SMEM_MIN_BLOCKS
 #define MCSBR_SMEM_MIN_BLOCKS 4
 #endif
-// (A/B knob) register budget of the PEC register-mode / fan instantiations
+// (A/B knob) register budget of the PEC instantiations (all modes)
 #ifndef MCSBR_PEC_MIN_BLOCKS
-#define MCSBR_PEC_MIN_BLOCKS 5  // c1 -5%, c2 -0.1% against 4 (96 registers, 5 blocks/SM)
+#define MCSBR_PEC_MIN_BLOCKS 5  // against 4: c1 -5%, c4 -3%, c2 -0.1% (96 registers, 5 blocks/SM)
 #endif
 template <int kMode, bool kDiel, bool kLossy>
 struct MinBlocks {
-    static constexpr int value = (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS
-                                 : !kDiel               ? MCSBR_PEC_MIN_BLOCKS
-                                                        : MCSBR_MIN_BLOCKS;
+    static constexpr int value = (!kDiel && !kLossy)    ? MCSBR_PEC_MIN_BLOCKS
+                                 : (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS
+                                                          : MCSBR_MIN_BLOCKS;
 };
 // kDet: the deterministic solver (solver_det.cpp:30-174) on the same engine:
 // midpoint launch (P.jitter = 0, spp = 1), no draws; at a two-branch hit the
