@@ -12,5 +12,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 1 -c 1 -o gpurun_out/path_full -f python tools/profile_c2.py > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 1 -c 1 -o gpurun_out/c4_full -f python tools/profile_isar.py c4 --angles 16 > gpurun_out/ncu_c4.log 2>&1; echo "ncu c4 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 1 -c 1 -o gpurun_out/c5_full -f python tools/profile_isar.py c5 --angles 2 > gpurun_out/ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 2 -c 1 -o gpurun_out/c3_full -f python tools/bench_configs.py --configs c3 --out /tmp/c3.json > gpurun_out/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:accumulate_kernel -s 1 -c 1 -o gpurun_out/c5_acc -f python tools/profile_isar.py c5 --angles 2 > gpurun_out/ncu_c5acc.log 2>&1; echo "ncu c5acc rc=$?"
 timeout 1200 python tools/bench_configs.py --configs c1,c3,c4,c5 --cpu --out gpurun_out/configs.json > gpurun_out/configs.log 2>&1; echo "configs rc=$?"
