@@ -812,9 +812,13 @@ enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2 };
 #ifndef MCSBR_PEC_MIN_BLOCKS
 #define MCSBR_PEC_MIN_BLOCKS 5  // against 4: c1 -5%, c4 -3%, c2 -0.1% (96 registers, 5 blocks/SM)
 #endif
+// (A/B knob) the PEC deferred-accumulation instantiation (F > 1 sweeps)
+#ifndef MCSBR_PEC_DEFER_MIN_BLOCKS
+#define MCSBR_PEC_DEFER_MIN_BLOCKS 6  // against 5: c4 -2.4% (80 registers)
+#endif
 template <int kMode, bool kDiel, bool kLossy>
 struct MinBlocks {
-    static constexpr int value = (!kDiel && !kLossy)    ? MCSBR_PEC_MIN_BLOCKS
+    static constexpr int value = (!kDiel && !kLossy)    ? (kMode == 0 ? MCSBR_PEC_DEFER_MIN_BLOCKS : MCSBR_PEC_MIN_BLOCKS)
                                  : (kMode == 0 || kLossy) ? MCSBR_SMEM_MIN_BLOCKS
                                                           : MCSBR_MIN_BLOCKS;
 };
