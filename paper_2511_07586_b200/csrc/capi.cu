@@ -547,8 +547,8 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // the aperture (their BVH working set outgrows L1/L2: c4 -35% going from
     // 4096 to 256); a small scene's BVH stays cache-resident whatever the
     // window, and fewer, longer chunks there save the per-chunk scheduling
-    // and incidence changes (c2 -2.7% at 1024, c4 +4% at 512).
-    p.chunk_max = env_u32("MCSBR_CHUNK_MAX", s->nt <= kSmallSceneTris ? 1024u : 256u);
+    // and incidence changes (c2 -2.7% at 1024, -3.3% at 2048; c4 +4% at 512).
+    p.chunk_max = env_u32("MCSBR_CHUNK_MAX", s->nt <= kSmallSceneTris ? 2048u : 256u);
     p.chunk_min = env_u32("MCSBR_CHUNK_MIN", 32);
     p.gss_div = env_u32("MCSBR_GSS", 16);
     // band height of the launch-entry dispatch order (0 = linear; a power of two)
