@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define MCSBR_GPU_ABI_VERSION 2
+#define MCSBR_GPU_ABI_VERSION 3
 
 /* ---- status codes ------------------------------------------------------ */
 #define MCSBR_OK 0
@@ -148,6 +148,11 @@ typedef struct mcsbr_stats {
      * = 192 B; the GPU's actual branch-stack allocation is device_stack_bytes. */
     uint64_t forced_stack_bytes;
     uint64_t device_stack_bytes;
+    /* launch rays retired without tracing because no triangle's projection
+     * meets their strata group (provable misses; still counted in
+     * rays_launched and rays_per_bounce[0] exactly as the reference counts
+     * a launch ray that escapes) */
+    uint64_t culled_launch_rays;
 } mcsbr_stats;
 
 /* Mirrors mcsbr::DetConfig (proj/include/mcsbr/solver_det.hpp:12-22).
@@ -333,6 +338,16 @@ MCSBR_API int mcsbr_gpu_path_log(mcsbr_scene* scene, const mcsbr_excitation* exc
 /* Number of kernel launches the last compute call on this thread issued
  * (evidence for the benchmark's gpu_launches key). */
 MCSBR_API uint64_t mcsbr_gpu_last_launch_count(void);
+
+/* Per-kernel device timing on the calling thread (evidence for the
+ * benchmark's roofline): enable = 1 resets the record and starts bracketing
+ * every path-kernel and accumulate launch of this thread's compute calls with
+ * CUDA events on the launch stream; enable = 0 stops.  mcsbr_gpu_kernel_times
+ * waits for the recorded events and returns the summed device milliseconds
+ * and launch counts since the last enable. */
+MCSBR_API void mcsbr_gpu_kernel_timing(int enable);
+MCSBR_API int mcsbr_gpu_kernel_times(double* path_ms, uint64_t* path_launches, double* acc_ms,
+                                     uint64_t* acc_launches);
 
 #ifdef __cplusplus
 }

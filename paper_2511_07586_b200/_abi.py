@@ -109,6 +109,7 @@ class Stats(C.Structure):
         ("roulette_survivors", C.c_uint64 * MCSBR_MAX_BOUNCE_LIMIT),
         ("wall_ms", C.c_double), ("kernel_ms", C.c_double),
         ("forced_stack_bytes", C.c_uint64), ("device_stack_bytes", C.c_uint64),
+        ("culled_launch_rays", C.c_uint64),
     ]
 
 
@@ -226,6 +227,8 @@ SIGNATURES = {
                   _DP],
     ),
     "mcsbr_gpu_last_launch_count": (C.c_uint64, []),
+    "mcsbr_gpu_kernel_timing": (None, [C.c_int]),
+    "mcsbr_gpu_kernel_times": (C.c_int, [_DP, _U64P, _DP, _U64P]),
 }
 
 _lib = None

@@ -50,26 +50,164 @@ struct Box {
     float lo[3], hi[3];
 };
 
-__global__ void prim_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri, uint32_t n,
+// Early split clipping (Ernst & Greiner, RT 2007): a sliver triangle whose
+// bounding box is much larger than the triangle itself (the long thin fan
+// triangles of a capped cylinder, a wing-tip cap, ...) makes every ray near
+// it descend to its leaf.  Such a triangle is referenced by k pieces: its
+// box is cut into k equal slabs along the longest axis, and piece j's box is
+// the bounding box of the triangle clipped to slab j (fp64, then padded and
+// rounded outward like every other box).  The pieces' boxes cover the
+// triangle, every piece's leaf record is the WHOLE triangle (same fp64
+// record, same id), so closest hits and any-hit answers are unchanged: a
+// duplicate test returns the identical (t, id) and never replaces the best
+// hit.  Criterion: box surface area > kEscRatio x twice the triangle's area;
+// k = ceil(ratio / kEscTarget) <= kEscMaxPieces.  Well-shaped meshes (the
+// icospheres, the dihedral plates) have ratios <= ~5 and are not split.
+constexpr double kEscRatio = 16.0;
+constexpr double kEscTarget = 4.0;
+constexpr uint32_t kEscMaxPieces = 64;
+
+struct EscInfo {
+    uint32_t pieces;
+    int axis;
+    double lo, hi;  // the triangle's extent along `axis`
+};
+
+__device__ __forceinline__ EscInfo esc_info(const double* a, const double* b, const double* c) {
+    double lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = fmin(a[k], fmin(b[k], c[k]));
+        hi[k] = fmax(a[k], fmax(b[k], c[k]));
+    }
+    const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+    const double sa = 2.0 * (dx * dy + dy * dz + dz * dx);
+    const double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    const double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+    const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
+                 cz = e1[0] * e2[1] - e1[1] * e2[0];
+    const double a2 = sqrt(cx * cx + cy * cy + cz * cz);  // twice the area
+    EscInfo r;
+    r.axis = dx >= dy && dx >= dz ? 0 : (dy >= dz ? 1 : 2);
+    r.lo = lo[r.axis];
+    r.hi = hi[r.axis];
+    r.pieces = 1;
+    if (a2 > 0.0 && sa > kEscRatio * a2)
+        r.pieces = static_cast<uint32_t>(fmin(ceil(sa / (kEscTarget * a2)), static_cast<double>(kEscMaxPieces)));
+    return r;
+}
+
+__global__ void esc_count_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri, uint32_t n,
+                                 uint32_t* __restrict__ extra) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4 t = tri[i];
+    extra[i] = esc_info(vtx + 3ull * t.x, vtx + 3ull * t.y, vtx + 3ull * t.z).pieces - 1;
+}
+
+// reference r -> (triangle, piece): piece 0 of triangle t is reference t,
+// pieces 1.. follow after the n triangles at the scanned offsets
+__global__ void esc_refs_kernel(const uint32_t* __restrict__ extra, const uint32_t* __restrict__ off, uint32_t n,
+                                uint32_t* __restrict__ ref_tri, uint32_t* __restrict__ ref_piece) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ref_tri[i] = i;
+    ref_piece[i] = 0;
+    for (uint32_t j = 1; j <= extra[i]; ++j) {
+        ref_tri[n + off[i] + j - 1] = i;
+        ref_piece[n + off[i] + j - 1] = j;
+    }
+}
+
+// bounding box of the triangle (a, b, c) clipped to lo_s <= p[axis] <= hi_s
+// (Sutherland-Hodgman against the two planes)
+__device__ void clip_box(const double* a, const double* b, const double* c, int axis, double lo_s, double hi_s,
+                         double bl[3], double bh[3]) {
+    double P[8][3], Q[8][3];
+    int n = 3;
+    for (int k = 0; k < 3; ++k) {
+        P[0][k] = a[k];
+        P[1][k] = b[k];
+        P[2][k] = c[k];
+    }
+    for (int side = 0; side < 2; ++side) {
+        const double s = side ? hi_s : lo_s;
+        int m = 0;
+        for (int i = 0; i < n; ++i) {
+            const double* u = P[i];
+            const double* v = P[(i + 1) % n];
+            const bool ui = side ? u[axis] <= s : u[axis] >= s;
+            const bool vi = side ? v[axis] <= s : v[axis] >= s;
+            if (ui) {
+                for (int k = 0; k < 3; ++k) Q[m][k] = u[k];
+                ++m;
+            }
+            if (ui != vi) {
+                const double w = (s - u[axis]) / (v[axis] - u[axis]);
+                for (int k = 0; k < 3; ++k) Q[m][k] = u[k] + (v[k] - u[k]) * w;
+                Q[m][axis] = s;
+                ++m;
+            }
+        }
+        n = m;
+        for (int i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) P[i][k] = Q[i][k];
+    }
+    for (int k = 0; k < 3; ++k) {
+        bl[k] = 1e300;
+        bh[k] = -1e300;
+    }
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            bl[k] = fmin(bl[k], P[i][k]);
+            bh[k] = fmax(bh[k], P[i][k]);
+        }
+    if (n == 0) {  // rounding left nothing: the slab of the triangle's box (conservative)
+        for (int k = 0; k < 3; ++k) {
+            bl[k] = fmin(a[k], fmin(b[k], c[k]));
+            bh[k] = fmax(a[k], fmax(b[k], c[k]));
+        }
+        bl[axis] = lo_s;
+        bh[axis] = hi_s;
+    }
+}
+
+__global__ void prim_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri,
+                            const uint32_t* __restrict__ ref_tri, const uint32_t* __restrict__ ref_piece,
+                            uint32_t n,
                             double lox, double loy, double loz, double sx, double sy, double sz,
                             double cx, double cy, double cz, double pad, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
                             float4* __restrict__ box_lo, float4* __restrict__ box_hi) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint4 t = tri[i];
+    const uint4 t = tri[ref_tri ? ref_tri[i] : i];
     const double* a = vtx + 3ull * t.x;
     const double* b = vtx + 3ull * t.y;
     const double* c = vtx + 3ull * t.z;
+    double mn[3], mx[3], cen[3];
+    const EscInfo esc = ref_tri ? esc_info(a, b, c) : EscInfo{1, 0, 0.0, 0.0};
+    if (esc.pieces > 1) {
+        const uint32_t j = ref_piece[i];
+        const double w = esc.hi - esc.lo;
+        const double lo_s = j == 0 ? esc.lo : esc.lo + w * (static_cast<double>(j) / esc.pieces);
+        const double hi_s = j + 1 == esc.pieces ? esc.hi : esc.lo + w * (static_cast<double>(j + 1) / esc.pieces);
+        clip_box(a, b, c, esc.axis, lo_s, hi_s, mn, mx);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) cen[k] = 0.5 * (mn[k] + mx[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mn[k] = fmin(a[k], fmin(b[k], c[k]));
+            mx[k] = fmax(a[k], fmax(b[k], c[k]));
+            cen[k] = (a[k] + b[k] + c[k]) * (1.0 / 3.0);
+        }
+    }
     float lo[3], hi[3];
-    double cen[3];
     const double ctr[3] = {cx, cy, cz};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double mn = fmin(a[k], fmin(b[k], c[k]));
-        const double mx = fmax(a[k], fmax(b[k], c[k]));
-        lo[k] = __double2float_rd((mn - ctr[k]) - pad);
-        hi[k] = __double2float_ru((mx - ctr[k]) + pad);
-        cen[k] = (a[k] + b[k] + c[k]) * (1.0 / 3.0);
+        lo[k] = __double2float_rd((mn[k] - ctr[k]) - pad);
+        hi[k] = __double2float_ru((mx[k] - ctr[k]) + pad);
     }
     box_lo[i] = make_float4(lo[0], lo[1], lo[2], 0.f);
     box_hi[i] = make_float4(hi[0], hi[1], hi[2], 0.f);
@@ -178,10 +316,11 @@ __global__ void emit_kernel(int n, const int2* __restrict__ child, const int2* _
 }
 
 __global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri,
-                           const uint32_t* __restrict__ order, uint32_t n, double2* __restrict__ out) {
+                           const uint32_t* __restrict__ order, const uint32_t* __restrict__ ref_tri, uint32_t n,
+                           double2* __restrict__ out) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const uint32_t id = order[k];
+    const uint32_t id = ref_tri ? ref_tri[order[k]] : order[k];
     const uint4 t = tri[id];
     const double* a = vtx + 3ull * t.x;
     const double* b = vtx + 3ull * t.y;
@@ -834,11 +973,67 @@ __global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
         }                                     \
     } while (0)
 
+// Early split clipping references (see esc_info): on success *n_refs is the
+// number of BVH primitives and, if any triangle is split, *ref_tri /
+// *ref_piece map each reference to its triangle and piece (else nullptr:
+// reference i is triangle i).
+static cudaError_t esc_references(const double* d_vertices, const uint4* d_tri_idx, uint32_t n_tri,
+                                  cudaStream_t stream, uint32_t* n_refs, uint32_t** ref_tri, uint32_t** ref_piece) {
+    *n_refs = n_tri;
+    *ref_tri = *ref_piece = nullptr;
+    if (std::getenv("MCSBR_ESC") && std::strcmp(std::getenv("MCSBR_ESC"), "0") == 0) return cudaSuccess;  // A/B
+    uint32_t *extra = nullptr, *off = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    uint32_t last[2] = {0, 0};
+    cudaError_t e = dev_malloc(&extra, sizeof(uint32_t) * n_tri);
+    if (e == cudaSuccess) e = dev_malloc(&off, sizeof(uint32_t) * n_tri);
+    if (e == cudaSuccess) {
+        esc_count_kernel<<<(n_tri + 255) / 256, 256, 0, stream>>>(d_vertices, d_tri_idx, n_tri, extra);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, extra, off, n_tri, stream);
+    if (e == cudaSuccess) e = dev_malloc(&tmp, tmp_bytes);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, extra, off, n_tri, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&last[0], off + (n_tri - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&last[1], extra + (n_tri - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    const uint64_t total = static_cast<uint64_t>(last[0]) + last[1];
+    if (e == cudaSuccess && total > 0 && n_tri + total < (uint64_t{1} << 28)) {
+        const uint32_t n = n_tri + static_cast<uint32_t>(total);
+        e = dev_malloc(ref_tri, sizeof(uint32_t) * n);
+        if (e == cudaSuccess) e = dev_malloc(ref_piece, sizeof(uint32_t) * n);
+        if (e == cudaSuccess) {
+            esc_refs_kernel<<<(n_tri + 255) / 256, 256, 0, stream>>>(extra, off, n_tri, *ref_tri, *ref_piece);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) {
+            *n_refs = n;
+        } else {
+            dev_free(*ref_tri);
+            dev_free(*ref_piece);
+            *ref_tri = *ref_piece = nullptr;
+        }
+    }
+    dev_free(extra);
+    dev_free(off);
+    dev_free(tmp);
+    return e;
+}
+
 cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t n_tri,
                       const double scene_lo[3], const double scene_hi[3], const double center[3],
                       double box_pad, cudaStream_t stream, BvhBuildOut* out) {
+    uint32_t n_refs = n_tri;
+    uint32_t *ref_tri = nullptr, *ref_piece = nullptr;
+    {
+        const cudaError_t e = esc_references(d_vertices, d_tri_idx, n_tri, stream, &n_refs, &ref_tri, &ref_piece);
+        if (e != cudaSuccess) return e;
+    }
     cudaError_t err = cudaSuccess;
-    const int n = static_cast<int>(n_tri);
+    const int n = static_cast<int>(n_refs);
     uint64_t *keys = nullptr, *keys_s = nullptr;
     uint32_t *ids = nullptr, *ids_s = nullptr;
     float4 *blo = nullptr, *bhi = nullptr, *blo_s = nullptr, *bhi_s = nullptr;
@@ -893,7 +1088,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     BVH_CHECK(cudaMemsetAsync(par_i, 0xff, sizeof(int) * inner, stream));  // root parent = -1
     BVH_CHECK(cudaMemsetAsync(par_l, 0xff, sizeof(int) * n, stream));
 
-    prim_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, n_tri, scene_lo[0], scene_lo[1], scene_lo[2],
+    prim_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, ref_tri, ref_piece, n_refs, scene_lo[0], scene_lo[1], scene_lo[2],
                                      s[0], s[1], s[2], center[0], center[1], center[2], box_pad, keys,
                                      ids, blo, bhi);
     BVH_CHECK(cudaGetLastError());
@@ -962,7 +1157,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
             BVH_CHECK(cudaGetLastError());
         }
     }
-    tri_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, order, n_tri, out->tri64);
+    tri_kernel<<<G, B, 0, stream>>>(d_vertices, d_tri_idx, order, ref_tri, n_refs, out->tri64);
     BVH_CHECK(cudaGetLastError());
     if (n > 1) {
         gather_boxes<<<G, B, 0, stream>>>(blo, bhi, order, n, blo_s, bhi_s);
@@ -996,12 +1191,14 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         out->max_depth = md;
         out->n_nodes = last[0] + last[1];
         out->root_ref = n <= kLeafMax ? ~(0 << 3 | n) : 0;
-        out->n_leaves = n_tri;
+        out->n_leaves = n_refs;  // leaf references (> n_tri when slivers were split)
         float ms = 0.f;
         BVH_CHECK(cudaEventElapsedTime(&ms, e0, e1));
         out->build_ms = ms;
     }
 done:
+    dev_free(ref_tri);
+    dev_free(ref_piece);
     dev_free(keys);
     dev_free(keys_s);
     dev_free(ids);

@@ -122,6 +122,39 @@ constexpr double kPi = 3.14159265358979323846;
 thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
 
+// Per-kernel device timing (mcsbr_gpu_kernel_timing): while enabled, run_job
+// brackets every path-kernel and accumulate launch with CUDA events on the
+// launch stream; mcsbr_gpu_kernel_times sums them.  Events are pooled per
+// thread and device.
+struct KernelTiming {
+    bool on = false;
+    int device = -1;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<int, size_t>> marks;  // (kind 0 path / 1 accumulate, first event index)
+};
+thread_local KernelTiming g_kt;
+
+// record the start (end = false) or end event of one timed launch
+cudaError_t kt_mark(int kind, cudaStream_t stream, int device, bool end) {
+    if (!g_kt.on) return cudaSuccess;
+    if (g_kt.device != device) {
+        for (cudaEvent_t e : g_kt.pool) cudaEventDestroy(e);
+        g_kt.pool.clear();
+        g_kt.used = 0;
+        g_kt.marks.clear();
+        g_kt.device = device;
+    }
+    if (g_kt.used == g_kt.pool.size()) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) return r;
+        g_kt.pool.push_back(e);
+    }
+    if (!end) g_kt.marks.emplace_back(kind, g_kt.used);
+    return cudaEventRecord(g_kt.pool[g_kt.used++], stream);
+}
+
 int set_err(int code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -200,6 +233,7 @@ struct mcsbr_scene {
     bool peak_pending = false;
     double* d_nim = nullptr;
     double* d_vtx = nullptr;
+    float* d_tri32 = nullptr;  // fp32 vertices relative to the centre, 9 per triangle (cover.cu)
     uint4* d_tri = nullptr;
     double2* d_info = nullptr;
     double2* d_mat = nullptr;
@@ -212,6 +246,7 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> counters;
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
+    DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     SceneView view() const {
@@ -337,6 +372,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 
 constexpr uint64_t kPathStateBytes = 192;
 constexpr uint64_t kRecCapMax = uint64_t{1} << 25;  // contribution records (96 B each): 3.2 GB
+constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: at most 256 MB per job
 
 // Fold the peak record count of the scene's previous F > 1 job (if its
 // readback has landed) into the records-per-entry estimate.
@@ -525,7 +561,29 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         rec_cap = env_u32("MCSBR_REC_CAP", static_cast<uint32_t>(rec_cap));
         CK(s->recs.reserve(rec_cap * 12), "dev_malloc(contribution records)");
     }
-    CK(cudaMemcpyAsync(s->inc.p, job.inc.data(), sizeof(IncDev) * job.inc.size(), cudaMemcpyHostToDevice,
+    // launch-ray coverage bitmaps (cover.cu): every incidence of the job,
+    // up to kCoverBudget words in total (later incidences go unculled); the
+    // deterministic solver's per-root stack accounting needs every root ray,
+    // so its jobs are not culled
+    std::vector<IncDev> incs = job.inc;
+    const bool det_job = extra && extra->det;
+    const bool cull = !det_job && env_u32("MCSBR_COVER", 1) != 0;
+    uint64_t cover_words = 0;
+    for (IncDev& d : incs) {
+        d.cover_off = kNoCover;
+        d.cover_shift = 0;
+        if (!cull) continue;
+        const uint64_t entries = static_cast<uint64_t>(d.nu) * static_cast<uint64_t>(d.nv) *
+                                 static_cast<uint64_t>(cfg->samples_per_stratum);
+        const uint32_t sh = cover_shift_for(entries);
+        const uint64_t words = (((entries + (uint64_t{1} << sh) - 1) >> sh) + 31) / 32;
+        if (cover_words + words > kCoverBudgetWords) continue;
+        d.cover_off = cover_words;
+        d.cover_shift = sh;
+        cover_words += words;
+    }
+    if (cover_words) CK(s->cover.reserve(cover_words), "dev_malloc(coverage bitmaps)");
+    CK(cudaMemcpyAsync(s->inc.p, incs.data(), sizeof(IncDev) * incs.size(), cudaMemcpyHostToDevice,
                        stream), "upload incidences");
     CK(cudaMemcpyAsync(s->rx.p, job.rx.data(), sizeof(RxDev) * job.rx.size(), cudaMemcpyHostToDevice, stream),
        "upload receivers");
@@ -533,6 +591,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
        "upload wavenumbers");
     TraceParams p = extra ? *extra : TraceParams{};
     p.scene = s->view();
+    p.cover = cover_words ? s->cover.p : nullptr;
     p.n_rx = job.n_rx;
     p.k0 = s->k0.p;
     p.nf = nf;
@@ -573,6 +632,12 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     const uint32_t step = fan ? 32u : 1u;
     p.fan = fan ? 1 : 0;
     if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
+    if (cover_words) {
+        CK(launch_cover(s->inc.p, static_cast<uint32_t>(incs.size()), s->d_tri32, s->nt, s->center, s->radius,
+                        p.spp, static_cast<uint32_t>(p.band_order), s->cover.p, stream),
+           "coverage kernel launch");
+        ++g_launches;
+    }
     for (uint32_t r = 0; r < job.n_rx; r += step) {
         p.rx_index = r;
         for (const Job::Group& gr : job.groups) {
@@ -583,8 +648,14 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
             p.sums = d_sums + static_cast<size_t>(gr.a0) * job.n_rx * nf * 8;
             p.total_entries = gr.entries;
             CK(cudaMemsetAsync(s->tile.p, 0, 2 * sizeof(unsigned long long), stream), "reset tile counter");
+            CK(kt_mark(0, stream, s->device, false), "cudaEventRecord");
             CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
-            if (defer) CK(launch_accumulate(p, s->sms, stream, &g_launches), "accumulate launch");
+            CK(kt_mark(0, stream, s->device, true), "cudaEventRecord");
+            if (defer) {
+                CK(kt_mark(1, stream, s->device, false), "cudaEventRecord");
+                CK(launch_accumulate(p, s->sms, stream, &g_launches), "accumulate launch");
+                CK(kt_mark(1, stream, s->device, true), "cudaEventRecord");
+            }
         }
     }
     if (defer && s->peak_host) {  // learn the record ratio for the next job
@@ -609,6 +680,7 @@ void decode(const unsigned long long* c, mcsbr_stats* st) {
     st->grazing_kills = c[kCntGrazing];
     st->cap_kills = c[kCntCap];
     st->occlusion_queries = c[kCntOcclusion];
+    st->culled_launch_rays = c[kCntCulled];
     uint32_t rounds = 0;
     uint64_t seg = 0;
     for (int i = 0; i < MCSBR_MAX_BOUNCE_LIMIT; ++i) {
@@ -663,6 +735,30 @@ const char* mcsbr_gpu_last_error(void) { return g_err.c_str(); }
 void mcsbr_gpu_internal_set_error(const char* msg) { g_err = msg; }  // imaging.cu (not exported)
 int mcsbr_gpu_abi_version(void) { return MCSBR_GPU_ABI_VERSION; }
 uint64_t mcsbr_gpu_last_launch_count(void) { return g_launches; }
+
+void mcsbr_gpu_kernel_timing(int enable) {
+    g_kt.on = enable != 0;
+    g_kt.used = 0;
+    g_kt.marks.clear();
+}
+
+int mcsbr_gpu_kernel_times(double* path_ms, uint64_t* path_launches, double* acc_ms, uint64_t* acc_launches) {
+    double t[2] = {0.0, 0.0};
+    uint64_t n[2] = {0, 0};
+    if (g_kt.device >= 0) CK(cudaSetDevice(g_kt.device), "cudaSetDevice");
+    for (const auto& m : g_kt.marks) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(g_kt.pool[m.second + 1]), "cudaEventSynchronize");
+        CK(cudaEventElapsedTime(&ms, g_kt.pool[m.second], g_kt.pool[m.second + 1]), "cudaEventElapsedTime");
+        t[m.first] += ms;
+        n[m.first] += 1;
+    }
+    if (path_ms) *path_ms = t[0];
+    if (path_launches) *path_launches = n[0];
+    if (acc_ms) *acc_ms = t[1];
+    if (acc_launches) *acc_launches = n[1];
+    return MCSBR_OK;
+}
 
 void mcsbr_gpu_default_config(mcsbr_mc_config* c) {
     std::memset(c, 0, sizeof(*c));
@@ -816,6 +912,10 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
         return fail(e, "BVH build");
     g_launches += 7;
+    if ((e = dev_malloc(&s->d_tri32, sizeof(float) * 9 * nt)) != cudaSuccess) return fail(e, "dev_malloc(tri32)");
+    if ((e = build_tri32(s->d_vtx, s->d_tri, nt, s->center, s->d_tri32, s->stream)) != cudaSuccess)
+        return fail(e, "fp32 triangle copy");
+    ++g_launches;
     // a 4-wide level pushes at most 3 refs; BVH4 depth <= ceil(binary depth / 2) + 1
     if (3 * ((s->bvh.max_depth + 1) / 2 + 1) > static_cast<uint32_t>(kStackSize)) {
         mcsbr_gpu_scene_destroy(s);
@@ -834,6 +934,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     dev_free(s->d_info);
     dev_free(s->d_mat);
     dev_free(s->d_nim);
+    dev_free(s->d_tri32);
     dev_free(s->bvh.nodes);
     dev_free(s->bvh.tri64);
     s->inc.release();
@@ -843,6 +944,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->counters.release();
     s->tile.release();
     s->recs.release();
+    s->cover.release();
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->peak_ev) cudaEventDestroy(s->peak_ev);
     if (s->peak_host) cudaFreeHost(s->peak_host);

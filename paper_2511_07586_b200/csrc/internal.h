@@ -61,8 +61,12 @@ struct IncDev {
     uint64_t entry_begin;     // this shard's entry range [begin, end)
     uint64_t entry_end;
     uint64_t g_begin;         // index of entry_begin in the job's flattened entry space
-    uint64_t _pad;
+    uint64_t cover_off;       // launch-ray coverage bitmap (cover.cu): first word, kNoCover = none
+    uint32_t cover_shift;     // log2 of the launch entries per coverage bit
+    uint32_t _pad;
 };
+constexpr uint64_t kNoCover = ~uint64_t{0};
+constexpr uint64_t kCoverMaxBits = uint64_t{1} << 19;  // 64 KB of shared memory per incidence
 
 struct RxDev {
     double k_s[3], rx_v[3], rx_h[3];
@@ -81,6 +85,7 @@ enum : int {
     kCntRaysPerBounce = 8,
     kCntRouletteCand = 72,
     kCntRouletteSurv = 136,
+    kCntCulled = 200,  // launch entries retired by the coverage bitmap (provable bounce-0 misses)
     kCntWords = 256,
 };
 
@@ -97,6 +102,7 @@ struct TraceParams {
     uint32_t nf;
     int occlusion;
     double* sums;           // [n_inc][n_rx][nf][4] complex (re, im)
+    const uint32_t* cover;  // launch-ray coverage bitmaps (IncDev::cover_off), or nullptr
     // deferred accumulation (F > 1): contribution records of this launch
     double* recs;                      // [rec_cap][12]: amp[4], s (re, im), incidence
     unsigned long long* rec_count;
@@ -176,6 +182,14 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                       const double scene_lo[3], const double scene_hi[3], const double center[3],
                       double box_pad,
                       cudaStream_t stream, BvhBuildOut* out);
+
+// cover.cu: launch-ray coverage bitmaps
+cudaError_t build_tri32(const double* d_vtx, const uint4* d_tri, uint32_t n, const double center[3], float* out,
+                        cudaStream_t stream);
+uint32_t cover_shift_for(uint64_t entries);
+cudaError_t launch_cover(const IncDev* d_inc, uint32_t n_inc, const float* tri32, uint32_t n_tri,
+                         const double center[3], double radius, uint32_t spp, uint32_t band, uint32_t* out,
+                         cudaStream_t stream);
 
 // trace.cu
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream,

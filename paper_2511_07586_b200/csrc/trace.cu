@@ -213,9 +213,10 @@ __device__ __forceinline__ bool tri_test(const double2* __restrict__ rec, V3 o, 
 // One runtime-flagged routine (not two template copies) so the path kernel
 // has a single traversal loop in its instruction stream.
 #ifdef MCSBR_TRAVERSAL_STATS
-// diagnostic build only (tools/build_variants.py --stats): per-thread node-visit
-// and triangle-test counts, flushed into counter words 240/241
-__device__ unsigned long long g_visits[2];
+// diagnostic build only (tools/build_variants.py --stats): node visits,
+// triangle tests and queries per query kind (0 launch rays, 1 surface
+// closest-hit rays, 2 occlusion rays) in g_visits[3 * kind + {0, 1, 2}]
+__device__ unsigned long long g_visits[9];
 #define MCSBR_STAT(i) (++tstat[i])
 #else
 #define MCSBR_STAT(i) ((void)0)
@@ -227,11 +228,13 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
     uint32_t tstat[2] = {0, 0};
     struct Flush {
         uint32_t* s;
+        int kind;
         __device__ ~Flush() {
-            atomicAdd(&g_visits[0], static_cast<unsigned long long>(s[0]));
-            atomicAdd(&g_visits[1], static_cast<unsigned long long>(s[1]));
+            atomicAdd(&g_visits[3 * kind], static_cast<unsigned long long>(s[0]));
+            atomicAdd(&g_visits[3 * kind + 1], static_cast<unsigned long long>(s[1]));
+            atomicAdd(&g_visits[3 * kind + 2], 1ull);
         }
-    } flush_{tstat};
+    } flush_{tstat, kAny ? 2 : (outside ? 0 : 1)};
 #endif
     const FRay r = make_fray(S, o, d, outside, t_min);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
@@ -572,6 +575,30 @@ __device__ __forceinline__ Entry locate(const TraceParams& P, const IncDev& I, u
     return e;
 }
 
+// Launch-ray culling (cover.cu): is dispatch index d of incidence I in a
+// group whose coverage bit is set?  (No bitmap: every entry is traced.)
+__device__ __forceinline__ bool covered(const TraceParams& P, const IncDev& I, uint64_t d) {
+    if (!P.cover || I.cover_off == kNoCover) return true;
+    const uint64_t g = d >> I.cover_shift;
+    return (__ldg(P.cover + I.cover_off + (g >> 5)) >> (g & 31)) & 1u;
+}
+
+// First dispatch index >= cursor (and < e_end) in a covered group, reading
+// the bitmap a word (32 groups) at a time; warp-uniform.
+__device__ __forceinline__ uint64_t skip_uncovered(const uint32_t* bits, uint32_t sh, uint64_t cursor,
+                                                   uint64_t e_end) {
+    while (cursor < e_end) {
+        const uint64_t g = cursor >> sh;
+        const uint32_t w = __ldg(bits + (g >> 5)) >> (g & 31);
+        if (w) {
+            const uint64_t ng = g + static_cast<uint64_t>(__ffs(w) - 1);
+            return ng > g ? min(ng << sh, e_end) : cursor;
+        }
+        cursor = ((g | 31ull) + 1) << sh;
+    }
+    return e_end;
+}
+
 // sample_stratum + init_path (solver_mc.cpp:33-42, :117-125; path_engine.cpp:5-15)
 template <typename NT, typename EF>
 __device__ __forceinline__ void init_path(const TraceParams& P, const IncDev& I, uint32_t inc_idx,
@@ -835,7 +862,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
     using EF = typename std::conditional<L::pec, V3, CV3>::type;  // field type
     constexpr int kFAcc = L::Acc;               // register-mode phasor sums
     constexpr int kSlotFields = L::Fields;      // doubles per thread
-    __shared__ unsigned long long s_cnt[8];  // launched .. rounds (kCntLaunched..kCntRounds)
+    __shared__ unsigned long long s_cnt[9];  // launched .. rounds (kCntLaunched..kCntRounds), culled
     // per-bounce counters as native 32-bit shared atomics (ATOMS.ADD); the
     // 64-bit shared atomicAdd is a CAS loop on sm_100 and cost ~20% of the
     // kernel.  Per block and bounce they stay far below 2^32.
@@ -843,7 +870,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
     __shared__ double s_state[kSlotFields * kSlotThreads];
     __shared__ unsigned long long s_sched[kSlotThreads / 32][4];
     __shared__ double s_rcp[kSlotThreads / 32][2];  // reciprocals of the incidence's nu, nv (init_path)
-    for (int i = threadIdx.x; i < 8; i += blockDim.x) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < 9; i += blockDim.x) s_cnt[i] = 0;
     for (int i = threadIdx.x; i < 3 * 64; i += blockDim.x) s_bounce[i] = 0;
     __syncthreads();
     const Slot sl{s_state + threadIdx.x};
@@ -853,6 +880,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
     const SceneView& S = P.scene;
     uint32_t fault = 0;
     uint64_t n_launched = 0, n_contrib = 0, n_graze = 0, n_cap = 0, n_occ = 0;
+    uint64_t n_miss0 = 0;  // culled launch entries (launched, escaped at bounce 0)
     int max_round = 0;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     mcsbr_contribution* scratch =
@@ -973,41 +1001,61 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                 alive = true;
             }
             // ---- regenerate dead lanes from the tile ----
-            const unsigned need = __ballot_sync(kFull, !alive);
-            if (need && cursor >= e_end) {
-                // sub-range dry: continue with the next chunk if it is the same incidence
-                if (q[0] >= q[1]) fetch();
-                const uint64_t n0 = q[0], n1 = q[1];
-                if (n0 < n1 && n0 >= I.g_begin && n0 < g_end_a) {
-                    cursor = I.entry_begin + (n0 - I.g_begin);
-                    e_end = I.entry_begin + (min(n1, g_end_a) - I.g_begin);
-                    __syncwarp();
-                    if (lane == 0) q[0] = min(n1, g_end_a);
-                    __syncwarp();
+            // Dead lanes take the next launch entries of the warp's sub-range
+            // (continuing into the next chunk when it is the same incidence).
+            // Entries whose coverage bit is clear provably escape (cover.cu):
+            // they are retired here as launched bounce-0 misses, without ray
+            // generation or traversal, and whole empty runs of the bitmap are
+            // skipped at once; the lanes keep drawing until they hold a path
+            // or the incidence's entries are used up.
+            unsigned need = __ballot_sync(kFull, !alive);
+            while (need) {
+                if (cursor >= e_end) {
+                    // sub-range dry: continue with the next chunk if it is the same incidence
+                    if (q[0] >= q[1]) fetch();
+                    const uint64_t n0 = q[0], n1 = q[1];
+                    if (n0 < n1 && n0 >= I.g_begin && n0 < g_end_a) {
+                        cursor = I.entry_begin + (n0 - I.g_begin);
+                        e_end = I.entry_begin + (min(n1, g_end_a) - I.g_begin);
+                        __syncwarp();
+                        if (lane == 0) q[0] = min(n1, g_end_a);
+                        __syncwarp();
+                    } else {
+                        break;
+                    }
                 }
-            }
-            if (need && cursor < e_end) {
+                if (!kDet && P.cover && I.cover_off != kNoCover) {
+                    const uint64_t c2 = skip_uncovered(P.cover + I.cover_off, I.cover_shift, cursor, e_end);
+                    if (lane == 0) n_miss0 += c2 - cursor;  // warp-uniform run, counted once
+                    cursor = c2;
+                    if (cursor >= e_end) continue;
+                }
                 const unsigned rank = __popc(need & ((1u << lane) - 1u));
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
-                    init_path(P, I, a + P.inc_base, locate(P, I, mine), s, s_rcp[warp]);
-                    save_em<L>(sl, s);
-                    alive = true;
-                    ++n_launched;
-                    if (kDet) {  // a new root ray (solver_det.cpp:72-82)
-                        const uint64_t blk = s.cell / P.det_block_size;
-                        dacc_peak += dpeak;
-                        if (blk != dblk) {
-                            det_flush(P, dblk, dacc_peak, dacc_push);
-                            dacc_peak = dacc_push = 0;
-                            dblk = blk;
+                    if (!kDet && !covered(P, I, mine)) {
+                        ++n_miss0;  // provable miss: one launched ray, one bounce-0 segment
+                    } else {
+                        init_path(P, I, a + P.inc_base, locate(P, I, mine), s, s_rcp[warp]);
+                        save_em<L>(sl, s);
+                        alive = true;
+                        ++n_launched;
+                        if (kDet) {  // a new root ray (solver_det.cpp:72-82)
+                            const uint64_t blk = s.cell / P.det_block_size;
+                            dacc_peak += dpeak;
+                            if (blk != dblk) {
+                                det_flush(P, dblk, dacc_peak, dacc_push);
+                                dacc_peak = dacc_push = 0;
+                                dblk = blk;
+                            }
+                            dpeak = 1;
+                            dacc_push += 1;
+                            dev = 0;
                         }
-                        dpeak = 1;
-                        dacc_push += 1;
-                        dev = 0;
                     }
                 }
                 cursor = min(cursor + static_cast<uint64_t>(__popc(need)), e_end);
+                need = __ballot_sync(kFull, !alive);
             }
             if (!__any_sync(kFull, alive)) break;
 
@@ -1389,7 +1437,9 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
         return v;
     };
-    n_launched = wsum(n_launched);
+    if (!kDet && n_miss0) atomicAdd(&s_bounce[0], static_cast<unsigned int>(n_miss0));
+    n_launched = wsum(n_launched + n_miss0);
+    n_miss0 = wsum(n_miss0);
     n_contrib = wsum(n_contrib);
     n_graze = wsum(n_graze);
     n_cap = wsum(n_cap);
@@ -1404,16 +1454,17 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
         atomicAdd(&s_cnt[kCntOcclusion], n_occ);
         atomicOr(&s_cnt[kCntFault], static_cast<unsigned long long>(fault_w));
         atomicMax(&s_cnt[kCntRounds], static_cast<unsigned long long>(round_w));
+        atomicAdd(&s_cnt[8], n_miss0);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 8 + 3 * 64; i += blockDim.x) {
+    for (int i = threadIdx.x; i < 9 + 3 * 64; i += blockDim.x) {
         unsigned long long v;
         int dst;
-        if (i < 8) {
+        if (i < 9) {
             v = s_cnt[i];
-            dst = i;
+            dst = i < 8 ? i : kCntCulled;
         } else {
-            const int j = i - 8;
+            const int j = i - 9;
             v = s_bounce[j];
             dst = j < 64 ? kCntRaysPerBounce + j : (j < 128 ? kCntRouletteCand + j - 64 : kCntRouletteSurv + j - 128);
         }
@@ -1632,8 +1683,9 @@ cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stre
     if (const char* v = std::getenv("MCSBR_EXTRA_SMEM")) smem += std::strtoul(v, nullptr, 10);  // A/B only
     // three physics instantiations: all-PEC (dielectric code compiled out),
     // the reference's lossless dielectric model (bit-exact), lossy media
+    static const bool force_diel = std::getenv("MCSBR_FORCE_DIEL") != nullptr;  // A/B only
     cudaError_t e = p.scene.lossy     ? launch_kind<true, true>(mode, p, device_sms, threads, smem, stream)
-                    : p.scene.all_pec ? launch_kind<false, false>(mode, p, device_sms, threads, smem, stream)
+                    : (p.scene.all_pec && !force_diel) ? launch_kind<false, false>(mode, p, device_sms, threads, smem, stream)
                                       : launch_kind<true, false>(mode, p, device_sms, threads, smem, stream);
     if (launches) ++*launches;
     return e;

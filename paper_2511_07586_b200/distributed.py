@@ -46,12 +46,22 @@ def allreduce_finalize(sums, counters, freqs, n: int, group=None):
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        fault = counters[6:7].clone()
-        counters[6] = 0
+        # word 6 holds fault BITS (atomicOr on the device) and word 7 the
+        # deepest bounce round (atomicMax): they are combined with a bitwise
+        # OR and a max over ranks; everything else is a sum
+        special = counters[6:8].clone()
+        counters[6:8] = 0
         dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(counters, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(fault, op=dist.ReduceOp.MAX, group=group)
-        counters[6] = fault[0]
+        world = dist.get_world_size(group)
+        gathered = [torch.zeros_like(special) for _ in range(world)]
+        dist.all_gather(gathered, special, group=group)
+        fault, rounds = 0, 0
+        for g in gathered:
+            fault |= int(g[0].item())
+            rounds = max(rounds, int(g[1].item()))
+        counters[6] = fault
+        counters[7] = rounds
     freqs = np.ascontiguousarray(np.asarray(freqs, dtype=np.float64).reshape(-1))
     nf = len(freqs)
     raw = np.ascontiguousarray(sums.detach().to("cpu", torch.float64).numpy())

@@ -226,6 +226,7 @@ class RunStats:
     kernel_ms: float = 0.0
     forced_stack_bytes: int = 0
     device_stack_bytes: int = 0
+    culled_launch_rays: int = 0
 
     @staticmethod
     def from_c(st: A.Stats) -> "RunStats":
@@ -242,6 +243,7 @@ class RunStats:
             state_bytes_per_ray=st.state_bytes_per_ray, block_size=st.block_size,
             wall_ms=st.wall_ms, kernel_ms=st.kernel_ms,
             forced_stack_bytes=st.forced_stack_bytes, device_stack_bytes=st.device_stack_bytes,
+            culled_launch_rays=st.culled_launch_rays,
         )
 
 

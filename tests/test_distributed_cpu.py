@@ -87,3 +87,39 @@ def test_two_rank_gloo_reduction_matches_single_process(tmp_path):
     assert np.max(np.abs(got - ref["values"])) <= 1e-12 * scale
     st = ref["stats"]
     assert list(cnt) == [st.rays_launched, st.contributions, st.cap_kills, st.segments_traced]
+
+
+def _fault_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sums = torch.zeros(8, dtype=torch.float64)
+        counters = torch.zeros(256, dtype=torch.int64)
+        counters[0] = 10 + rank
+        counters[6] = 1 << rank        # rank 0: fresnel domain, rank 1: non-transverse field
+        counters[7] = 3 + 2 * rank     # deepest round seen: 3 and 5
+        msg = ""
+        try:
+            D.allreduce_finalize(sums, counters, [1e9], 1)
+        except Exception as e:  # noqa: BLE001 - the EDEVICE error is the point
+            msg = str(e)
+        if rank == 0:
+            np.save(out, np.array([int(counters[0]), int(counters[6]), int(counters[7])]))
+            with open(out + ".msg", "w") as f:
+                f.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_fault_bits_are_ored_and_rounds_max_reduced(tmp_path):
+    """the fault word carries bit flags (device atomicOr) and word 7
+    the deepest bounce round (atomicMax); ranks raising different faults must
+    all be reported, and the round count must not be summed."""
+    out = str(tmp_path / "cnt.npy")
+    mp.spawn(_fault_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    launched, fault, rounds = np.load(out)
+    assert launched == 21 and fault == 3 and rounds == 5
+    msg = open(out + ".msg").read()
+    assert "fresnel" in msg and "transverse" in msg, msg

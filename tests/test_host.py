@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
 def test_library_cpu_entry_points():
     """Host-only entry points work without a device; compute ones fail loudly."""
     L = A.lib()
-    assert L.mcsbr_gpu_abi_version() == 2
+    assert L.mcsbr_gpu_abi_version() == 3
     det = A.DetConfigC()
     L.mcsbr_gpu_default_det_config(C.byref(det))
     assert (det.rays_per_wavelength, det.max_bounce, det.amplitude_cutoff, det.block_size) == (20.0, 9, 0.0, 8192)

@@ -16,14 +16,15 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2511_07586_b200 as M  # noqa: E402
 
-sd, excs = bench.workload(M)
+W = bench.WORKLOADS['c2']
+sd, excs = W.scene_fn(), W.excs_fn()
 scene = M.Scene(sd)
-lam = bench.C0 / bench.FREQ
-spws = [bench.spw_for(M, scene, e, lam) for e in excs]
-cfg = bench.config(M)
+lam = bench.C0 / W.freqs[-1]
+spws = [bench.spw_for(M, scene, e, lam, W.rays) for e in excs]
+cfg = W.config(M)
 inc = list(zip(excs, spws))
 rx = [[e] for e in excs]
-freqs = np.array([bench.FREQ])
+freqs = W.freqs
 for k in range(4):
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -1,0 +1,112 @@
+"""Per-region stall samples / instructions of the path kernel from an ncu report.
+
+    python tools/ncu_regions.py <rep.ncu-rep> <kernel-mangled-substring> [cubin]
+
+Maps every SASS instruction (ncu --page source --print-source sass) to the
+nearest preceding trace.cu source line in `nvdisasm -gi` of the same kernel
+(inlined dmath / rng / physics code is attributed to the trace.cu line that
+called it), then sums samples and executed instructions per trace.cu region.
+"""
+import csv
+import io
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rep, kern = sys.argv[1], sys.argv[2]
+cubin = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "-" else None
+if cubin is None:
+    os.makedirs("/tmp/ncu_regions", exist_ok=True)
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_2511_07586_b200/csrc/trace.o")],
+                   cwd="/tmp/ncu_regions", capture_output=True)
+    cubin = "/tmp/ncu_regions/trace.sm_100a.cubin"
+sass = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True).stdout
+# the kernel's text section
+start = None
+lines = sass.splitlines()
+for i, l in enumerate(lines):
+    if l.startswith(".text.") and kern in l and l.endswith(":"):
+        start = i
+        break
+assert start is not None, "kernel not found"
+ctx_line = {}  # offset -> (file, line, trace_line)
+cur_file, cur_line, trace_line = None, None, 0
+for l in lines[start + 1:]:
+    if l.startswith(".text.") or l.startswith("//---------------------"):
+        break
+    m = re.match(r'\s*//## File "([^"]+)", line (\d+)', l)
+    if m:
+        cur_file, cur_line = os.path.basename(m.group(1)), int(m.group(2))
+        if cur_file == "trace.cu":
+            trace_line = cur_line
+        continue
+    m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
+    if m:
+        ctx_line[int(m.group(1), 16)] = (cur_file, cur_line, trace_line)
+
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[1]
+ai, si, ii = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
+data = [(int(r[ai], 16), int(r[si] or 0), int(r[ii] or 0)) for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")]
+base = min(a for a, _, _ in data)
+
+# regions: each starts at the first trace.cu line containing its marker and
+# runs to the next region's start (markers in file order)
+MARKERS = [
+    ("helpers", "constexpr unsigned kFull"), ("make_fray", "FRay make_fray("), ("minmax/ffma2", "float fmin3("),
+    ("tri_test", "bool tri_test("), ("traverse", "bool traverse("), ("fill_hit", "HitInfo<NT> fill_hit("),
+    ("slot/state", "struct Path {"), ("locate", "Entry locate("), ("cover", "bool covered("),
+    ("init_path", "void init_path("), ("project", "void project("), ("det helpers", "det_at("),
+    ("flush_sums", "void flush_sums("), ("freq_phasor", "Cx freq_phasor("), ("kernel setup", "path_kernel(TraceParams P)"),
+    ("next sub-range", "// ---- next sub-range"), ("regen", "// ---- regenerate dead lanes"),
+    ("query", "double t = 0.0;"), ("pend/visible", "bool visible = false;"), ("shading", "load_em<L>(sl, s, S.ambient_n);"),
+    ("chi/queue", "// ---- chi visibility"), ("accumulate/records", "// ---- bistatic fan"),
+    ("counters", "// ---- counters ----"), ("accumulate_kernel", "accumulate_kernel(TraceParams P"),
+]
+src = open(os.path.join(ROOT, "paper_2511_07586_b200/csrc/trace.cu")).read().splitlines()
+REGIONS = []
+starts = []
+for name, mk in MARKERS:
+    ln = next((i + 1 for i, l in enumerate(src) if mk in l), None)
+    if ln is not None:
+        starts.append((ln, name))
+starts.sort()
+for k, (ln, name) in enumerate(starts):
+    REGIONS.append((name, ln, starts[k + 1][0] - 1 if k + 1 < len(starts) else 10**9))
+
+
+def region(tl):
+    for n, a, b in REGIONS:
+        if a <= tl <= b:
+            return n
+    return f"other:{tl}"
+
+
+agg = {}
+for a, s, i in data:
+    f, ln, tl = ctx_line.get(a - base, (None, None, 0))
+    r = region(tl)
+    x = agg.setdefault(r, [0, 0, 0])
+    x[0] += s
+    x[1] += i
+    x[2] += 1
+ts = sum(v[0] for v in agg.values()) or 1
+ti = sum(v[1] for v in agg.values()) or 1
+print(f"{len(data)} SASS instructions ({len(data) * 16 / 1024:.0f} KB), {ts} samples, {ti:.3e} warp inst")
+for r, (s, i, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+    print(f"{r:22s} {100 * s / ts:5.1f}% samples  {100 * i / ti:5.1f}% inst  {n:5d} sass ({n * 16 / 1024:.1f} KB)")
+
+if len(sys.argv) > 4:  # top SASS instructions of one region
+    want = sys.argv[4]
+    sass_text = {}
+    for r in rows[2:]:
+        if len(r) > ii and r[ai].startswith("0x"):
+            sass_text[int(r[ai], 16)] = r[1].strip()
+    top = sorted(((s, i, a) for a, s, i in data if region(ctx_line.get(a - base, (0, 0, 0))[2]) == want), reverse=True)
+    for s, i, a in top[:60]:
+        f, ln, tl = ctx_line.get(a - base, (None, None, 0))
+        print(f"{100 * s / ts:5.2f}% {i:>11d} {a - base:6x} {f}:{ln} ({tl})  {sass_text[a][:70]}")

@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (committed evidence).
 
-usage: python tools/ncu_summary.py <launches.csv|-> <full.ncu-rep> <round-tag> [name] [command]
+usage: python tools/ncu_summary.py <launches.csv|-> <full.ncu-rep> <round-tag> [name] [command] [workload paths]
 writes profiles/<tag>_launches.csv            (kernel, count, total/mean ms, share) unless '-'
        profiles/<tag>_<name>.json             key metrics of the full capture (name default
                                               'path_kernel' = the c2 bench workload)
@@ -102,7 +102,21 @@ dram = to_bytes(out["dram_read"]) + to_bytes(out["dram_write"])
 out["dram_bytes_per_launch"] = dram
 with open(os.path.join(prof, f"{tag}_{name}.json"), "w") as f:
     json.dump(out, f, indent=1)
-if name == "path_kernel":
-    with open(os.path.join(prof, "path_kernel_dram.json"), "w") as f:
-        json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_{name}.json"}, f, indent=1)
+if len(sys.argv) > 7:  # the bench workload's path-kernel evidence: profiles/path_kernel_<workload>.json
+    wl, paths = sys.argv[6], float(sys.argv[7])
+
+    def num(k, scale=1.0):
+        x = out.get(k)
+        return None if x is None else float(str(x["value"]).replace(",", "")) * scale
+
+    digest = {"source": f"profiles/{tag}_{name}.json", "command": command,
+              "duration_ms": num("duration"), "dram_bytes_per_launch": dram,
+              "l2_hit_pct": num("l2_hit_pct"), "l1_hit_pct": num("l1_hit_pct"),
+              "l2_throughput_pct": num("l2_throughput_pct"),
+              "issue_active_pct": num("smsp_issue_active_pct"), "warps_active_per_sm": num("warps_active_per_sm"),
+              "fp64_pipe_pct": num("fp64_pipe_pct"), "fp32_fma_pipe_pct": num("fma_pipe_pct"),
+              "sfu_xu_inst_pct": num("sfu_xu_inst_pct"), "simt_threads_per_warp": num("simt_efficiency_threads"),
+              "stall_mix_pct": out.get("stall_mix_pct")}
+    with open(os.path.join(prof, f"path_kernel_{wl}.json"), "w") as f:
+        json.dump({"dram_bytes_per_path": dram / paths, "paths_per_launch": paths, "digest": digest}, f, indent=1)
 print(json.dumps(out, indent=1))

@@ -18,17 +18,18 @@ import paper_2511_07586_b200 as M  # noqa: E402
 from paper_2511_07586_b200 import _abi as A  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--angles", type=int, default=bench.N_ANGLES)
+ap.add_argument("--angles", type=int, default=181)
 args = ap.parse_args()
-sd, excs = bench.workload(M)
+W = bench.WORKLOADS["c2"]
+sd, excs = W.scene_fn(), W.excs_fn()
 excs = excs[:: max(1, len(excs) // args.angles)][: args.angles]
 scene = M.Scene(sd)
-lam = bench.C0 / bench.FREQ
-spws = [bench.spw_for(M, scene, e, lam) for e in excs]
-cfg = bench.config(M)
+lam = bench.C0 / W.freqs[-1]
+spws = [bench.spw_for(M, scene, e, lam, W.rays) for e in excs]
+cfg = W.config(M)
 for it in range(2):
     vals, st = M.estimate_batch(scene, [(e, s) for e, s in zip(excs, spws)], [[e] for e in excs],
-                                [bench.FREQ], cfg)
+                                W.freqs, cfg)
 print(f"paths {st.rays_launched} kernel_ms {st.kernel_ms:.3f} "
       f"Gpaths/s {st.rays_launched / st.kernel_ms / 1e6:.3f} segments {st.segments_traced} "
       f"occlusion {st.occlusion_queries}")

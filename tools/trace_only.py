@@ -19,14 +19,15 @@ import paper_2511_07586_b200 as M  # noqa: E402
 from paper_2511_07586_b200 import _abi as A  # noqa: E402
 
 step = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-sd, excs = bench.workload(M)
+W = bench.WORKLOADS['c2']
+sd, excs = W.scene_fn(), W.excs_fn()
 scene = M.Scene(sd)
-lam = bench.C0 / bench.FREQ
+lam = bench.C0 / W.freqs[-1]
 L = A.lib()
 dev = torch.device("cuda", 0)
 P, D = [], []
 for e in excs[::step]:
-    spw = bench.spw_for(M, scene, e, lam)
+    spw = bench.spw_for(M, scene, e, lam, W.rays)
     grid, n = M.launch_plan(scene, e.k_inc, 0.0, spw, lam, 1)
     r = grid.rect
     su = -1 + 2 * (np.arange(grid.nu) + 0.5) / grid.nu

@@ -21,12 +21,12 @@ from paper_2511_07586_b200.geometry import airframe  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 if cfg_name == "c2":
-    sd, excs = bench.workload(M)
-    excs = excs[::10]
+    W = bench.WORKLOADS["c2"]
+    sd, excs = W.scene_fn(), W.excs_fn()[::10]
     scene = M.Scene(sd)
-    lam = bench.C0 / bench.FREQ
-    incs = [(e, bench.spw_for(M, scene, e, lam)) for e in excs]
-    freqs, cfg = [bench.FREQ], bench.config(M)
+    lam = bench.C0 / W.freqs[-1]
+    incs = [(e, bench.spw_for(M, scene, e, lam, W.rays)) for e in excs]
+    freqs, cfg = W.freqs, W.config(M)
 elif cfg_name == "c1":
     sd = M.make_builtin_scene("sphere", {"subdivisions": 5})
     scene = M.Scene(sd)
@@ -35,7 +35,7 @@ elif cfg_name == "c1":
     freqs, cfg = [10e9], M.McConfig(strata_per_wavelength=30, samples_per_stratum=1, max_bounce=8, seed=1)
 else:
     c4 = cfg_name == "c4"
-    sd, _ = airframe(200_000, seed=4) if c4 else airframe(1_000_000, seed=5, dielectric_skin=True)
+    sd, _ = airframe(200_000, seed=4) if c4 else airframe(1_000_000, seed=5, dielectric_skin="--pec" not in sys.argv)
     scene = M.Scene(sd)
     freqs = np.linspace(9.5e9, 10.5e9, 64) if c4 else np.linspace(8e9, 12e9, 128)
     lam = 299792458.0 / freqs[-1]
@@ -52,11 +52,16 @@ L = A.lib()
 get = L.mcsbr_gpu_stats_visits
 get.restype = None
 get.argtypes = [C.POINTER(C.c_ulonglong)]
-buf = (C.c_ulonglong * 2)()
-get(buf)
-v0, t0 = buf[0], buf[1]
+b0 = (C.c_ulonglong * 9)()
+b1 = (C.c_ulonglong * 9)()
+get(b0)
 vals, st = M.estimate_batch(scene, incs, [[e] for e in excs], freqs, cfg)
-get(buf)
+get(b1)
+d = [b1[i] - b0[i] for i in range(9)]
 q = st.segments_traced + st.occlusion_queries
-print(f"{cfg_name}: queries {q}  node visits/query {(buf[0] - v0) / q:.2f}  triangle tests/query "
-      f"{(buf[1] - t0) / q:.2f}  bvh {scene.bvh_info()}")
+print(f"{cfg_name}: paths {st.rays_launched} segments {st.segments_traced} occlusion {st.occlusion_queries} "
+      f"kernel {st.kernel_ms:.2f} ms bvh {scene.bvh_info()}")
+for k, name in enumerate(("launch", "surface", "occlusion")):
+    n = max(d[3 * k + 2], 1)
+    print(f"  {name:9s} traced {d[3 * k + 2]:>11d}  node visits/query {d[3 * k] / n:6.2f}  "
+          f"triangle tests/query {d[3 * k + 1] / n:6.2f}")
