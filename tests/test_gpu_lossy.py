@@ -109,3 +109,79 @@ def test_lossy_coated_sphere_config3_geometry():
     assert a.stats.rays_launched == b.stats.rays_launched
     assert b.stats.contributions > 0
     assert not np.allclose(a.sweep.values, b.sweep.values)
+
+
+def layered_slab(a, layers, metal=0.01):
+    """A planar stack on a PEC block, lateral extent [-a, a]^2, top face at
+    z = 0: layers = [(name, eps_r, eps_i, thickness), ...] from the top.
+    Every interface is one horizontal quad (normal +z, front = the medium
+    above); the side walls of every band close its medium against air."""
+    from paper_2511_07586_b200.geometry import scene_from_arrays
+
+    verts, faces, reg, regions = [], [], [], []
+
+    index = {}
+
+    def vid(q):  # shared vertices: the media boundaries must be closed manifolds
+        if q not in index:
+            index[q] = len(verts)
+            verts.append(q)
+        return index[q]
+
+    def quad(p, region):
+        if region not in regions:
+            regions.append(region)
+        i = [vid(q) for q in p]
+        faces.extend([(i[0], i[1], i[2]), (i[0], i[2], i[3])])
+        reg.extend([regions.index(region)] * 2)
+
+    def band(z0, z1, inside):  # side walls of z in [z0, z1], outward normals
+        quad([(a, -a, z0), (a, a, z0), (a, a, z1), (a, -a, z1)], ("air", inside))
+        quad([(-a, a, z0), (-a, -a, z0), (-a, -a, z1), (-a, a, z1)], ("air", inside))
+        quad([(a, a, z0), (-a, a, z0), (-a, a, z1), (a, a, z1)], ("air", inside))
+        quad([(-a, -a, z0), (a, -a, z0), (a, -a, z1), (-a, -a, z1)], ("air", inside))
+
+    def horiz(z, above, below):
+        quad([(-a, -a, z), (a, -a, z), (a, a, z), (-a, a, z)], (above, below))
+
+    mats = {"air": {"eps_r": 1.0}, "metal": {"pec": True}}
+    z, above = 0.0, "air"
+    for name, er, ei, t in layers:
+        horiz(z, above, name)
+        band(z - t, z, name)
+        mats[name] = {"eps_r": er, "eps_i": ei}
+        z, above = z - t, name
+    horiz(z, above, "metal")
+    band(z - metal, z, "metal")
+    quad([(-a, a, z - metal), (a, a, z - metal), (a, -a, z - metal), (-a, -a, z - metal)], ("air", "metal"))
+    return scene_from_arrays(np.array(verts, float), np.array(faces), np.array(reg), regions, mats)
+
+
+@pytest.mark.parametrize("name,layers,f0,f1", [
+    # c5's two-layer skin: 2 mm eps 3.5-0.05j over 4 mm eps 10-1.0j on PEC (8-12 GHz)
+    ("c5_skin", [("outer", 3.5, 0.05, 0.002), ("inner", 10.0, 1.0, 0.004)], 8e9, 12e9),
+    # the planar analogue of c3's shells: 5 mm eps 2.2-0.01j over 10 mm eps 4.0-0.1j on PEC (2.5-3.5 GHz)
+    ("c3_shells", [("outer", 2.2, 0.01, 0.005), ("inner", 4.0, 0.1, 0.010)], 2.5e9, 3.5e9),
+])
+def test_multilayer_lossy_stack_matches_chain_matrix_oracle(name, layers, f0, f1):
+    """SURVEY.md §8c lossy pin: Monte Carlo on a planar PEC-backed two-layer
+    lossy slab at normal incidence against the complex chain-matrix oracle
+    (oracles.cpp:32-64 generalised to complex index, incl. its pec_backed
+    branch :56-59): within 0.1 dB and 0.05 rad at every frequency."""
+    a = 0.15
+    sd = layered_slab(a, layers)
+    ns = [np.sqrt(er - 1j * ei) for _, er, ei, _ in layers]
+    freqs = np.linspace(f0, f1, 9)
+    cfg = M.McConfig(strata_per_wavelength=8, samples_per_stratum=64, seed=17, max_bounce=40,
+                     branch_strategy=M.BranchStrategy.FRESNEL)
+    r = M.estimate(M.Scene(sd), M.monostatic_excitation(0.0, 0.0), freqs, cfg)
+    k0 = 2 * np.pi * freqs / C0
+    area = (2 * a) ** 2
+    want = np.array([1j * k * area * slab_reflection([(n, t) for n, (_, _, _, t) in zip(ns, layers)], f,
+                                                     pec_backed=True) / np.sqrt(np.pi)
+                     for k, f in zip(k0, freqs)])
+    got = r.sweep.values[M.VV]
+    db = 20 * np.log10(np.abs(got) / np.abs(want))
+    ph = np.angle(got / want)
+    assert np.max(np.abs(db)) < 0.1, (db, ph)
+    assert np.max(np.abs(ph)) < 0.05, (db, ph)

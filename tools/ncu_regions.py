@@ -48,7 +48,18 @@ for l in lines[start + 1:]:
 
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))
+rows_all = list(csv.reader(io.StringIO(out)))
+# one block per profiled kernel: a "Kernel Name" row, a header row, then SASS rows
+rows, take = [], False
+for r in rows_all:
+    if r and r[0] == "Kernel Name":
+        take = kern.split("ILi")[0].split("_")[-1] in r[1].replace(" ", "") or kern in r[1]
+        if take and rows:
+            break  # first matching kernel only
+        continue
+    if take:
+        rows.append(r)
+rows.insert(0, ["Kernel Name"])
 hdr = rows[1]
 ai, si, ii = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 data = [(int(r[ai], 16), int(r[si] or 0), int(r[ii] or 0)) for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")]
