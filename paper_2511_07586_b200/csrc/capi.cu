@@ -247,6 +247,12 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
+    // wavefront path pool (wavefront.cu): fields, (kind, rid, list), control words
+    DevBuf<double> wf_pool;
+    DevBuf<uint32_t> wf_u32;
+    DevBuf<unsigned long long> wf_ctl;
+    unsigned long long* wf_host = nullptr;  // pinned: a work-list length read back
+    cudaEvent_t wf_ev = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     SceneView view() const {
@@ -371,7 +377,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 
 constexpr uint64_t kPathStateBytes = 192;
-constexpr uint64_t kRecCapMax = uint64_t{1} << 25;  // contribution records (96 B each): 3.2 GB
+constexpr uint64_t kRecCapMax = uint64_t{1} << 26;  // contribution records (96 B each): 6.4 GB
 constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: at most 256 MB per job
 
 // Fold the peak record count of the scene's previous F > 1 job (if its
@@ -540,6 +546,31 @@ void fill_config(TraceParams& p, const mcsbr_mc_config* cfg) {
     p.rng_mode = cfg->rng_mode;
 }
 
+// One launch group through the wavefront kernels: shade + trace per
+// iteration until the shading pass leaves no query (every path finished and
+// every launch entry taken).  The work-list length is read back every
+// kWfCheck iterations; the iterations in between that find no work return at
+// once.
+int run_wavefront(mcsbr_scene* s, const TraceParams& p, const WfParams& w, cudaStream_t stream) {
+    constexpr uint32_t kWfCheck = 8;
+    constexpr uint32_t kWfMaxIters = 1u << 20;
+    CK(cudaMemsetAsync(w.kind, 0, sizeof(uint32_t) * w.np, stream), "memset path pool");
+    CK(cudaMemsetAsync(w.list_n, 0, sizeof(unsigned long long) * (6 + 2ull * (w.np / 32)), stream),
+       "memset path pool");
+    for (uint32_t it = 0; it < kWfMaxIters; ++it) {
+        CK(launch_wavefront_iteration(p, w, it, s->sms, stream), "wavefront launch");
+        g_launches += 2;
+        if (it % kWfCheck == kWfCheck - 1) {
+            CK(cudaMemcpyAsync(s->wf_host, w.list_n + it % 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               stream), "work-list readback");
+            CK(cudaEventRecord(s->wf_ev, stream), "cudaEventRecord");
+            CK(cudaEventSynchronize(s->wf_ev), "cudaEventSynchronize");
+            if (*s->wf_host == 0) return MCSBR_OK;
+        }
+    }
+    return set_err(MCSBR_EDEVICE, "wavefront: iteration limit reached");
+}
+
 // Upload a planned job and run the path kernel(s) on s->stream, adding into
 // d_sums / d_counters.  One launch per receiver index (receivers of one
 // incidence share nothing but the geometry).
@@ -634,9 +665,32 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
     if (cover_words) {
         CK(launch_cover(s->inc.p, static_cast<uint32_t>(incs.size()), s->d_tri32, s->nt, s->center, s->radius,
-                        p.spp, static_cast<uint32_t>(p.band_order), s->cover.p, stream),
+                        p.spp, static_cast<uint32_t>(p.band_order), s->cover.p, cover_words, s->sms, stream),
            "coverage kernel launch");
         ++g_launches;
+    }
+    // Wavefront (wavefront.cu) for the deferred-accumulation Monte Carlo
+    // mode without parity instrumentation; the megakernel otherwise.
+    const bool wavefront = defer && !fan && !p.det && !p.contrib_out && !p.plog_tri &&
+                           env_u32("MCSBR_WAVEFRONT", 0) != 0;
+    WfParams w{};
+    if (wavefront) {
+        const uint32_t np = static_cast<uint32_t>(s->sms) * env_u32("MCSBR_WF_SLOTS_PER_SM", 4096);
+        w.np = (np + 127) / 128 * 128;
+        CK(s->wf_pool.reserve(static_cast<size_t>(kWfFieldsHost) * w.np), "dev_malloc(path pool)");
+        CK(s->wf_u32.reserve(3ull * w.np), "dev_malloc(path pool)");
+        CK(s->wf_ctl.reserve(6 + 2ull * (w.np / 32)), "dev_malloc(path pool)");
+        if (!s->wf_host) {
+            CK(cudaMallocHost(&s->wf_host, sizeof(unsigned long long)), "cudaMallocHost");
+            CK(cudaEventCreateWithFlags(&s->wf_ev, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        w.pool = s->wf_pool.p;
+        w.kind = s->wf_u32.p;
+        w.rid = s->wf_u32.p + w.np;
+        w.list = s->wf_u32.p + 2ull * w.np;
+        w.list_n = s->wf_ctl.p;
+        w.trace_cursor = s->wf_ctl.p + 3;
+        w.wrange = s->wf_ctl.p + 6;
     }
     for (uint32_t r = 0; r < job.n_rx; r += step) {
         p.rx_index = r;
@@ -649,7 +703,12 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
             p.total_entries = gr.entries;
             CK(cudaMemsetAsync(s->tile.p, 0, 2 * sizeof(unsigned long long), stream), "reset tile counter");
             CK(kt_mark(0, stream, s->device, false), "cudaEventRecord");
-            CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
+            if (wavefront) {
+                int rc = run_wavefront(s, p, w, stream);
+                if (rc) return rc;
+            } else {
+                CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
+            }
             CK(kt_mark(0, stream, s->device, true), "cudaEventRecord");
             if (defer) {
                 CK(kt_mark(1, stream, s->device, false), "cudaEventRecord");
@@ -945,6 +1004,11 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->tile.release();
     s->recs.release();
     s->cover.release();
+    s->wf_pool.release();
+    s->wf_u32.release();
+    s->wf_ctl.release();
+    if (s->wf_host) cudaFreeHost(s->wf_host);
+    if (s->wf_ev) cudaEventDestroy(s->wf_ev);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->peak_ev) cudaEventDestroy(s->peak_ev);
     if (s->peak_host) cudaFreeHost(s->peak_host);

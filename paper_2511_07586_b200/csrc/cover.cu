@@ -19,9 +19,10 @@
 // descent of rays that leave the scene untouched -- 87% of the c5 launch
 // rays (nose-on airframe in its bounding aperture).
 //
-// One block per incidence builds the incidence's bitmap in shared memory
-// (<= 64 KB: the group size grows past 32 entries only for incidences of
-// more than 2^24 entries) and writes it out with plain stores.
+// Blocks (incidence, triangle slice) build the slice's bitmap of the
+// incidence in shared memory (<= 64 KB: the group size grows past 32 entries
+// only for incidences of more than 2^24 entries) and OR it into the
+// incidence's bitmap in HBM.
 #include <cstdint>
 
 #include "internal.h"
@@ -79,7 +80,10 @@ __global__ void __launch_bounds__(512) cover_kernel(const IncDev* __restrict__ i
     const float ux = static_cast<float>(I.u[0]), uy = static_cast<float>(I.u[1]), uz = static_cast<float>(I.u[2]);
     const float vx = static_cast<float>(I.v[0]), vy = static_cast<float>(I.v[1]), vz = static_cast<float>(I.v[2]);
     const uint32_t bh = band ? band : 1u;
-    for (uint32_t t = threadIdx.x; t < n_tri; t += blockDim.x) {
+    // blockIdx.y of gridDim.y: this block's slice of the triangles
+    const uint32_t t0 = static_cast<uint32_t>(static_cast<uint64_t>(n_tri) * blockIdx.y / gridDim.y);
+    const uint32_t t1 = static_cast<uint32_t>(static_cast<uint64_t>(n_tri) * (blockIdx.y + 1) / gridDim.y);
+    for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
         const float* p = tri32 + 9ull * t;
         float umin = 3e38f, umax = -3e38f, vmin = 3e38f, vmax = -3e38f;
 #pragma unroll
@@ -114,8 +118,10 @@ __global__ void __launch_bounds__(512) cover_kernel(const IncDev* __restrict__ i
         }
     }
     __syncthreads();
+    // merge the slice's bits (the bitmap was zeroed by the host)
     uint32_t* dst = out + I.cover_off;
-    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) dst[w] = sbits[w];
+    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x)
+        if (sbits[w]) atomicOr(dst + w, sbits[w]);
 }
 
 }  // namespace
@@ -135,14 +141,23 @@ uint32_t cover_shift_for(uint64_t entries) {
 
 cudaError_t launch_cover(const IncDev* d_inc, uint32_t n_inc, const float* tri32, uint32_t n_tri,
                          const double center[3], double radius, uint32_t spp, uint32_t band, uint32_t* out,
-                         cudaStream_t stream) {
+                         uint64_t out_words, int device_sms, cudaStream_t stream) {
     if (n_inc == 0) return cudaSuccess;
+    cudaError_t z = cudaMemsetAsync(out, 0, sizeof(uint32_t) * out_words, stream);
+    if (z != cudaSuccess) return z;
+    // enough blocks to fill the GPU: triangle slices per incidence, each slice
+    // at least 4096 triangles
+    uint32_t slices = static_cast<uint32_t>(device_sms) * 2u / n_inc;
+    slices = slices < 1u ? 1u : slices;
+    const uint32_t max_slices = (n_tri + 4095u) / 4096u;
+    slices = slices > max_slices ? max_slices : slices;
+    slices = slices > 65535u ? 65535u : slices;
     const int smem = static_cast<int>(kCoverMaxBits / 8);
     cudaError_t e = cudaFuncSetAttribute(cover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const float margin = static_cast<float>(1e-5 * radius);
-    cover_kernel<<<n_inc, 512, smem, stream>>>(d_inc, tri32, n_tri, center[0], center[1], center[2], spp, band, margin,
-                                               out);
+    cover_kernel<<<dim3(n_inc, slices), 512, smem, stream>>>(d_inc, tri32, n_tri, center[0], center[1], center[2], spp,
+                                                             band, margin, out);
     return cudaGetLastError();
 }
 

@@ -183,13 +183,28 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                       double box_pad,
                       cudaStream_t stream, BvhBuildOut* out);
 
+// wavefront.cu: the pool of paths between the shading and traversal kernels
+struct WfParams {
+    double* pool;                      // [kWfFields][np] doubles (wavefront.cu field map)
+    uint32_t np;                       // slots, a multiple of 128
+    uint32_t* kind;                    // [np] query kind (0 none / launch / surface / occlusion)
+    uint32_t* rid;                     // [np] query result: triangle id or 0xffffffff
+    uint32_t* list;                    // [np] work list of the next traversal
+    unsigned long long* list_n;        // [3] work-list lengths (rotating per iteration)
+    unsigned long long* trace_cursor;  // [3] traversal cursors (rotating per iteration)
+    unsigned long long* wrange;        // [np / 32][2] each warp's launch-entry range
+};
+constexpr int kWfFieldsHost = 41;
+cudaError_t launch_wavefront_iteration(const TraceParams& p, const WfParams& w, uint32_t iter, int device_sms,
+                                       cudaStream_t stream);
+
 // cover.cu: launch-ray coverage bitmaps
 cudaError_t build_tri32(const double* d_vtx, const uint4* d_tri, uint32_t n, const double center[3], float* out,
                         cudaStream_t stream);
 uint32_t cover_shift_for(uint64_t entries);
 cudaError_t launch_cover(const IncDev* d_inc, uint32_t n_inc, const float* tri32, uint32_t n_tri,
                          const double center[3], double radius, uint32_t spp, uint32_t band, uint32_t* out,
-                         cudaStream_t stream);
+                         uint64_t out_words, int device_sms, cudaStream_t stream);
 
 // trace.cu
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream,
