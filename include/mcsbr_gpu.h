@@ -104,6 +104,20 @@ typedef struct mcsbr_receiver {
 
 #define MCSBR_MAX_BOUNCE_LIMIT 64
 
+/* Far-field reduction (mcsbr_mc_config.reduction).  FAST sums contributions
+ * with fp64 atomics in whatever order the GPU schedules them (rerun-to-rerun
+ * differences in the last bits).  EXACT converts every (contribution,
+ * frequency, channel) term to a 192-bit fixed-point integer (LSB 2^-120,
+ * range +-2^71) and sums integers, which is associative: the result is
+ * byte-identical across reruns, launch groupings and shard / GPU counts,
+ * like the reference's fixed-order block merge (solver_mc.cpp:212-216,
+ * runner.hpp:2-5).  Raw device sums of EXACT jobs are 4 int64 limbs of 48
+ * bits per fp64 value (MCSBR_EXACT_LIMBS), summable across ranks with any
+ * integer all-reduce and finalized by mcsbr_gpu_finalize_exact. */
+#define MCSBR_REDUCE_FAST 0
+#define MCSBR_REDUCE_EXACT 1
+#define MCSBR_EXACT_LIMBS 4
+
 /* Mirrors mcsbr::McConfig + RouletteConfig (proj/include/mcsbr/solver_mc.hpp:14-36),
  * plus the GPU-only rng_mode.  mcsbr_gpu_default_config() returns the
  * reference defaults. */
@@ -122,6 +136,9 @@ typedef struct mcsbr_mc_config {
     double p_min;                 /* 0.05 */
     int32_t block_size;           /* 8192 (validated only; the GPU has no CPU blocks) */
     int32_t rng_mode;             /* MCSBR_RNG_REFERENCE */
+    int32_t reduction;            /* MCSBR_REDUCE_FAST */
+    int32_t parity_fp64_refine;   /* 1: every triangle test in the reference's fp64 arithmetic (parity);
+                                     0: statistical-mode fast path (fp32 triangle tests, PHILOX only) */
 } mcsbr_mc_config;
 
 /* Mirrors mcsbr::RunStats (proj/include/mcsbr/solver_common.hpp:37-53). */
@@ -282,7 +299,8 @@ MCSBR_API int mcsbr_gpu_estimate_batch(mcsbr_scene* scene, const mcsbr_incidence
 /* Device-resident variant for multi-GPU sharding and benchmarking: traces the
  * entry range [shard_index/shard_count] of every incidence and ADDS raw
  * (un-finalized) sums into the caller's device buffer d_sums
- * ([n_inc][n_rx][nf][4] complex) and counters into d_counters
+ * ([n_inc][n_rx][nf][4] complex; for MCSBR_REDUCE_EXACT configs int64 limbs
+ * [n_inc][n_rx][nf][8][MCSBR_EXACT_LIMBS]) and counters into d_counters
  * (MCSBR_COUNTER_WORDS uint64), on `stream` (a cudaStream_t, NULL = legacy
  * default).  Asynchronous: no host synchronisation.  The caller all-reduces
  * the buffers (NCCL) and finalizes with mcsbr_gpu_finalize. */
@@ -298,6 +316,10 @@ MCSBR_API int mcsbr_gpu_trace_device(mcsbr_scene* scene, const mcsbr_incidence* 
  * [n][4][nf] output layout (host arrays). */
 MCSBR_API int mcsbr_gpu_finalize(const double* raw_sums, uint32_t n, const double* frequencies,
                        uint32_t n_frequencies, double* values);
+/* The same for the raw sums of an MCSBR_REDUCE_EXACT job: limbs
+ * [n][nf][8][MCSBR_EXACT_LIMBS] int64 (possibly summed over ranks). */
+MCSBR_API int mcsbr_gpu_finalize_exact(const int64_t* limbs, uint32_t n, const double* frequencies,
+                                       uint32_t n_frequencies, double* values);
 
 /* Decode a counter block (device layout above, copied to host) into stats. */
 MCSBR_API int mcsbr_gpu_decode_counters(const uint64_t* counters, mcsbr_stats* stats);

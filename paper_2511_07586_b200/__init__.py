@@ -9,7 +9,7 @@ from .geometry import (SceneData, SceneError, Material, load_scene, load_scene_f
                        builtin_scene, builtin_scene_names, make_builtin_scene, dihedral_grid,
                        coated_sphere, MeshBuilder)
 from .solver import (Scene, Excitation, monostatic_excitation, bistatic_excitation, McConfig,
-                     RouletteConfig, BranchStrategy, RngMode, DetConfig, DetResult, solve, SweepResult, RunStats, McResult,
+                     RouletteConfig, BranchStrategy, RngMode, Reduction, DetConfig, DetResult, solve, SweepResult, RunStats, McResult,
                      LaunchRect, StrataGrid, DomainError, estimate, estimate_batch, launch_plan,
                      launch_rect, rcs_m2, VV, HH, VH, HV, K_SPEED_OF_LIGHT)
 from . import signal
@@ -19,7 +19,7 @@ __all__ = [
     "SceneData", "SceneError", "Material", "load_scene", "load_scene_files", "airframe", "builtin_scene",
     "builtin_scene_names", "make_builtin_scene", "dihedral_grid", "coated_sphere", "MeshBuilder",
     "Scene", "Excitation", "monostatic_excitation", "bistatic_excitation", "McConfig",
-    "RouletteConfig", "BranchStrategy", "RngMode", "DetConfig", "DetResult", "solve", "SweepResult", "RunStats", "McResult",
+    "RouletteConfig", "BranchStrategy", "RngMode", "Reduction", "DetConfig", "DetResult", "solve", "SweepResult", "RunStats", "McResult",
     "LaunchRect", "StrataGrid", "DomainError", "estimate", "estimate_batch", "launch_plan",
     "launch_rect", "rcs_m2", "VV", "HH", "VH", "HV", "K_SPEED_OF_LIGHT",
     "signal", "Window", "RangeProfile", "IsarImage", "SignalError", "range_profile", "isar",

@@ -26,6 +26,9 @@ MCSBR_BRANCH_FIFTY_FIFTY = 0
 MCSBR_BRANCH_FRESNEL = 1
 MCSBR_RNG_REFERENCE = 0
 MCSBR_RNG_PHILOX = 1
+MCSBR_REDUCE_FAST = 0
+MCSBR_REDUCE_EXACT = 1
+MCSBR_EXACT_LIMBS = 4
 MCSBR_MAX_BOUNCE_LIMIT = 64
 MCSBR_COUNTER_WORDS = 256
 
@@ -94,6 +97,8 @@ class McConfigC(C.Structure):
         ("p_min", C.c_double),
         ("block_size", C.c_int32),
         ("rng_mode", C.c_int32),
+        ("reduction", C.c_int32),
+        ("parity_fp64_refine", C.c_int32),
     ]
 
 
@@ -213,6 +218,7 @@ SIGNATURES = {
          C.c_void_p],
     ),
     "mcsbr_gpu_finalize": (C.c_int, [_DP, C.c_uint32, _DP, C.c_uint32, _DP]),
+    "mcsbr_gpu_finalize_exact": (C.c_int, [C.POINTER(C.c_int64), C.c_uint32, _DP, C.c_uint32, _DP]),
     "mcsbr_gpu_decode_counters": (C.c_int, [_U64P, C.POINTER(Stats)]),
     "mcsbr_gpu_path_log": (
         C.c_int,

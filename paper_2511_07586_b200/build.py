@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmcsbr_gpu.so")
 SOURCES = ["capi.cu", "bvh.cu", "trace.cu", "imaging.cu", "cover.cu", "wavefront.cu"]
-HEADERS = ["dmath.cuh", "rng.cuh", "physics.cuh", "internal.h", "pathcore.cuh"]
+HEADERS = ["dmath.cuh", "rng.cuh", "physics.cuh", "internal.h", "pathcore.cuh", "fixedpoint.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

@@ -23,6 +23,7 @@
 #include <mutex>
 #include <unordered_map>
 
+#include "fixedpoint.cuh"
 #include "internal.h"
 #include "mcsbr_gpu.h"
 
@@ -247,6 +248,8 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
+    DevBuf<unsigned long long> xsums;  // MCSBR_REDUCE_EXACT: 192-bit sums of the current job
+    DevBuf<long long> limbs;           // MCSBR_REDUCE_EXACT: their limbs (estimate / estimate_batch)
     // wavefront path pool (wavefront.cu): fields, (kind, rid, list), control words
     DevBuf<double> wf_pool;
     DevBuf<uint32_t> wf_u32;
@@ -338,6 +341,13 @@ int validate(const mcsbr_mc_config* c) {
         return set_err(MCSBR_EINVAL, "mc: max_bounce exceeds MCSBR_MAX_BOUNCE_LIMIT (64)");
     if (c->rng_mode != MCSBR_RNG_REFERENCE && c->rng_mode != MCSBR_RNG_PHILOX)
         return set_err(MCSBR_EINVAL, "mc: unknown rng_mode");
+    if (c->reduction != MCSBR_REDUCE_FAST && c->reduction != MCSBR_REDUCE_EXACT)
+        return set_err(MCSBR_EINVAL, "mc: unknown reduction");
+    if (c->parity_fp64_refine != 0 && c->parity_fp64_refine != 1)
+        return set_err(MCSBR_EINVAL, "mc: parity_fp64_refine must be 0 or 1");
+    if (c->parity_fp64_refine == 0 && c->rng_mode != MCSBR_RNG_PHILOX)
+        return set_err(MCSBR_EINVAL, "mc: parity_fp64_refine = 0 (fp32 triangle tests) is a statistical-mode "
+                                     "option: it needs rng_mode PHILOX");
     return MCSBR_OK;
 }
 
@@ -368,6 +378,7 @@ mcsbr_mc_config det_as_mc(const mcsbr_det_config* d) {
     c.reference_wavelength = d->reference_wavelength;
     c.launch_padding = d->launch_padding;
     c.block_size = d->block_size;
+    c.reduction = MCSBR_REDUCE_EXACT;  // deterministic solver, reproducible sums (any F, any grouping)
     return c;
 }
 
@@ -576,7 +587,17 @@ int run_wavefront(mcsbr_scene* s, const TraceParams& p, const WfParams& w, cudaS
 // incidence share nothing but the geometry).
 int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* cfg, int occlusion,
             double* d_sums, unsigned long long* d_counters, cudaStream_t stream, TraceParams* extra,
-            float* kernel_ms) {
+            float* kernel_ms, long long* d_limbs = nullptr) {
+    // MCSBR_REDUCE_EXACT (fixedpoint.cuh): every F goes through the records
+    // and the integer accumulate kernel, receivers are traced one by one
+    // (no fan), and the 192-bit sums are ADDED as limbs into d_limbs
+    const bool exact = cfg->reduction == MCSBR_REDUCE_EXACT;
+    if (exact && !d_limbs) return set_err(MCSBR_EINVAL, "exact reduction: no limb buffer");
+    const uint64_t n_values = static_cast<uint64_t>(job.inc.size()) * job.n_rx * nf * 8;
+    if (exact) {
+        CK(s->xsums.reserve(3 * n_values), "dev_malloc(exact sums)");
+        CK(cudaMemsetAsync(s->xsums.p, 0, sizeof(unsigned long long) * 3 * n_values, stream), "memset exact sums");
+    }
     CK(s->inc.reserve(job.inc.size()), "dev_malloc(incidences)");
     CK(s->rx.reserve(job.rx.size()), "dev_malloc(receivers)");
     CK(s->k0.reserve(nf), "dev_malloc(k0)");
@@ -584,7 +605,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // deferred accumulation (F > 1): one 96-byte record per visible
     // contribution; sized for one per launched path of the largest group
     // (measured c4/c5: ~0.1 per path), overflow falls back to direct atomics
-    const bool defer = nf > 1;
+    const bool defer = nf > 1 || exact;
     uint64_t rec_cap = 0;
     if (defer) {
         rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1) + 4096;
@@ -659,7 +680,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // once per chunk of 32 receivers (fan mode).  Otherwise one launch per
     // receiver index (multi-frequency bistatic sweeps re-trace per receiver,
     // as the reference does).
-    const bool fan = job.n_rx > 1 && trace_fan_supported(nf);
+    const bool fan = job.n_rx > 1 && trace_fan_supported(nf) && !exact;
     const uint32_t step = fan ? 32u : 1u;
     p.fan = fan ? 1 : 0;
     if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
@@ -700,6 +721,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
             p.inc_base = gr.a0;
             p.rx = s->rx.p + static_cast<size_t>(gr.a0) * job.n_rx;
             p.sums = d_sums + static_cast<size_t>(gr.a0) * job.n_rx * nf * 8;
+            p.xsums = exact ? s->xsums.p + 3ull * gr.a0 * job.n_rx * nf * 8 : nullptr;
             p.total_entries = gr.entries;
             CK(cudaMemsetAsync(s->tile.p, 0, 2 * sizeof(unsigned long long), stream), "reset tile counter");
             CK(kt_mark(0, stream, s->device, false), "cudaEventRecord");
@@ -716,6 +738,10 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
                 CK(kt_mark(1, stream, s->device, true), "cudaEventRecord");
             }
         }
+    }
+    if (exact) {
+        CK(launch_exact_limbs(s->xsums.p, n_values, d_limbs, stream), "exact limbs launch");
+        ++g_launches;
     }
     if (defer && s->peak_host) {  // learn the record ratio for the next job
         CK(cudaMemcpyAsync(s->peak_host, s->tile.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -761,7 +787,8 @@ int fault_check(const unsigned long long* c) {
     if (f & 1u) m += " fresnel: refractive indices / cos_theta_i out of domain;";
     if (f & 2u) m += " interface_transform: field is not transverse to dir_in;";
     if (f & 4u) m += " reflect_dir/refract_dir: grazing incidence;";
-    if (f & 8u) m += " BVH traversal stack overflow;";
+    if (f & 8u) m += " deterministic solver branch stack overflow;";
+    if (f & 16u) m += " exact reduction: a term outside the 192-bit fixed-point range (|v| >= 2^71);";
     return set_err(MCSBR_EDEVICE, m);
 }
 
@@ -778,6 +805,13 @@ void finalize_values(const double* raw, uint32_t n, const double* freqs, uint32_
                 o[1] = pre_re * sv[1] + pre_im * sv[0];
             }
         }
+    }
+}
+
+void limbs_to_doubles(const long long* limbs, size_t n, double* out) {
+    for (size_t i = 0; i < n; ++i) {
+        const int64_t l[4] = {limbs[4 * i], limbs[4 * i + 1], limbs[4 * i + 2], limbs[4 * i + 3]};
+        out[i] = mcsbr_fx::fx_limbs_to_double(l);
     }
 }
 
@@ -835,6 +869,8 @@ void mcsbr_gpu_default_config(mcsbr_mc_config* c) {
     c->p_min = 0.05;
     c->block_size = 8192;
     c->rng_mode = MCSBR_RNG_REFERENCE;
+    c->reduction = MCSBR_REDUCE_FAST;
+    c->parity_fp64_refine = 1;
 }
 
 int mcsbr_gpu_validate_config(const mcsbr_mc_config* cfg) { return validate(cfg); }
@@ -1004,6 +1040,8 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->tile.release();
     s->recs.release();
     s->cover.release();
+    s->xsums.release();
+    s->limbs.release();
     s->wf_pool.release();
     s->wf_u32.release();
     s->wf_ctl.release();
@@ -1174,7 +1212,13 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         extra.det_block_size = static_cast<uint64_t>(det->block_size);
     }
     float kms = 0.f;
-    rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms);
+    const bool exact = cfg->reduction == MCSBR_REDUCE_EXACT;
+    if (exact) {
+        CK(s->limbs.reserve(nsum * MCSBR_EXACT_LIMBS), "dev_malloc(limbs)");
+        CK(cudaMemsetAsync(s->limbs.p, 0, sizeof(long long) * nsum * MCSBR_EXACT_LIMBS, s->stream), "memset limbs");
+    }
+    rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms,
+                 exact ? s->limbs.p : nullptr);
     std::vector<unsigned long long> det_acc(2 * det_nblocks);
     if (rc == MCSBR_OK && det && det_nblocks) {
         const cudaError_t e2 = cudaMemcpy(det_acc.data(), d_blocks, sizeof(unsigned long long) * det_acc.size(),
@@ -1200,9 +1244,13 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         dev_free(d_cnt);
         return rc;
     }
-    std::vector<double> raw(nsum);
+    std::vector<double> raw(exact ? 0 : nsum);
+    std::vector<long long> raw_limbs(exact ? nsum * MCSBR_EXACT_LIMBS : 0);
     unsigned long long cnt[kCntWords];
-    cudaError_t e = cudaMemcpyAsync(raw.data(), s->sums.p, sizeof(double) * nsum, cudaMemcpyDeviceToHost, s->stream);
+    cudaError_t e = exact ? cudaMemcpyAsync(raw_limbs.data(), s->limbs.p, sizeof(long long) * raw_limbs.size(),
+                                            cudaMemcpyDeviceToHost, s->stream)
+                          : cudaMemcpyAsync(raw.data(), s->sums.p, sizeof(double) * nsum, cudaMemcpyDeviceToHost,
+                                            s->stream);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(cnt, s->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, s->stream);
     unsigned long long ncol = 0;
@@ -1223,6 +1271,10 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     if (e != cudaSuccess) return cuda_err(e, "estimate readback");
     rc = fault_check(cnt);
     if (rc) return rc;
+    if (exact) {
+        raw.resize(nsum);
+        limbs_to_doubles(raw_limbs.data(), nsum, raw.data());
+    }
     finalize_values(raw.data(), n_inc * n_rx, freqs, nf, values);
     if (stats) {
         decode(cnt, stats);
@@ -1342,12 +1394,22 @@ int mcsbr_gpu_trace_device(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, shard, nshard, s->sms * 16, &job);
     if (rc) return rc;
     return run_job(s, job, nf, cfg, occlusion, d_sums, reinterpret_cast<unsigned long long*>(d_counters),
-                   static_cast<cudaStream_t>(stream), nullptr, nullptr);
+                   static_cast<cudaStream_t>(stream), nullptr, nullptr,
+                   cfg->reduction == MCSBR_REDUCE_EXACT ? reinterpret_cast<long long*>(d_sums) : nullptr);
 }
 
 int mcsbr_gpu_finalize(const double* raw, uint32_t n, const double* freqs, uint32_t nf, double* values) {
     if (!raw || !freqs || !values) return set_err(MCSBR_EINVAL, "finalize: null argument");
     finalize_values(raw, n, freqs, nf, values);
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_finalize_exact(const int64_t* limbs, uint32_t n, const double* freqs, uint32_t nf, double* values) {
+    if (!limbs || !freqs || !values) return set_err(MCSBR_EINVAL, "finalize_exact: null argument");
+    const size_t nsum = static_cast<size_t>(n) * nf * 8;
+    std::vector<double> raw(nsum);
+    limbs_to_doubles(reinterpret_cast<const long long*>(limbs), nsum, raw.data());
+    finalize_values(raw.data(), n, freqs, nf, values);
     return MCSBR_OK;
 }
 

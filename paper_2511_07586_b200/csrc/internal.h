@@ -103,6 +103,7 @@ struct TraceParams {
     int occlusion;
     double* sums;           // [n_inc][n_rx][nf][4] complex (re, im)
     const uint32_t* cover;  // launch-ray coverage bitmaps (IncDev::cover_off), or nullptr
+    unsigned long long* xsums;  // MCSBR_REDUCE_EXACT: 192-bit fixed-point sums, 3 words per value of `sums`
     // deferred accumulation (F > 1): contribution records of this launch
     double* recs;                      // [rec_cap][12]: amp[4], s (re, im), incidence
     unsigned long long* rec_count;
@@ -209,6 +210,9 @@ cudaError_t launch_cover(const IncDev* d_inc, uint32_t n_inc, const float* tri32
 // trace.cu
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream,
                          uint64_t* launches);
+// exact sums (3 words per value) -> 48-bit limbs ADDED into limbs (4 per value)
+cudaError_t launch_exact_limbs(const unsigned long long* xsums, uint64_t n_values, long long* limbs,
+                               cudaStream_t stream);
 cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream,
                               uint64_t* launches);
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,

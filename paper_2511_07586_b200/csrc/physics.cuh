@@ -20,6 +20,7 @@ enum : uint32_t {
     kFaultTransverse = 2u,
     kFaultGrazingDir = 4u,
     kFaultStack = 8u,
+    kFaultFixedRange = 16u,  // MCSBR_REDUCE_EXACT: a term outside the 192-bit fixed-point range
 };
 
 struct Coeffs {

@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "dmath.cuh"
+#include "fixedpoint.cuh"
 #include "internal.h"
 #include "physics.cuh"
 #include "rng.cuh"
@@ -643,6 +644,10 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                         }
                         const NT sp = shfl_nt(s_path, src);
                         for (uint32_t f = lane; f < P.nf; f += 32) {
+                            if (P.xsums) {
+                                exact_add_global(P, P.xsums + ((out - P.sums) + f * 8) * 3, f, am, sp);
+                                continue;
+                            }
                             const Cx z = freq_phasor(P, f, sp);
 #pragma unroll
                             for (int ch = 0; ch < 4; ++ch) {
@@ -836,6 +841,87 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
     }
 }
 
+// K4b, MCSBR_REDUCE_EXACT: the same record sweep with one frequency per lane
+// (f_begin + lane); every term is rounded once to 192-bit fixed point and
+// summed in integer registers (fixedpoint.cuh), so the sums are independent
+// of the record order, the span split and the launch grouping.  Phasors and
+// products are exact_add_global's (freq_phasor, one IEEE operation each).
+__global__ void __launch_bounds__(128) accumulate_exact_kernel(TraceParams P, uint32_t f_begin) {
+    __shared__ double2 st[4][32][6];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t n_all = *P.rec_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(P.rec_count + 1, n_all);  // peak for the host
+    const uint64_t n = min(n_all, P.rec_cap);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 4, gw = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
+    uint64_t span = ((n + nw - 1) / nw + 31) & ~31ull;
+    span = span < 512 ? 512 : span;
+    const uint32_t f = f_begin + static_cast<uint32_t>(lane);
+    const bool has_f = f < P.nf;
+    uint64_t acc[8][3];
+    bool ok = true;
+    const double2* recs = reinterpret_cast<const double2*>(P.recs);
+    for (uint64_t r0 = gw * span; r0 < n; r0 += nw * span) {
+        const uint64_t r1 = min(r0 + span, n);
+        uint32_t cur = 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0;
+        auto flush = [&]() {
+            if (cur == 0xffffffffu || !has_f) return;
+            unsigned long long* g = P.xsums + ((static_cast<size_t>(cur) * P.n_rx + P.rx_index) * P.nf + f) * 8 * 3;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                mcsbr_fx::fx_atomic_add(g + 3 * k, acc[k]);
+                acc[k][0] = acc[k][1] = acc[k][2] = 0;
+            }
+        };
+        for (uint64_t rb = r0; rb < r1; rb += 32) {
+            const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(32), r1 - rb));
+            if (static_cast<uint32_t>(lane) < cnt) {
+                const double2* r = recs + (rb + lane) * kRecD2;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) st[warp][lane][c] = __ldcs(r + c);
+            }
+            __syncwarp();
+            for (uint32_t j = 0; j < cnt; ++j) {
+                const double2* t = st[warp][j];
+                const uint32_t a = static_cast<uint32_t>(__double_as_longlong(t[5].x));
+                if (a != cur) {
+                    flush();
+                    cur = a;
+                }
+                if (!has_f) continue;
+                Cx am[4];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) am[ch] = {t[ch].x, t[ch].y};
+                const Cx sp = {t[4].x, t[4].y};
+                const Cx z = P.scene.lossy ? freq_phasor(P, f, sp) : freq_phasor(P, f, sp.re);
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const Cx v = am[ch] * z;
+                    uint64_t w[3];
+                    ok = mcsbr_fx::fx_from_double(v.re, w) && ok;
+                    mcsbr_fx::fx_add(acc[2 * ch], w);
+                    ok = mcsbr_fx::fx_from_double(v.im, w) && ok;
+                    mcsbr_fx::fx_add(acc[2 * ch + 1], w);
+                }
+            }
+            __syncwarp();
+        }
+        flush();
+    }
+    if (!ok) atomicOr(P.counters + kCntFault, static_cast<unsigned long long>(kFaultFixedRange));
+}
+
+__global__ void exact_limbs_kernel(const unsigned long long* __restrict__ x, uint64_t n, long long* __restrict__ limbs) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t w[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    int64_t l[4];
+    mcsbr_fx::fx_to_limbs(w, l);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) limbs[4 * i + k] += l[k];
+}
+
 __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, const double* __restrict__ d,
                                  const double* __restrict__ tmin, uint32_t n, int any_hit,
                                  double* __restrict__ t_out, uint32_t* __restrict__ id_out) {
@@ -852,7 +938,7 @@ __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, cons
 
 }  // namespace
 
-bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1; }
+bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1 && !p.xsums; }
 
 bool trace_fan_supported(uint32_t nf) { return nf == 1; }
 
@@ -889,9 +975,26 @@ static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int thre
                               : launch_mode<kModeDefer, kDiel, kLossy, false>(p, sms, threads, smem, stream);
 }
 
-// deferred accumulation of one path-kernel launch's records (F > 1)
+cudaError_t launch_exact_limbs(const unsigned long long* xsums, uint64_t n_values, long long* limbs,
+                               cudaStream_t stream) {
+    if (n_values == 0) return cudaSuccess;
+    exact_limbs_kernel<<<static_cast<unsigned>((n_values + 255) / 256), 256, 0, stream>>>(xsums, n_values, limbs);
+    return cudaGetLastError();
+}
+
+// deferred accumulation of one path-kernel launch's records (F > 1, or any
+// F under MCSBR_REDUCE_EXACT)
 cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const unsigned blocks = static_cast<unsigned>(device_sms) * 4;
+    if (p.xsums) {
+        for (uint32_t fb = 0; fb < p.nf; fb += 32) {
+            accumulate_exact_kernel<<<blocks, 128, 0, stream>>>(p, fb);
+            if (launches) ++*launches;
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     const uint32_t fpl = p.nf <= 32 ? 1 : (p.nf <= 64 ? 2 : 4);
     const bool real_amp = p.scene.all_pec && !p.scene.lossy;  // PEC paths carry real amplitudes
     for (uint32_t fb = 0; fb < p.nf; fb += 32 * fpl) {

@@ -33,6 +33,7 @@
 #include <type_traits>
 
 #include "dmath.cuh"
+#include "fixedpoint.cuh"
 #include "internal.h"
 #include "physics.cuh"
 #include "rng.cuh"
@@ -378,6 +379,10 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                 const uint32_t ia = __shfl_sync(kFull, rec_inc, src);
                 double* out = P.sums + (static_cast<size_t>(ia) * P.n_rx + P.rx_index) * P.nf * 8;
                 for (uint32_t f = lane; f < P.nf; f += 32) {
+                    if (P.xsums) {
+                        exact_add_global(P, P.xsums + ((out - P.sums) + f * 8) * 3, f, am, sp);
+                        continue;
+                    }
                     const Cx z = freq_phasor(P, f, sp);
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) {

@@ -38,7 +38,9 @@ def allreduce_finalize(sums, counters, freqs, n: int, group=None):
     """Sum raw accumulators / counters over the process group, finalize on host.
 
     sums: torch float64 tensor with n * nf * 8 elements ([n][nf][4] complex,
-    the device layout); counters: torch int64 tensor of MCSBR_COUNTER_WORDS.
+    the device layout), or for MCSBR_REDUCE_EXACT jobs an int64 tensor of
+    n * nf * 8 * MCSBR_EXACT_LIMBS limbs (summed exactly by the integer
+    all-reduce); counters: torch int64 tensor of MCSBR_COUNTER_WORDS.
     Works with any backend (NCCL for CUDA tensors, gloo for CPU tensors).
     Returns (values complex [n][4][nf], mcsbr_stats).
     """
@@ -64,12 +66,18 @@ def allreduce_finalize(sums, counters, freqs, n: int, group=None):
         counters[7] = rounds
     freqs = np.ascontiguousarray(np.asarray(freqs, dtype=np.float64).reshape(-1))
     nf = len(freqs)
-    raw = np.ascontiguousarray(sums.detach().to("cpu", torch.float64).numpy())
     values = np.zeros((n, 4, nf, 2), dtype=np.float64)
     L = A.lib()
-    A.check(L.mcsbr_gpu_finalize(raw.ctypes.data_as(C.POINTER(C.c_double)), n,
-                                 freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
-                                 values.ctypes.data_as(C.POINTER(C.c_double))))
+    if sums.dtype == torch.int64:  # MCSBR_REDUCE_EXACT: integer limbs, summed exactly over ranks
+        raw = np.ascontiguousarray(sums.detach().cpu().numpy())
+        A.check(L.mcsbr_gpu_finalize_exact(raw.ctypes.data_as(C.POINTER(C.c_int64)), n,
+                                           freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
+                                           values.ctypes.data_as(C.POINTER(C.c_double))))
+    else:
+        raw = np.ascontiguousarray(sums.detach().to("cpu", torch.float64).numpy())
+        A.check(L.mcsbr_gpu_finalize(raw.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                     freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
+                                     values.ctypes.data_as(C.POINTER(C.c_double))))
     cnt = np.ascontiguousarray(counters.detach().cpu().numpy().astype(np.uint64))
     st = A.Stats()
     rc = L.mcsbr_gpu_decode_counters(cnt.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(st))
@@ -99,7 +107,9 @@ def sweep_sharded(scene, incidences, receivers, frequencies, config, occlusion_e
     n_rx = len(receivers[0])
     inc_arr = (A.Incidence * n_inc)(*[e.incidence(spw) for e, spw in incidences])
     rx_arr = (A.Receiver * (n_inc * n_rx))(*[r.receiver() for rl in receivers for r in rl])
-    sums = torch.zeros(n_inc * n_rx * len(freqs) * 8, dtype=torch.float64, device=dev)
+    exact = int(config.reduction) == A.MCSBR_REDUCE_EXACT
+    sums = (torch.zeros(n_inc * n_rx * len(freqs) * 8 * A.MCSBR_EXACT_LIMBS, dtype=torch.int64, device=dev) if exact
+            else torch.zeros(n_inc * n_rx * len(freqs) * 8, dtype=torch.float64, device=dev))
     counters = torch.zeros(A.MCSBR_COUNTER_WORDS, dtype=torch.int64, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     cfg = config.to_c()

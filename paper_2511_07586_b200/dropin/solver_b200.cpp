@@ -287,6 +287,10 @@ McResult estimate(const Scene& scene, const Excitation& excitation, const std::v
     c.p_min = config.p_min;
     c.block_size = config.block_size;
     c.rng_mode = MCSBR_RNG_REFERENCE;  // the reference's per-ray stream
+    // order-independent integer sums: sweeps (and the runner's CSV artifacts)
+    // byte-identical across reruns and worker counts, as the reference's
+    // fixed-order block merge makes them (solver_mc.cpp:212-216, runner.hpp:2-5)
+    c.reduction = MCSBR_REDUCE_EXACT;
     const uint32_t nf = static_cast<uint32_t>(frequencies.size());
     std::vector<double> values(8ull * nf);
     mcsbr_stats st;

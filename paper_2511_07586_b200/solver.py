@@ -122,6 +122,11 @@ class RngMode(enum.IntEnum):
     PHILOX = A.MCSBR_RNG_PHILOX        # statistical mode
 
 
+class Reduction(enum.IntEnum):
+    FAST = A.MCSBR_REDUCE_FAST    # fp64 atomics (summation order varies run to run)
+    EXACT = A.MCSBR_REDUCE_EXACT  # 192-bit fixed-point integer sums: byte-reproducible
+
+
 @dataclass
 class RouletteConfig:
     enabled: bool = False
@@ -143,6 +148,8 @@ class McConfig:
     jitter: bool = True
     block_size: int = 8192
     rng_mode: RngMode = RngMode.REFERENCE
+    reduction: Reduction = Reduction.FAST
+    parity_fp64_refine: bool = True
 
     def to_c(self) -> A.McConfigC:
         c = A.McConfigC()
@@ -160,6 +167,8 @@ class McConfig:
         c.p_min = float(self.p_min)
         c.block_size = int(self.block_size)
         c.rng_mode = int(self.rng_mode)
+        c.reduction = int(self.reduction)
+        c.parity_fp64_refine = 1 if self.parity_fp64_refine else 0
         return c
 
     def validate(self) -> None:

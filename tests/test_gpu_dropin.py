@@ -216,3 +216,19 @@ def test_dropin_contribution_order_matches_reference():
     got = oracle._estimate(L.ref_solve, L.ref_last_error, dh.h, exc, freqs, dcfg, True, 1 << 20, 4)
     want = oracle.ref_solve(oracle.ref_scene(sd), exc, freqs, dcfg, 4, True, 1 << 20)
     assert contribs_identical(got["contributions"], want["contributions"])
+
+
+@pytest.mark.parametrize("solver", ["mc", "deterministic"])
+def test_dropin_artifacts_byte_identical_across_reruns_and_workers(tmp_path, solver):
+    """The reference's reproducibility promise (runner.hpp:2-5,
+    tests/test_cli_config.cpp:95-123: sweep.csv byte-identical across reruns
+    and worker counts) through the drop-in: its solvers sum exactly
+    (MCSBR_REDUCE_EXACT), so the GPU artifacts are byte-identical too."""
+    cfg = _cfg() if solver == "mc" else _cfg(
+        solver={"type": "deterministic", "deterministic": {"rays_per_wavelength": 6, "max_bounce": 7}})
+    outs = []
+    for k, workers in enumerate((4, 4, 1, 3)):
+        d = str(tmp_path / f"run{k}")
+        assert oracle.ref_run_command("sweep", cfg, d, workers, None, lib=oracle.dropin()) == 0
+        outs.append(_read(d, "sweep.csv", "rb"))
+    assert all(o == outs[0] for o in outs[1:])

@@ -155,3 +155,53 @@ def test_excitation_bases():
     assert np.allclose(e.pol_v, [0, 0, -1], atol=1e-15) and np.allclose(e.pol_h, [0, 1, 0])
     b = M.bistatic_excitation(90.0, 0.0, 0.0, 0.0)
     assert np.allclose(b.k_scatter, [0, 0, 1])
+
+
+def _limbs(x: float) -> list:
+    """The 192-bit fixed-point pattern (LSB 2^-120) of x as 4 limbs of 48 bits
+    (csrc/fixedpoint.cuh), from Python integers."""
+    from fractions import Fraction
+
+    v = int(Fraction(x) * (1 << 120))  # exact, truncated toward zero
+    v &= (1 << 192) - 1  # two's complement
+    return [(v >> (48 * i)) & ((1 << 48) - 1) for i in range(4)]
+
+
+def test_exact_limbs_finalize_on_host():
+    """mcsbr_gpu_finalize_exact: limbs summed over 'ranks' (plain int64 adds,
+    as an integer all-reduce does) decode to the exact sum of the terms and
+    finalize like mcsbr_gpu_finalize."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2511_07586_b200 import _abi as A
+
+    rng = np.random.default_rng(7)
+    n, nf = 2, 3
+    terms = rng.normal(size=(5, n * nf * 8)) * 10.0 ** rng.integers(-9, 4, size=(5, n * nf * 8))
+    terms[0, :4] = [0.0, -0.0, 1.5, -2.75]
+    limbs = np.zeros((n * nf * 8, 4), dtype=np.int64)
+    for rank in range(5):
+        limbs += np.array([_limbs(float(x)) for x in terms[rank]], dtype=np.int64)
+    freqs = np.array([1e9, 2e9, 3.5e9])
+    got = np.zeros((n, 4, nf, 2))
+    L = A.lib()
+    A.check(L.mcsbr_gpu_finalize_exact(np.ascontiguousarray(limbs).ctypes.data_as(C.POINTER(C.c_int64)), n,
+                                       freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
+                                       got.ctypes.data_as(C.POINTER(C.c_double))))
+    raw = np.ascontiguousarray(terms.sum(axis=0))
+    want = np.zeros_like(got)
+    A.check(L.mcsbr_gpu_finalize(raw.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                 freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
+                                 want.ctypes.data_as(C.POINTER(C.c_double))))
+    assert np.allclose(got, want, rtol=1e-13, atol=1e-30)
+    # a single exact value decodes exactly
+    one = np.zeros((n * nf * 8, 4), dtype=np.int64)
+    one[0] = _limbs(-2.75)
+    out = np.zeros((n, 4, nf, 2))
+    A.check(L.mcsbr_gpu_finalize_exact(one.ctypes.data_as(C.POINTER(C.c_int64)), n,
+                                       freqs.ctypes.data_as(C.POINTER(C.c_double)), nf,
+                                       out.ctypes.data_as(C.POINTER(C.c_double))))
+    k0 = 2 * np.pi * freqs[0] / 299792458.0
+    assert out[0, 0, 0, 1] == -2.75 * (1.0 * k0 / (2.0 * np.sqrt(np.pi)))
