@@ -230,6 +230,24 @@ MCSBR_API int mcsbr_gpu_scene_create(const double* vertices_xyz, uint32_t n_vert
                            const double* eps_imag, int device, mcsbr_scene** out);
 MCSBR_API void mcsbr_gpu_scene_destroy(mcsbr_scene* scene);
 
+/* A scene on several devices (replaces run_blocks' worker threads,
+ * proj/src/solver_common.cpp:70-89, by GPUs): the BVH is built once on
+ * devices[0] and its arrays are copied to devices[1..] (peer copies over
+ * NVLink).  estimate() with workers = w shards every incidence's launch
+ * entries over min(w, n_devices) devices (workers <= 0: all of them),
+ * estimate_batch() over all of them; one host thread and stream per device,
+ * partial sums added on the host in device order (MCSBR_REDUCE_EXACT: the
+ * result is byte-identical to a single device's).  Parity instrumentation
+ * (contributions, path logs) and the deterministic solver run on devices[0].
+ * A device may be listed more than once (independent streams on one GPU). */
+MCSBR_API int mcsbr_gpu_scene_create_multi(const double* vertices_xyz, uint32_t n_vertices,
+                                           const mcsbr_triangle* triangles, uint32_t n_triangles,
+                                           const mcsbr_material* materials, uint32_t n_materials,
+                                           const double* eps_imag, const int* devices, int n_devices,
+                                           mcsbr_scene** out);
+MCSBR_API int mcsbr_gpu_scene_devices(const mcsbr_scene* scene, int* n_devices);
+MCSBR_API int mcsbr_gpu_device_count(int* n_devices);
+
 /* Scene::diameter / bounding_center / bounding_radius (geometry.hpp:77-80). */
 MCSBR_API int mcsbr_gpu_scene_bounds(const mcsbr_scene* scene, double center[3], double* radius,
                            double* diameter);
@@ -261,8 +279,9 @@ MCSBR_API int mcsbr_gpu_intersect_device(const mcsbr_scene* scene, const double*
 /* The drop-in: one Excitation, host buffers in and out.  values receives
  * [4][nf] complex (interleaved) sqrt(m^2) values, channel order VV,HH,VH,HV,
  * finalized with j*k0/(2 sqrt(pi)) as SweepAccumulator::finalize does
- * (farfield.cpp:154-167).  `workers` is accepted for signature parity and
- * ignored.  If contributions != NULL, up to capacity records are written
+ * (farfield.cpp:154-167).  `workers`: the number of the scene's devices to
+ * shard over (see mcsbr_gpu_scene_create_multi; 1 for a single-device
+ * scene).  If contributions != NULL, up to capacity records are written
  * sorted by order_key (the reference emits them in block order, which is the
  * same order for one block) and *n_contributions receives the total count. */
 MCSBR_API int mcsbr_gpu_estimate(mcsbr_scene* scene, const mcsbr_excitation* excitation,
@@ -285,7 +304,8 @@ MCSBR_API int mcsbr_gpu_solve(mcsbr_scene* scene, const mcsbr_excitation* excita
                               mcsbr_stats* stats, mcsbr_contribution* contributions,
                               uint64_t capacity, uint64_t* n_contributions);
 
-/* Batched sweeps in ONE device launch: n_inc incidences, each observed by
+/* Batched sweeps in ONE device launch (per device of a multi-device scene):
+ * n_inc incidences, each observed by
  * n_rx receivers (receivers[i*n_rx + r]); occlusion applies to all.  values
  * receives [n_inc][n_rx][4][nf] complex.  Equivalent to n_inc*n_rx calls of
  * mcsbr_gpu_estimate except that each incidence is traced once for all its

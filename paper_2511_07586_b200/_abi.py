@@ -181,6 +181,13 @@ SIGNATURES = {
          C.POINTER(C.c_void_p)],
     ),
     "mcsbr_gpu_scene_destroy": (None, [C.c_void_p]),
+    "mcsbr_gpu_scene_create_multi": (
+        C.c_int,
+        [_DP, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, _DP, C.POINTER(C.c_int), C.c_int,
+         C.POINTER(C.c_void_p)],
+    ),
+    "mcsbr_gpu_scene_devices": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    "mcsbr_gpu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "mcsbr_gpu_scene_bounds": (C.c_int, [C.c_void_p, _DP, _DP, _DP]),
     "mcsbr_gpu_scene_bvh_info": (C.c_int, [C.c_void_p, _U32P, _U32P, _U32P, _DP]),
     "mcsbr_gpu_launch_plan": (

@@ -214,6 +214,10 @@ struct DevBuf {
 }  // namespace
 
 struct mcsbr_scene {
+    // multi-device scenes (mcsbr_gpu_scene_create_multi): this object is the
+    // primary (devices[0], where the BVH was built); replicas hold copies of
+    // the device arrays on devices[1..] and share nothing else
+    std::vector<mcsbr_scene*> replicas;
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
@@ -1020,8 +1024,100 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     return MCSBR_OK;
 }
 
+// A replica of the primary scene p on `device`: the device arrays copied
+// from p's device (peer copies over NVLink when the devices differ), no
+// second BVH build.
+static int make_replica(mcsbr_scene* p, int device, mcsbr_scene** out) {
+    *out = nullptr;
+    CK(cudaSetDevice(p->device), "cudaSetDevice");
+    CK(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
+    CK(cudaSetDevice(device), "cudaSetDevice");
+    auto* r = new mcsbr_scene();
+    r->device = device;
+    r->vtx = p->vtx;
+    r->nv = p->nv;
+    r->nt = p->nt;
+    r->nm = p->nm;
+    std::memcpy(r->center, p->center, sizeof(r->center));
+    r->radius = p->radius;
+    r->diameter = p->diameter;
+    r->ambient_n = p->ambient_n;
+    r->all_pec = p->all_pec;
+    r->lossy = p->lossy;
+    r->bvh = p->bvh;
+    r->bvh.nodes = nullptr;
+    r->bvh.tri64 = nullptr;
+    auto fail = [&](cudaError_t e, const char* what) {
+        mcsbr_gpu_scene_destroy(r);
+        return cuda_err(e, what);
+    };
+    cudaError_t e = cudaDeviceGetAttribute(&r->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return fail(e, "cudaDeviceGetAttribute");
+    if ((e = cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate");
+    auto copy = [&](auto** dst, const auto* src, size_t bytes) {
+        cudaError_t e2 = dev_malloc(dst, bytes);
+        if (e2 == cudaSuccess) e2 = cudaMemcpyPeerAsync(*dst, device, src, p->device, bytes, r->stream);
+        return e2;
+    };
+    if ((e = copy(&r->bvh.nodes, p->bvh.nodes, sizeof(float4) * 8 * std::max<uint32_t>(p->bvh.n_nodes, 1))) !=
+            cudaSuccess ||
+        (e = copy(&r->bvh.tri64, p->bvh.tri64, sizeof(double2) * 5 * p->bvh.n_leaves)) != cudaSuccess ||
+        (e = copy(&r->d_info, p->d_info, sizeof(double2) * 2 * p->nt)) != cudaSuccess ||
+        (e = copy(&r->d_mat, p->d_mat, sizeof(double2) * p->nm)) != cudaSuccess ||
+        (e = copy(&r->d_tri32, p->d_tri32, sizeof(float) * 9 * p->nt)) != cudaSuccess ||
+        (p->d_nim && (e = copy(&r->d_nim, p->d_nim, sizeof(double) * p->nm)) != cudaSuccess))
+        return fail(e, "replica copy");
+    if ((e = cudaStreamSynchronize(r->stream)) != cudaSuccess) return fail(e, "replica copy");
+    *out = r;
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_scene_create_multi(const double* xyz, uint32_t nv, const mcsbr_triangle* tris, uint32_t nt,
+                                 const mcsbr_material* mats, uint32_t nm, const double* eps_imag, const int* devices,
+                                 int n_devices, mcsbr_scene** out) {
+    if (!out) return set_err(MCSBR_EINVAL, "scene_create: null output");
+    *out = nullptr;
+    if (!devices || n_devices < 1) return set_err(MCSBR_EINVAL, "scene_create_multi: empty device list");
+    int rc = mcsbr_gpu_scene_create(xyz, nv, tris, nt, mats, nm, eps_imag, devices[0], out);
+    if (rc) return rc;
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    for (int i = 1; i < n_devices; ++i) {
+        mcsbr_scene* r = nullptr;
+        rc = devices[i] < 0 || devices[i] >= ndev ? set_err(MCSBR_EINVAL, "scene_create: bad device index")
+                                                  : make_replica(*out, devices[i], &r);
+        if (rc) {
+            mcsbr_gpu_scene_destroy(*out);
+            *out = nullptr;
+            return rc;
+        }
+        (*out)->replicas.push_back(r);
+    }
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_scene_devices(const mcsbr_scene* s, int* n_devices) {
+    if (!s || !n_devices) return set_err(MCSBR_EINVAL, "null argument");
+    *n_devices = 1 + static_cast<int>(s->replicas.size());
+    return MCSBR_OK;
+}
+
+int mcsbr_gpu_device_count(int* n) {
+    if (!n) return set_err(MCSBR_EINVAL, "null argument");
+    *n = 0;
+    const cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+        *n = 0;
+        return cuda_err(e, "cudaGetDeviceCount");
+    }
+    return MCSBR_OK;
+}
+
 void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     if (!s) return;
+    for (mcsbr_scene* r : s->replicas) mcsbr_gpu_scene_destroy(r);
+    s->replicas.clear();
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
     dev_free(s->d_vtx);
@@ -1131,15 +1227,141 @@ int mcsbr_gpu_intersect_device(const mcsbr_scene* s, const double* d_o, const do
     return MCSBR_OK;
 }
 
+// Counter blocks of several shards: sums, except the fault bits (OR) and
+// the deepest round (max).
+static void merge_counters(unsigned long long* dst, const unsigned long long* src) {
+    for (int i = 0; i < kCntWords; ++i) {
+        if (i == kCntFault) dst[i] |= src[i];
+        else if (i == kCntRounds) dst[i] = std::max(dst[i], src[i]);
+        else dst[i] += src[i];
+    }
+}
+
+// One shard of a multi-device job on replica `r` (its own device, stream and
+// buffers), on the calling host thread; raw sums (or exact limbs) and
+// counters come back to the host.
+struct ShardOut {
+    int rc = MCSBR_OK;
+    std::string err;
+    std::vector<double> raw;
+    std::vector<long long> limbs;
+    unsigned long long cnt[kCntWords] = {};
+    float kms = 0.f;
+    uint64_t launches = 0;
+};
+
+static void run_shard(mcsbr_scene* r, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs, uint32_t n_rx,
+               int occlusion, const double* freqs, uint32_t nf, const mcsbr_mc_config* cfg, uint32_t shard,
+               uint32_t nshard, ShardOut* o) {
+    const uint64_t launches0 = g_launches;
+    auto fail = [&](int rc) {
+        o->rc = rc;
+        o->err = g_err;
+    };
+    auto cuda_fail = [&](cudaError_t e, const char* what) { fail(cuda_err(e, what)); };
+    cudaError_t e = cudaSetDevice(r->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    Job job;
+    int rc = plan_job(r, incs, n_inc, rxs, n_rx, freqs, nf, cfg, shard, nshard, r->sms * 16, &job);
+    if (rc) return fail(rc);
+    const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
+    const bool exact = cfg->reduction == MCSBR_REDUCE_EXACT;
+    if ((e = r->sums.reserve(nsum)) != cudaSuccess || (e = r->counters.reserve(kCntWords)) != cudaSuccess ||
+        (exact && (e = r->limbs.reserve(nsum * MCSBR_EXACT_LIMBS)) != cudaSuccess))
+        return cuda_fail(e, "dev_malloc(shard sums)");
+    if ((e = cudaMemsetAsync(r->sums.p, 0, sizeof(double) * nsum, r->stream)) != cudaSuccess ||
+        (e = cudaMemsetAsync(r->counters.p, 0, sizeof(unsigned long long) * kCntWords, r->stream)) != cudaSuccess ||
+        (exact && (e = cudaMemsetAsync(r->limbs.p, 0, sizeof(long long) * nsum * MCSBR_EXACT_LIMBS, r->stream)) !=
+                      cudaSuccess))
+        return cuda_fail(e, "memset shard sums");
+    rc = run_job(r, job, nf, cfg, occlusion, r->sums.p, r->counters.p, r->stream, nullptr, &o->kms,
+                 exact ? r->limbs.p : nullptr);
+    if (rc) return fail(rc);
+    if (exact) {
+        o->limbs.resize(nsum * MCSBR_EXACT_LIMBS);
+        e = cudaMemcpyAsync(o->limbs.data(), r->limbs.p, sizeof(long long) * o->limbs.size(), cudaMemcpyDeviceToHost,
+                            r->stream);
+    } else {
+        o->raw.resize(nsum);
+        e = cudaMemcpyAsync(o->raw.data(), r->sums.p, sizeof(double) * nsum, cudaMemcpyDeviceToHost, r->stream);
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(o->cnt, r->counters.p, sizeof(o->cnt), cudaMemcpyDeviceToHost, r->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(r->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "shard readback");
+    o->launches = g_launches - launches0;
+}
+
+// estimate / estimate_batch over `ndev` devices of a multi-device scene:
+// launch entries sharded exactly as mcsbr_gpu_trace_device shards them
+// (every device a contiguous share of every incidence), one host thread per
+// device, partial sums added on the host in device order (exact limbs add
+// exactly: the result is byte-identical to one device's).
+static int estimate_multi(mcsbr_scene* s, uint32_t ndev, const mcsbr_incidence* incs, uint32_t n_inc,
+                   const mcsbr_receiver* rxs, uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
+                   const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats,
+                   std::chrono::steady_clock::time_point t0) {
+    std::vector<ShardOut> outs(ndev);
+    std::vector<std::thread> pool;
+    for (uint32_t d = 0; d < ndev; ++d) {
+        mcsbr_scene* r = d == 0 ? s : s->replicas[d - 1];
+        pool.emplace_back(run_shard, r, incs, n_inc, rxs, n_rx, occlusion, freqs, nf, cfg, d, ndev, &outs[d]);
+    }
+    for (auto& t : pool) t.join();
+    for (const ShardOut& o : outs) {
+        g_launches += o.launches;
+        if (o.rc) return set_err(o.rc, o.err);
+    }
+    const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
+    std::vector<double> raw(nsum, 0.0);
+    unsigned long long cnt[kCntWords] = {};
+    float kms = 0.f;
+    if (cfg->reduction == MCSBR_REDUCE_EXACT) {
+        std::vector<long long> limbs(nsum * MCSBR_EXACT_LIMBS, 0);
+        for (const ShardOut& o : outs)
+            for (size_t i = 0; i < limbs.size(); ++i) limbs[i] += o.limbs[i];
+        limbs_to_doubles(limbs.data(), nsum, raw.data());
+    } else {
+        for (const ShardOut& o : outs)
+            for (size_t i = 0; i < nsum; ++i) raw[i] += o.raw[i];
+    }
+    for (const ShardOut& o : outs) {
+        merge_counters(cnt, o.cnt);
+        kms = std::max(kms, o.kms);
+    }
+    int rc = fault_check(cnt);
+    if (rc) return rc;
+    finalize_values(raw.data(), n_inc * n_rx, freqs, nf, values);
+    if (stats) {
+        decode(cnt, stats);
+        stats->block_size = static_cast<uint64_t>(cfg->block_size);
+        uint64_t threads = 0;
+        for (uint32_t d = 0; d < ndev; ++d) threads += static_cast<uint64_t>((d == 0 ? s : s->replicas[d - 1])->sms) * 2048;
+        stats->peak_live_state_bytes = threads * stats->state_bytes_per_ray;
+        stats->kernel_ms = kms;
+        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return MCSBR_OK;
+}
+
 static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc, const mcsbr_receiver* rxs,
                            uint32_t n_rx, int occlusion, const double* freqs, uint32_t nf,
                            const mcsbr_mc_config* cfg, double* values, mcsbr_stats* stats,
                            mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs,
-                           const PathLog* plog = nullptr, const mcsbr_det_config* det = nullptr) {
+                           const PathLog* plog = nullptr, const mcsbr_det_config* det = nullptr,
+                           int workers = 0) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!s) return set_err(MCSBR_EINVAL, "null scene");
     int rc = use_device(s);
     if (rc) return rc;
+    // several devices: workers <= 0 means all of the scene's devices
+    const uint32_t have = 1 + static_cast<uint32_t>(s->replicas.size());
+    const uint32_t ndev = workers <= 0 ? have : std::min<uint32_t>(have, static_cast<uint32_t>(workers));
+    if (ndev > 1 && !contribs && !(plog && plog->n) && !det) {
+        rc = validate(cfg);
+        if (rc) return rc;
+        return estimate_multi(s, ndev, incs, n_inc, rxs, n_rx, occlusion, freqs, nf, cfg, values, stats, t0);
+    }
     Job job;
     rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, 0, 1, s->sms * 16, &job, det != nullptr);
     if (rc) return rc;
@@ -1301,7 +1523,6 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
 int mcsbr_gpu_estimate(mcsbr_scene* s, const mcsbr_excitation* exc, const double* freqs, uint32_t nf,
                        const mcsbr_mc_config* cfg, int workers, double* values, mcsbr_stats* stats,
                        mcsbr_contribution* contribs, uint64_t capacity, uint64_t* n_contribs) {
-    (void)workers;
     if (!exc) return set_err(MCSBR_EINVAL, "estimate: null excitation");
     mcsbr_incidence inc;
     std::memcpy(inc.k_inc, exc->k_inc, sizeof(inc.k_inc));
@@ -1313,7 +1534,7 @@ int mcsbr_gpu_estimate(mcsbr_scene* s, const mcsbr_excitation* exc, const double
     std::memcpy(rx.rx_v, exc->rx_v, sizeof(rx.rx_v));
     std::memcpy(rx.rx_h, exc->rx_h, sizeof(rx.rx_h));
     return estimate_common(s, &inc, 1, &rx, 1, exc->occlusion_enabled, freqs, nf, cfg, values, stats, contribs,
-                           capacity, n_contribs);
+                           capacity, n_contribs, nullptr, nullptr, workers < 1 ? 1 : workers);
 }
 
 void mcsbr_gpu_default_det_config(mcsbr_det_config* c) {

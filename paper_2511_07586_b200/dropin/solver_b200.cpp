@@ -64,6 +64,21 @@ int device_index() {
     return e ? std::atoi(e) : 0;
 }
 
+// The GPUs the solvers shard over (estimate's `workers` picks how many):
+// MCSBR_DEVICE first, then every other visible device; MCSBR_DEVICES=1 keeps
+// one.  run_blocks' worker threads (solver_common.cpp:70-89) become devices.
+std::vector<int> device_list() {
+    int n = 0;
+    mcsbr_gpu_device_count(&n);
+    const int first = device_index();
+    std::vector<int> d{first};
+    const char* lim = std::getenv("MCSBR_DEVICES");
+    const int want = lim ? std::max(1, std::atoi(lim)) : n;
+    for (int i = 0; i < n && static_cast<int>(d.size()) < want; ++i)
+        if (i != first) d.push_back(i);
+    return d;
+}
+
 // ---- device-resident scenes --------------------------------------------------
 // A Scene is immutable after finalize(); the runner re-uses one Scene for a
 // whole angle sweep / ISAR, so the uploaded geometry + BVH is cached by
@@ -121,11 +136,13 @@ mcsbr_scene* device_scene(const Scene& s) {
         mats[i].is_pec = s.materials[i].is_pec ? 1 : 0;
     }
     mcsbr_scene* dev = nullptr;
-    check(mcsbr_gpu_scene_create(reinterpret_cast<const double*>(s.vertices.data()),
-                                 static_cast<uint32_t>(s.vertices.size()),
-                                 reinterpret_cast<const mcsbr_triangle*>(s.triangles.data()),
-                                 static_cast<uint32_t>(s.triangles.size()), mats.data(),
-                                 static_cast<uint32_t>(mats.size()), nullptr, device_index(), &dev));
+    const std::vector<int> devs = device_list();
+    check(mcsbr_gpu_scene_create_multi(reinterpret_cast<const double*>(s.vertices.data()),
+                                       static_cast<uint32_t>(s.vertices.size()),
+                                       reinterpret_cast<const mcsbr_triangle*>(s.triangles.data()),
+                                       static_cast<uint32_t>(s.triangles.size()), mats.data(),
+                                       static_cast<uint32_t>(mats.size()), nullptr, devs.data(),
+                                       static_cast<int>(devs.size()), &dev));
     g_cache.push_front({&s, s.vertices.data(), s.triangles.data(), s.vertices.size(), s.triangles.size(),
                         s.materials.size(), h, dev});
     while (g_cache.size() > kCacheScenes) {

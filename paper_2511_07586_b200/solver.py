@@ -306,18 +306,25 @@ class Scene:
     handle created by ``mcsbr_gpu_scene_create`` (upload + GPU BVH build).
     """
 
-    def __init__(self, data: SceneData, device: int = 0):
+    def __init__(self, data: SceneData, device: int = 0, devices: list | None = None):
+        """device: the GPU; devices: several GPUs (mcsbr_gpu_scene_create_multi:
+        BVH built on devices[0], copied to the others; estimate / estimate_batch
+        shard the launch entries over them)."""
         self.data = data
-        self.device = device
+        self.devices = list(devices) if devices else [device]
+        self.device = self.devices[0]
         self._h = C.c_void_p()
         L = A.lib()
         v = np.ascontiguousarray(data.vertices, dtype=np.float64)
         eps_i = data.eps_imag
-        _raise(L.mcsbr_gpu_scene_create(
-            v.ctypes.data_as(C.POINTER(C.c_double)), len(v), data.triangles.ctypes.data,
-            len(data.triangles), data.materials.ctypes.data, len(data.materials),
-            eps_i.ctypes.data_as(C.POINTER(C.c_double)) if eps_i is not None else None,
-            device, C.byref(self._h)))
+        args = (v.ctypes.data_as(C.POINTER(C.c_double)), len(v), data.triangles.ctypes.data,
+                len(data.triangles), data.materials.ctypes.data, len(data.materials),
+                eps_i.ctypes.data_as(C.POINTER(C.c_double)) if eps_i is not None else None)
+        if len(self.devices) == 1:
+            _raise(L.mcsbr_gpu_scene_create(*args, self.device, C.byref(self._h)))
+        else:
+            dv = (C.c_int * len(self.devices))(*self.devices)
+            _raise(L.mcsbr_gpu_scene_create_multi(*args, dv, len(self.devices), C.byref(self._h)))
 
     @property
     def handle(self):
