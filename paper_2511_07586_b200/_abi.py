@@ -265,7 +265,10 @@ def lib() -> C.CDLL:
                 "(there is no CPU fallback)"
             )
         L = C.CDLL(LIB_PATH)
+        lenient = os.environ.get("MCSBR_ABI_LENIENT") == "1"  # A/B tooling: older library builds
         for name, (res, args) in SIGNATURES.items():
+            if lenient and not hasattr(L, name):
+                continue
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

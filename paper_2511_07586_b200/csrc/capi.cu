@@ -623,7 +623,8 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // so its jobs are not culled
     std::vector<IncDev> incs = job.inc;
     const bool det_job = extra && extra->det;
-    const bool cull = !det_job && env_u32("MCSBR_COVER", 1) != 0;
+    // only the deferred-accumulation kernels cull (trace.cu kCull)
+    const bool cull = !det_job && (nf > 1 || exact) && env_u32("MCSBR_COVER", 1) != 0;
     uint64_t cover_words = 0;
     for (IncDev& d : incs) {
         d.cover_off = kNoCover;

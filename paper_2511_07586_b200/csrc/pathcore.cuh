@@ -771,24 +771,19 @@ __device__ __forceinline__ Cx freq_phasor(const TraceParams& P, uint32_t f, NT s
 
 constexpr int kRecD2 = 6;  // contribution record: 6 double2 = 96 B (amp[4], s, incidence)
 
-// MCSBR_REDUCE_EXACT: the 8 terms (channel re / im) of one contribution at
-// frequency f, each rounded once to 192-bit fixed point (fixedpoint.cuh) and
-// added into the accumulators at g (device atomics with carries) -- the
-// same value whichever kernel adds it, so the integer sums are exact
-template <typename NT>
-__device__ __forceinline__ void exact_add_global(const TraceParams& P, unsigned long long* g, uint32_t f,
-                                                 const Cx am[4], NT sp) {
-    const Cx z = freq_phasor(P, f, sp);
-    bool ok = true;
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
-        const Cx v = am[ch] * z;
-        uint64_t w[3];
-        ok = mcsbr_fx::fx_from_double(v.re, w) && ok;
-        mcsbr_fx::fx_atomic_add(g + (2 * ch) * 3, w);
-        ok = mcsbr_fx::fx_from_double(v.im, w) && ok;
-        mcsbr_fx::fx_atomic_add(g + (2 * ch + 1) * 3, w);
+// Record-buffer overflow: one term added straight into the sums -- an fp64
+// atomic, or under MCSBR_REDUCE_EXACT the term rounded once to 192-bit fixed
+// point (fixedpoint.cuh) and added with carries into P.xsums (the same value
+// accumulate_exact_kernel adds for a stored record, so the integer sums stay
+// exact).  `out` is this incidence's block of P.sums, k the value's index in it.
+__device__ __forceinline__ void add_value(const TraceParams& P, double* out, uint32_t k, double v) {
+    if (!P.xsums) {
+        atomicAdd(out + k, v);
+        return;
     }
-    if (!ok) atomicOr(P.counters + kCntFault, static_cast<unsigned long long>(kFaultFixedRange));
+    uint64_t w[3];
+    if (!mcsbr_fx::fx_from_double(v, w))
+        atomicOr(P.counters + kCntFault, static_cast<unsigned long long>(kFaultFixedRange));
+    mcsbr_fx::fx_atomic_add(P.xsums + ((out - P.sums) + k) * 3, w);
 }
 

@@ -93,6 +93,10 @@ struct MinBlocks {
 template <int kMode, bool kDiel, bool kLossy, bool kDet>
 __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value)) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeDefer;
+    // launch-ray culling by the coverage bitmaps (cover.cu): the deferred-
+    // accumulation Monte Carlo kernels (large ISAR scenes); run_job builds
+    // bitmaps only for those
+    constexpr bool kCull = kMode == kModeDefer && !kDet;
     using NT = typename std::conditional<kLossy, Cx, double>::type;
     using L = Layout<!kDiel && !kLossy, kLossy, kRegAcc>;
     using EF = typename std::conditional<L::pec, V3, CV3>::type;  // field type
@@ -245,6 +249,46 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
             // skipped at once; the lanes keep drawing until they hold a path
             // or the incidence's entries are used up.
             unsigned need = __ballot_sync(kFull, !alive);
+            if (!kCull) {
+                // register-sum / fan kernels (F = 1: small, cache-resident
+                // scenes) regenerate in one pass without the bitmap: the
+                // culling loop's registers cost them more than it saves
+                if (need && cursor >= e_end) {
+                    if (q[0] >= q[1]) fetch();
+                    const uint64_t n0 = q[0], n1 = q[1];
+                    if (n0 < n1 && n0 >= I.g_begin && n0 < g_end_a) {
+                        cursor = I.entry_begin + (n0 - I.g_begin);
+                        e_end = I.entry_begin + (min(n1, g_end_a) - I.g_begin);
+                        __syncwarp();
+                        if (lane == 0) q[0] = min(n1, g_end_a);
+                        __syncwarp();
+                    }
+                }
+                if (need && cursor < e_end) {
+                    const unsigned rank = __popc(need & ((1u << lane) - 1u));
+                    const uint64_t mine = cursor + rank;
+                    if (!alive && mine < e_end) {
+                        init_path(P, I, a + P.inc_base, locate(P, I, mine), s, s_rcp[warp]);
+                        save_em<L>(sl, s);
+                        alive = true;
+                        ++n_launched;
+                        if (kDet) {  // a new root ray (solver_det.cpp:72-82)
+                            const uint64_t blk = s.cell / P.det_block_size;
+                            dacc_peak += dpeak;
+                            if (blk != dblk) {
+                                det_flush(P, dblk, dacc_peak, dacc_push);
+                                dacc_peak = dacc_push = 0;
+                                dblk = blk;
+                            }
+                            dpeak = 1;
+                            dacc_push += 1;
+                            dev = 0;
+                        }
+                    }
+                    cursor = min(cursor + static_cast<uint64_t>(__popc(need)), e_end);
+                }
+                need = 0;
+            }
             while (need) {
                 if (cursor >= e_end) {
                     // sub-range dry: continue with the next chunk if it is the same incidence
@@ -260,7 +304,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                         break;
                     }
                 }
-                if (!kDet && P.cover && I.cover_off != kNoCover) {
+                if (kCull && P.cover && I.cover_off != kNoCover) {
                     const uint64_t c2 = skip_uncovered(P.cover + I.cover_off, I.cover_shift, cursor, e_end);
                     if (lane == 0) n_miss0 += c2 - cursor;  // warp-uniform run, counted once
                     cursor = c2;
@@ -269,7 +313,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                 const unsigned rank = __popc(need & ((1u << lane) - 1u));
                 const uint64_t mine = cursor + rank;
                 if (!alive && mine < e_end) {
-                    if (!kDet && !covered(P, I, mine)) {
+                    if (kCull && !covered(P, I, mine)) {
                         ++n_miss0;  // provable miss: one launched ray, one bounce-0 segment
                     } else {
                         init_path(P, I, a + P.inc_base, locate(P, I, mine), s, s_rcp[warp]);
@@ -644,16 +688,12 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                         }
                         const NT sp = shfl_nt(s_path, src);
                         for (uint32_t f = lane; f < P.nf; f += 32) {
-                            if (P.xsums) {
-                                exact_add_global(P, P.xsums + ((out - P.sums) + f * 8) * 3, f, am, sp);
-                                continue;
-                            }
                             const Cx z = freq_phasor(P, f, sp);
 #pragma unroll
                             for (int ch = 0; ch < 4; ++ch) {
                                 const Cx v = am[ch] * z;
-                                atomicAdd(out + f * 8 + 2 * ch, v.re);
-                                atomicAdd(out + f * 8 + 2 * ch + 1, v.im);
+                                add_value(P, out, f * 8 + 2 * ch, v.re);
+                                add_value(P, out, f * 8 + 2 * ch + 1, v.im);
                             }
                         }
                     }
@@ -677,7 +717,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
         return v;
     };
-    if (!kDet && n_miss0) atomicAdd(&s_bounce[0], static_cast<unsigned int>(n_miss0));
+    if (kCull && n_miss0) atomicAdd(&s_bounce[0], static_cast<unsigned int>(n_miss0));
     n_launched = wsum(n_launched + n_miss0);
     n_miss0 = wsum(n_miss0);
     n_contrib = wsum(n_contrib);

@@ -379,16 +379,12 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                 const uint32_t ia = __shfl_sync(kFull, rec_inc, src);
                 double* out = P.sums + (static_cast<size_t>(ia) * P.n_rx + P.rx_index) * P.nf * 8;
                 for (uint32_t f = lane; f < P.nf; f += 32) {
-                    if (P.xsums) {
-                        exact_add_global(P, P.xsums + ((out - P.sums) + f * 8) * 3, f, am, sp);
-                        continue;
-                    }
                     const Cx z = freq_phasor(P, f, sp);
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) {
                         const Cx v = am[ch] * z;
-                        atomicAdd(out + f * 8 + 2 * ch, v.re);
-                        atomicAdd(out + f * 8 + 2 * ch + 1, v.im);
+                        add_value(P, out, f * 8 + 2 * ch, v.re);
+                        add_value(P, out, f * 8 + 2 * ch + 1, v.im);
                     }
                 }
             }

@@ -63,6 +63,9 @@ rows.insert(0, ["Kernel Name"])
 hdr = rows[1]
 ai, si, ii = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 data = [(int(r[ai], 16), int(r[si] or 0), int(r[ii] or 0)) for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")]
+stall_cols = [(h, hdr.index(h)) for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+stall_by_addr = {int(r[ai], 16): {h: int(r[c] or 0) for h, c in stall_cols}
+                 for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")}
 base = min(a for a, _, _ in data)
 
 # regions: each starts at the first trace.cu line containing its marker and
@@ -78,7 +81,7 @@ MARKERS = [
     ("chi/queue", "// ---- chi visibility"), ("accumulate/records", "// ---- bistatic fan"),
     ("counters", "// ---- counters ----"), ("accumulate_kernel", "accumulate_kernel(TraceParams P"),
 ]
-src = open(os.path.join(ROOT, "paper_2511_07586_b200/csrc/trace.cu")).read().splitlines()
+src = open(os.environ.get("MCSBR_TRACE_SRC", os.path.join(ROOT, "paper_2511_07586_b200/csrc/trace.cu"))).read().splitlines()
 REGIONS = []
 starts = []
 for name, mk in MARKERS:
@@ -108,8 +111,19 @@ for a, s, i in data:
 ts = sum(v[0] for v in agg.values()) or 1
 ti = sum(v[1] for v in agg.values()) or 1
 print(f"{len(data)} SASS instructions ({len(data) * 16 / 1024:.0f} KB), {ts} samples, {ti:.3e} warp inst")
+stall_reg = {}
+for a, s_, i in data:
+    r = region(ctx_line.get(a - base, (None, None, 0))[2])
+    d = stall_reg.setdefault(r, {})
+    for h, v in stall_by_addr.get(a, {}).items():
+        d[h] = d.get(h, 0) + v
 for r, (s, i, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
     print(f"{r:22s} {100 * s / ts:5.1f}% samples  {100 * i / ti:5.1f}% inst  {n:5d} sass ({n * 16 / 1024:.1f} KB)")
+    d = stall_reg.get(r, {})
+    tot = sum(d.values()) or 1
+    top = sorted(d.items(), key=lambda kv: -kv[1])[:6]
+    if s / ts > 0.02:
+        print("      " + "  ".join(f"{h[6:]} {100 * v / tot:.0f}%" for h, v in top))
 
 if len(sys.argv) > 4:  # top SASS instructions of one region
     want = sys.argv[4]

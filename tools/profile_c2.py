@@ -27,9 +27,14 @@ scene = M.Scene(sd)
 lam = bench.C0 / W.freqs[-1]
 spws = [bench.spw_for(M, scene, e, lam, W.rays) for e in excs]
 cfg = W.config(M)
-for it in range(2):
+L = A.lib()
+for it in range(3):
+    L.mcsbr_gpu_kernel_timing(1)
     vals, st = M.estimate_batch(scene, [(e, s) for e, s in zip(excs, spws)], [[e] for e in excs],
                                 W.freqs, cfg)
-print(f"paths {st.rays_launched} kernel_ms {st.kernel_ms:.3f} "
+pk = C.c_double()
+L.mcsbr_gpu_kernel_times(C.byref(pk), None, None, None)
+L.mcsbr_gpu_kernel_timing(0)
+print(f"paths {st.rays_launched} kernel_ms {st.kernel_ms:.3f} path_kernel_ms {pk.value:.3f} "
       f"Gpaths/s {st.rays_launched / st.kernel_ms / 1e6:.3f} segments {st.segments_traced} "
       f"occlusion {st.occlusion_queries}")
