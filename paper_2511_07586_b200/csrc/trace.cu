@@ -770,12 +770,18 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
 // Sums use fused multiply-adds (their order differs from the reference's
 // anyway); the records of one span are nearly always one incidence, and the
 // sums are flushed with fp64 atomics whenever the incidence changes.
-template <int FPL, bool kRealAmp>
+// kUniform: the uniform-grid recurrence (P.uniform_f, compile time);
+// kFull: every lane owns all FPL of its frequencies (nf - f_begin >= 32 FPL),
+// so the per-frequency bounds tests drop out of the inner loop.
+template <int FPL, bool kRealAmp, bool kUniform, bool kFull>
 __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t f_begin) {
     // staged record: [0..3] amplitudes, [4] (ph0, dph) | s, [5] (la0, dla),
     // [6] W = e^{-j 32 dk s}, [7] incidence.  (Measured and rejected: a
     // per-record table of w^r, w^4q replacing the lane's sincos by two
     // complex multiplies -- c5 +3.5%, the table doubles the shared memory.)
+    // (Measured and rejected as well: W^2 .. W^(FPL-1) staged per record so
+    // a lane forms its phasors by independent products instead of the
+    // recurrence chain -- c5 +2%.)
     constexpr int kSt = 8;
     __shared__ double2 st[4][32][kSt];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -787,6 +793,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
     span = span < 512 ? 512 : span;
     const uint32_t f_end = min(P.nf, f_begin + 32u * FPL);
     const uint32_t f0 = f_begin + static_cast<uint32_t>(lane);
+    const double f0d = static_cast<double>(f0);
     double acc[FPL][8];
     const double2* recs = reinterpret_cast<const double2*>(P.recs);
     auto cmul = [](Cx x, Cx y) { return Cx{__fma_rn(x.re, y.re, -x.im * y.im), __fma_rn(x.re, y.im, x.im * y.re)}; };
@@ -807,7 +814,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                 const uint32_t f = f0 + 32u * m;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    if (f < f_end && acc[m][k] != 0.0) atomicAdd(out + f * 8 + k, acc[m][k]);
+                    if ((kFull || f < f_end) && acc[m][k] != 0.0) atomicAdd(out + f * 8 + k, acc[m][k]);
                     acc[m][k] = 0.0;
                 }
             }
@@ -821,7 +828,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                 for (int ch = 0; ch < 4; ++ch) t[ch] = __ldcs(r + ch);
                 const double2 sv = __ldcs(r + 4);
                 t[7] = __ldcs(r + 5);
-                if (P.uniform_f) {
+                if (kUniform) {
                     const double ph0 = P.kph0 * sv.x, dph = P.kdph * sv.x;
                     const double la0 = -(P.kph0 * sv.y), dla = -(P.kdph * sv.y);
                     t[4] = make_double2(ph0, dph);
@@ -839,12 +846,12 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                     flush();
                     cur = a;
                 }
-                if (f0 >= f_end) continue;
+                if (!kFull && f0 >= f_end) continue;
                 Cx z, w = {1.0, 0.0};
                 const double2 t4 = t[4];
-                if (P.uniform_f) {
+                if (kUniform) {
                     const double2 t5 = t[5];
-                    z = polar_la(t4.x + static_cast<double>(f0) * t4.y, t5.x + static_cast<double>(f0) * t5.y);
+                    z = polar_la(t4.x + f0d * t4.y, t5.x + f0d * t5.y);
                     if (FPL > 1) w = cx2(t[6]);
                 } else {
                     z = phasor(P.k0[f0], Cx{t4.x, t4.y});
@@ -855,7 +862,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
 #pragma unroll
                 for (int m = 0; m < FPL; ++m) {
                     const uint32_t f = f0 + 32u * m;
-                    if (f < f_end) {
+                    if (kFull || f < f_end) {
 #pragma unroll
                         for (int ch = 0; ch < 4; ++ch) {
                             if (kRealAmp) {  // PEC scenes: the amplitudes are real
@@ -868,8 +875,8 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                                     __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
                             }
                         }
-                        if (m + 1 < FPL && f + 32u < f_end) {
-                            if (P.uniform_f) z = cmul(z, w);
+                        if (m + 1 < FPL && (kFull || f + 32u < f_end)) {
+                            if (kUniform) z = cmul(z, w);
                             else z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
                         }
                     }
@@ -1038,15 +1045,27 @@ cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t
     const uint32_t fpl = p.nf <= 32 ? 1 : (p.nf <= 64 ? 2 : 4);
     const bool real_amp = p.scene.all_pec && !p.scene.lossy;  // PEC paths carry real amplitudes
     for (uint32_t fb = 0; fb < p.nf; fb += 32 * fpl) {
-        if (real_amp) {
-            if (fpl == 1) accumulate_kernel<1, true><<<blocks, 128, 0, stream>>>(p, fb);
-            else if (fpl == 2) accumulate_kernel<2, true><<<blocks, 128, 0, stream>>>(p, fb);
-            else accumulate_kernel<4, true><<<blocks, 128, 0, stream>>>(p, fb);
+        const bool full = p.nf - fb >= 32 * fpl;
+        const unsigned code = (real_amp ? 4u : 0u) | (p.uniform_f ? 2u : 0u) | (full ? 1u : 0u);
+#define MCSBR_ACC(F)                                                                                 \
+    switch (code) {                                                                                  \
+        case 0: accumulate_kernel<F, false, false, false><<<blocks, 128, 0, stream>>>(p, fb); break; \
+        case 1: accumulate_kernel<F, false, false, true><<<blocks, 128, 0, stream>>>(p, fb); break;  \
+        case 2: accumulate_kernel<F, false, true, false><<<blocks, 128, 0, stream>>>(p, fb); break;  \
+        case 3: accumulate_kernel<F, false, true, true><<<blocks, 128, 0, stream>>>(p, fb); break;   \
+        case 4: accumulate_kernel<F, true, false, false><<<blocks, 128, 0, stream>>>(p, fb); break;  \
+        case 5: accumulate_kernel<F, true, false, true><<<blocks, 128, 0, stream>>>(p, fb); break;   \
+        case 6: accumulate_kernel<F, true, true, false><<<blocks, 128, 0, stream>>>(p, fb); break;   \
+        default: accumulate_kernel<F, true, true, true><<<blocks, 128, 0, stream>>>(p, fb); break;   \
+    }
+        if (fpl == 1) {
+            MCSBR_ACC(1)
+        } else if (fpl == 2) {
+            MCSBR_ACC(2)
         } else {
-            if (fpl == 1) accumulate_kernel<1, false><<<blocks, 128, 0, stream>>>(p, fb);
-            else if (fpl == 2) accumulate_kernel<2, false><<<blocks, 128, 0, stream>>>(p, fb);
-            else accumulate_kernel<4, false><<<blocks, 128, 0, stream>>>(p, fb);
+            MCSBR_ACC(4)
         }
+#undef MCSBR_ACC
         if (launches) ++*launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

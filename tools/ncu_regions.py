@@ -53,7 +53,8 @@ rows_all = list(csv.reader(io.StringIO(out)))
 rows, take = [], False
 for r in rows_all:
     if r and r[0] == "Kernel Name":
-        take = kern.split("ILi")[0].split("_")[-1] in r[1].replace(" ", "") or kern in r[1]
+        base_name = kern.split("ILi")[0]
+        take = (base_name + "<") in r[1] or (base_name + "(") in r[1] or kern in r[1]
         if take and rows:
             break  # first matching kernel only
         continue
