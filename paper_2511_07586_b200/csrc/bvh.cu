@@ -1017,9 +1017,11 @@ static cudaError_t esc_references(const double* d_vertices, const uint4* d_tri_i
             *ref_tri = *ref_piece = nullptr;
         }
     }
-    dev_free(extra);
-    dev_free(off);
-    dev_free(tmp);
+    // esc_refs_kernel reads extra / off: wait for it, then free without a device sync
+    const bool synced = e == cudaSuccess && cudaStreamSynchronize(stream) == cudaSuccess;
+    dev_free(extra, synced);
+    dev_free(off, synced);
+    dev_free(tmp, synced);
     return e;
 }
 
@@ -1197,31 +1199,33 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         out->build_ms = ms;
     }
 done:
-    dev_free(ref_tri);
-    dev_free(ref_piece);
-    dev_free(keys);
-    dev_free(keys_s);
-    dev_free(ids);
-    dev_free(ids_s);
-    dev_free(blo);
-    dev_free(bhi);
-    dev_free(blo_s);
-    dev_free(bhi_s);
-    dev_free(ilo);
-    dev_free(ihi);
-    dev_free(child);
-    dev_free(range);
-    dev_free(par_i);
-    dev_free(par_l);
-    dev_free(flags);
-    dev_free(dmax);
-    dev_free(is4);
-    dev_free(idx4);
-    dev_free(tmp);
-    dev_free(scan_tmp);
-    dev_free(sidx);
-    dev_free(tasks);
-    dev_free(node_counter);
+    // on success the stream was synchronised by the readback above
+    const bool synced = err == cudaSuccess;
+    dev_free(ref_tri, synced);
+    dev_free(ref_piece, synced);
+    dev_free(keys, synced);
+    dev_free(keys_s, synced);
+    dev_free(ids, synced);
+    dev_free(ids_s, synced);
+    dev_free(blo, synced);
+    dev_free(bhi, synced);
+    dev_free(blo_s, synced);
+    dev_free(bhi_s, synced);
+    dev_free(ilo, synced);
+    dev_free(ihi, synced);
+    dev_free(child, synced);
+    dev_free(range, synced);
+    dev_free(par_i, synced);
+    dev_free(par_l, synced);
+    dev_free(flags, synced);
+    dev_free(dmax, synced);
+    dev_free(is4, synced);
+    dev_free(idx4, synced);
+    dev_free(tmp, synced);
+    dev_free(scan_tmp, synced);
+    dev_free(sidx, synced);
+    dev_free(tasks, synced);
+    dev_free(node_counter, synced);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (err != cudaSuccess) {

@@ -37,17 +37,36 @@ struct AllocCache {
     std::mutex m;
     std::unordered_map<void*, std::pair<int, size_t>> size_of;  // live and cached blocks
     std::multimap<size_t, void*> free_blocks[64];               // per device: size -> block
-    size_t cached = 0;
+    size_t cached[64] = {};                                     // per device: bytes held in free_blocks
+    size_t limit[64] = {};                                      // per device: cache bound (0 = not yet known)
 };
 AllocCache& alloc_cache() {
     static AllocCache* c = new AllocCache();  // never destroyed (used during process exit)
     return *c;
 }
-constexpr size_t kCacheLimit = size_t{4} << 30;
+// a sixth of the device's memory (B200: ~30 GB): large enough to keep a
+// sweep's multi-GB contribution-record buffer between scenes (a cudaFree of
+// it costs up to ~0.5 s), small enough to leave the device to others
+size_t cache_limit(AllocCache& c, int dev) {
+    if (!c.limit[dev]) {
+        size_t free_b = 0, total = 0;
+        c.limit[dev] = cudaMemGetInfo(&free_b, &total) == cudaSuccess ? total / 6 : (size_t{4} << 30);
+    }
+    return c.limit[dev];
+}
 size_t alloc_class(size_t n) {
     n = n ? n : 1;
     const size_t g = n >= (size_t{1} << 20) ? (size_t{1} << 16) : 256;  // 64 KB / 256 B granules
     return (n + g - 1) / g * g;
+}
+// hand device dev's cached blocks back to the driver (caller holds the lock)
+void release_cached(AllocCache& c, int dev) {
+    for (auto& kv : c.free_blocks[dev]) {
+        cudaFree(kv.second);
+        c.size_of.erase(kv.second);
+    }
+    c.free_blocks[dev].clear();
+    c.cached[dev] = 0;
 }
 }  // namespace
 
@@ -56,45 +75,41 @@ cudaError_t dev_malloc(void** p, size_t bytes) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    const bool cacheable = dev >= 0 && dev < 64;
     const size_t n = alloc_class(bytes);
     AllocCache& c = alloc_cache();
-    {
+    if (cacheable) {
         std::lock_guard<std::mutex> g(c.m);
-        if (dev >= 0 && dev < 64) {
-            auto& fb = c.free_blocks[dev];
-            auto it = fb.lower_bound(n);
-            if (it != fb.end() && it->first <= 2 * n) {  // reuse a block at most twice the size
-                *p = it->second;
-                c.cached -= it->first;
-                fb.erase(it);
-                return cudaSuccess;
-            }
+        auto& fb = c.free_blocks[dev];
+        auto it = fb.lower_bound(n);
+        if (it != fb.end() && it->first <= 2 * n) {  // reuse a block at most twice the size
+            *p = it->second;
+            c.cached[dev] -= it->first;
+            fb.erase(it);
+            return cudaSuccess;
         }
     }
     e = cudaMalloc(p, n);
-    if (e != cudaSuccess) {
-        // out of memory: hand the cache back to the driver and retry once
+    if (e != cudaSuccess && cacheable) {
+        // out of memory: hand this device's cache back to the driver and retry once
         cudaGetLastError();
         {
             std::lock_guard<std::mutex> g(c.m);
-            for (auto& kv : c.free_blocks[dev]) {
-                cudaFree(kv.second);
-                c.size_of.erase(kv.second);
-            }
-            c.cached = 0;
-            c.free_blocks[dev].clear();
+            release_cached(c, dev);
         }
         e = cudaMalloc(p, n);
-        if (e != cudaSuccess) return e;
     }
+    if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> g(c.m);
     c.size_of[*p] = {dev, n};
     return cudaSuccess;
 }
 
-void dev_free(void* p) {
+void dev_free(void* p, bool synced) {
     if (!p) return;
-    cudaDeviceSynchronize();  // the block may be read by work still in flight
+    // the block may be read by work still in flight; callers that have
+    // synchronised the streams that used it pass synced = true
+    if (!synced) cudaDeviceSynchronize();
     AllocCache& c = alloc_cache();
     std::lock_guard<std::mutex> g(c.m);
     auto it = c.size_of.find(p);
@@ -104,13 +119,13 @@ void dev_free(void* p) {
     }
     const int dev = it->second.first;
     const size_t n = it->second.second;
-    if (dev < 0 || dev >= 64 || c.cached + n > kCacheLimit) {
+    if (dev < 0 || dev >= 64 || c.cached[dev] + n > cache_limit(c, dev)) {
         c.size_of.erase(it);
         cudaFree(p);
         return;
     }
     c.free_blocks[dev].emplace(n, p);
-    c.cached += n;
+    c.cached[dev] += n;
 }
 
 }  // namespace mcsbr_int
@@ -204,8 +219,8 @@ struct DevBuf {
         if (e == cudaSuccess) n = want;
         return e;
     }
-    void release() {
-        if (p) dev_free(p);
+    void release(bool synced = false) {
+        if (p) dev_free(p, synced);
         p = nullptr;
         n = 0;
     }
@@ -221,8 +236,8 @@ struct mcsbr_scene {
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
-    std::vector<double> vtx;
     uint32_t nv = 0, nt = 0, nm = 0;
+    double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // vertex AABB
     double center[3] = {0, 0, 0};
     double radius = 0.0, diameter = 0.0;
     double ambient_n = 1.0;
@@ -252,6 +267,8 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
+    DevBuf<double> plan_axes;              // launch planning (prep.cu): axes in,
+    DevBuf<unsigned long long> plan_ext;   // projection extents out
     DevBuf<unsigned long long> xsums;  // MCSBR_REDUCE_EXACT: 192-bit sums of the current job
     DevBuf<long long> limbs;           // MCSBR_REDUCE_EXACT: their limbs (estimate / estimate_batch)
     // wavefront path pool (wavefront.cu): fields, (kind, rid, list), control words
@@ -290,24 +307,42 @@ namespace {
 // scenes up to this many triangles get the long scheduling chunks (run_job)
 constexpr uint32_t kSmallSceneTris = 131072;
 
-// launch_rect (geometry.cpp:246-275) + build_strata (solver_mc.cpp:19-31)
-int plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw, double lambda_ref,
-         int32_t spp, mcsbr_launch_plan* out) {
-    const V k = normalized(ld(k_inc));
+// launch_rect's axes (geometry.cpp:246-253): seed axis x, or y if |k.x| > 0.9
+void plan_axes(const double k_inc[3], V* k, V* u, V* v) {
+    *k = normalized(ld(k_inc));
     V seed{1.0, 0.0, 0.0};
-    if (std::abs(k.x) > 0.9) seed = V{0.0, 1.0, 0.0};
-    const V u = normalized(cross(k, seed));
-    const V v = cross(k, u);
-    double ulo = 1e300, uhi = -1e300, vlo = 1e300, vhi = -1e300;
-    for (uint32_t i = 0; i < s->nv; ++i) {
-        const V p = ld(&s->vtx[3ull * i]);
-        const double pu = dot(p, u);
-        const double pv = dot(p, v);
-        ulo = std::min(ulo, pu);
-        uhi = std::max(uhi, pu);
-        vlo = std::min(vlo, pv);
-        vhi = std::max(vhi, pv);
-    }
+    if (std::abs(k->x) > 0.9) seed = V{0.0, 1.0, 0.0};
+    *u = normalized(cross(*k, seed));
+    *v = cross(*k, *u);
+}
+
+// launch_rect's projection extents (min / max of dot(p, u), dot(p, v) over
+// the vertices, geometry.cpp:254-266) of n incidences at once on the device
+// (prep.cu extents_kernel, the host loop's exact arithmetic); ext[4a..4a+3] =
+// (ulo, uhi, vlo, vhi)
+int plan_extents(const mcsbr_scene* s, const std::vector<double>& axes, std::vector<double>* ext) {
+    const uint32_t n = static_cast<uint32_t>(axes.size() / 6);
+    auto* ms = const_cast<mcsbr_scene*>(s);
+    CK(ms->plan_axes.reserve(axes.size()), "dev_malloc(plan axes)");
+    CK(ms->plan_ext.reserve(4ull * n), "dev_malloc(plan extents)");
+    CK(cudaMemcpyAsync(ms->plan_axes.p, axes.data(), sizeof(double) * axes.size(), cudaMemcpyHostToDevice, s->stream),
+       "upload plan axes");
+    CK(launch_extents(s->d_vtx, s->nv, ms->plan_axes.p, n, ms->plan_ext.p, s->sms, s->stream), "extents launch");
+    ++g_launches;
+    std::vector<unsigned long long> o(4ull * n);
+    CK(cudaMemcpyAsync(o.data(), ms->plan_ext.p, sizeof(unsigned long long) * o.size(), cudaMemcpyDeviceToHost,
+                       s->stream), "plan extents readback");
+    CK(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    ext->resize(o.size());
+    for (size_t i = 0; i < o.size(); ++i) (*ext)[i] = unord(o[i]);
+    return MCSBR_OK;
+}
+
+// launch_rect (geometry.cpp:246-275) from its axes and extents + build_strata
+// (solver_mc.cpp:19-31)
+int plan_finish(const mcsbr_scene* s, V k, V u, V v, const double* ext, double padding, double spw, double lambda_ref,
+                int32_t spp, mcsbr_launch_plan* out) {
+    double ulo = ext[0], uhi = ext[1], vlo = ext[2], vhi = ext[3];
     ulo -= padding;
     uhi += padding;
     vlo -= padding;
@@ -331,6 +366,17 @@ int plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw
         return set_err(MCSBR_EINVAL, "build_strata: more than 2^32 strata per incidence");
     out->entries = cells * static_cast<uint64_t>(spp);
     return MCSBR_OK;
+}
+
+// one incidence
+int plan(const mcsbr_scene* s, const double k_inc[3], double padding, double spw, double lambda_ref, int32_t spp,
+         mcsbr_launch_plan* out) {
+    V k, u, v;
+    plan_axes(k_inc, &k, &u, &v);
+    std::vector<double> ext;
+    int rc = plan_extents(s, {u.x, u.y, u.z, v.x, v.y, v.z}, &ext);
+    if (rc) return rc;
+    return plan_finish(s, k, u, v, ext.data(), padding, spw, lambda_ref, spp, out);
 }
 
 int validate(const mcsbr_mc_config* c) {
@@ -392,7 +438,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 
 constexpr uint64_t kPathStateBytes = 192;
-constexpr uint64_t kRecCapMax = uint64_t{1} << 26;  // contribution records (96 B each): 6.4 GB
+constexpr uint64_t kRecCapMax = uint64_t{1} << 27;  // contribution records (96 B each): 12.9 GB
 constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: at most 256 MB per job
 
 // Fold the peak record count of the scene's previous F > 1 job (if its
@@ -450,35 +496,32 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     job->k0.resize(nf);
     for (uint32_t f = 0; f < nf; ++f) job->k0[f] = 2.0 * kPi * freqs[f] / kC;
     uint64_t total = 0;
-    // launch rectangles: O(vertices) each, independent per incidence -> host
-    // threads when the batch is large (an azimuth sweep); a failing incidence
-    // is re-planned on this thread so the error message lands here
+    // launch rectangles: the axes on the host, the O(vertices) projection
+    // extents of every incidence in one device pass (prep.cu)
     std::vector<mcsbr_launch_plan> plans(n_inc);
     std::vector<int> prc(n_inc, MCSBR_OK);
-    auto plan_range = [&](uint32_t a0, uint32_t a1) {
-        for (uint32_t a = a0; a < a1; ++a) {
+    {
+        std::vector<V> ks(n_inc), us(n_inc), vs(n_inc);
+        std::vector<double> axes(6ull * n_inc);
+        for (uint32_t a = 0; a < n_inc; ++a) {
+            plan_axes(incs[a].k_inc, &ks[a], &us[a], &vs[a]);
+            const double ax[6] = {us[a].x, us[a].y, us[a].z, vs[a].x, vs[a].y, vs[a].z};
+            std::memcpy(&axes[6ull * a], ax, sizeof(ax));
+        }
+        std::vector<double> ext;
+        int erc = plan_extents(s, axes, &ext);
+        if (erc) return erc;
+        for (uint32_t a = 0; a < n_inc; ++a) {
             const double spw_a = incs[a].strata_per_wavelength > 0.0 ? incs[a].strata_per_wavelength
                                                                        : cfg->strata_per_wavelength;
-            prc[a] = plan(s, incs[a].k_inc, cfg->launch_padding, spw_a, lambda_ref, cfg->samples_per_stratum,
-                          &plans[a]);
+            prc[a] = plan_finish(s, ks[a], us[a], vs[a], &ext[4ull * a], cfg->launch_padding, spw_a, lambda_ref,
+                                 cfg->samples_per_stratum, &plans[a]);
+            if (prc[a]) return prc[a];
         }
-    };
-    const uint64_t work = static_cast<uint64_t>(n_inc) * s->nv;
-    const uint32_t nthreads = work < 200000 ? 1u
-                              : std::min<uint32_t>(n_inc, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-    if (nthreads <= 1) {
-        plan_range(0, n_inc);
-    } else {
-        std::vector<std::thread> pool;
-        for (uint32_t t = 0; t < nthreads; ++t)
-            pool.emplace_back(plan_range, n_inc * t / nthreads, n_inc * (t + 1) / nthreads);
-        for (auto& th : pool) th.join();
     }
     for (uint32_t a = 0; a < n_inc; ++a) {
         const mcsbr_incidence& in = incs[a];
-        const double spw = in.strata_per_wavelength > 0.0 ? in.strata_per_wavelength : cfg->strata_per_wavelength;
         mcsbr_launch_plan lp = plans[a];
-        if (prc[a]) return plan(s, in.k_inc, cfg->launch_padding, spw, lambda_ref, cfg->samples_per_stratum, &lp);
         if (lp.entries == 0) return set_err(MCSBR_EINVAL, "estimate: empty strata grid");
         IncDev& d = job->inc[a];
         std::memset(&d, 0, sizeof(d));
@@ -898,13 +941,6 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
                                 !std::isfinite(mats[i].eps_r) || !std::isfinite(mats[i].mu_r)))
             return set_err(MCSBR_ESCENE, "material: eps_r and mu_r must be positive");
     }
-    for (uint32_t i = 0; i < nt; ++i) {
-        const mcsbr_triangle& t = tris[i];
-        if (t.v0 >= nv || t.v1 >= nv || t.v2 >= nv)
-            return set_err(MCSBR_ESCENE, "triangle " + std::to_string(i) + ": vertex index out of range");
-        if (t.front_material >= nm || t.back_material >= nm)
-            return set_err(MCSBR_ESCENE, "triangle " + std::to_string(i) + ": material index out of range");
-    }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -926,43 +962,10 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     s->nv = nv;
     s->nt = nt;
     s->nm = nm;
-    s->vtx.assign(xyz, xyz + 3ull * nv);
-    // Scene::finalize (geometry.cpp:146-162)
-    V lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
-    for (uint32_t i = 0; i < nv; ++i) {
-        const V v = ld(xyz + 3ull * i);
-        lo = {std::min(lo.x, v.x), std::min(lo.y, v.y), std::min(lo.z, v.z)};
-        hi = {std::max(hi.x, v.x), std::max(hi.y, v.y), std::max(hi.z, v.z)};
-    }
-    const V c = (lo + hi) * 0.5;
-    double r = 0.0;
-    for (uint32_t i = 0; i < nv; ++i) r = std::max(r, norm(ld(xyz + 3ull * i) - c));
-    st(s->center, c);
-    s->radius = r;
-    s->diameter = 2.0 * r;
-    if (!(s->diameter > 0.0)) {
-        delete s;
-        return set_err(MCSBR_ESCENE, "scene is degenerate (zero extent)");
-    }
     s->ambient_n = mats[0].is_pec ? 0.0 : std::sqrt(mats[0].eps_r * mats[0].mu_r);
-
-    std::vector<uint4> tri_idx(nt);
-    std::vector<double2> info(2ull * nt);
-    for (uint32_t i = 0; i < nt; ++i) {
-        tri_idx[i] = make_uint4(tris[i].v0, tris[i].v1, tris[i].v2, 0);
-        uint64_t packed = static_cast<uint64_t>(tris[i].front_material) |
-                          (static_cast<uint64_t>(tris[i].back_material) << 16) |
-                          (static_cast<uint64_t>(tris[i].exterior_facing ? 1 : 0) << 32);
-        double pd;
-        std::memcpy(&pd, &packed, sizeof(pd));
-        info[2ull * i] = make_double2(tris[i].normal[0], tris[i].normal[1]);
-        info[2ull * i + 1] = make_double2(tris[i].normal[2], pd);
-    }
-    s->all_pec = true;
-    for (uint32_t i = 0; i < nt && s->all_pec; ++i)
-        s->all_pec = mats[tris[i].front_material].is_pec || mats[tris[i].back_material].is_pec;
     std::vector<double2> mat(nm);
     std::vector<double> nim(nm, 0.0);
+    std::vector<uint8_t> is_pec(nm);
     s->lossy = eps_imag != nullptr;  // complex-permittivity transport requested
     for (uint32_t i = 0; i < nm; ++i) {
         double n_re = mats[i].is_pec ? 0.0 : std::sqrt(mats[i].eps_r * mats[i].mu_r);  // Material::index()
@@ -974,8 +977,8 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
             nim[i] = b / (2.0 * n_re);
         }
         mat[i] = make_double2(n_re, mats[i].is_pec ? 1.0 : 0.0);
+        is_pec[i] = mats[i].is_pec ? 1 : 0;
     }
-    if (s->lossy) s->all_pec = false;
 
     auto fail = [&](cudaError_t e2, const char* what) {
         mcsbr_gpu_scene_destroy(s);
@@ -990,12 +993,6 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     if ((e = cudaMemcpyAsync(s->d_vtx, xyz, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice, s->stream)) !=
         cudaSuccess)
         return fail(e, "upload vertices");
-    if ((e = cudaMemcpyAsync(s->d_tri, tri_idx.data(), sizeof(uint4) * nt, cudaMemcpyHostToDevice, s->stream)) !=
-        cudaSuccess)
-        return fail(e, "upload triangles");
-    if ((e = cudaMemcpyAsync(s->d_info, info.data(), sizeof(double2) * 2 * nt, cudaMemcpyHostToDevice, s->stream)) !=
-        cudaSuccess)
-        return fail(e, "upload tri info");
     if ((e = cudaMemcpyAsync(s->d_mat, mat.data(), sizeof(double2) * nm, cudaMemcpyHostToDevice, s->stream)) !=
         cudaSuccess)
         return fail(e, "upload materials");
@@ -1005,10 +1002,75 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
             cudaSuccess)
             return fail(e, "upload Im n");
     }
-    const double lo3[3] = {lo.x, lo.y, lo.z}, hi3[3] = {hi.x, hi.y, hi.z};
+    // Triangle checks + device layout, vertex bounds and the bounding sphere
+    // on the device (prep.cu): Scene::finalize (geometry.cpp:146-162)
+    {
+        mcsbr_triangle* d_raw = nullptr;
+        uint8_t* d_pec = nullptr;
+        unsigned long long* d_w = nullptr;  // [0] first bad, [1] not all PEC, [2..7] bounds, [8] radius
+        auto release = [&]() {
+            dev_free(d_raw);
+            dev_free(d_pec);
+            dev_free(d_w);
+        };
+        unsigned long long w[9];
+        if ((e = dev_malloc(&d_raw, sizeof(mcsbr_triangle) * nt)) != cudaSuccess ||
+            (e = dev_malloc(&d_pec, nm)) != cudaSuccess || (e = dev_malloc(&d_w, sizeof(w))) != cudaSuccess ||
+            (e = cudaMemcpyAsync(d_raw, tris, sizeof(mcsbr_triangle) * nt, cudaMemcpyHostToDevice, s->stream)) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(d_pec, is_pec.data(), nm, cudaMemcpyHostToDevice, s->stream)) != cudaSuccess ||
+            (e = cudaMemsetAsync(d_w, 0xff, sizeof(unsigned long long), s->stream)) != cudaSuccess ||
+            (e = cudaMemsetAsync(d_w + 1, 0, sizeof(unsigned long long), s->stream)) != cudaSuccess ||
+            (e = launch_pack(d_raw, nt, nv, nm, d_pec, s->d_tri, s->d_info, d_w,
+                             reinterpret_cast<unsigned int*>(d_w + 1), s->stream)) != cudaSuccess ||
+            (e = launch_bounds(s->d_vtx, nv, d_w + 2, s->sms, s->stream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(w, d_w, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, s->stream)) !=
+                cudaSuccess ||
+            (e = cudaStreamSynchronize(s->stream)) != cudaSuccess) {
+            release();
+            return fail(e, "scene preparation");
+        }
+        g_launches += 2;
+        if (w[0] != ~0ull) {
+            release();
+            mcsbr_gpu_scene_destroy(s);
+            const uint64_t i = w[0] >> 1;
+            return set_err(MCSBR_ESCENE, "triangle " + std::to_string(i) +
+                                             ((w[0] & 1) ? ": material index out of range"
+                                                         : ": vertex index out of range"));
+        }
+        s->all_pec = (w[1] & 0xffffffffull) == 0 && !s->lossy;
+        const V lo{unord(w[2]), unord(w[3]), unord(w[4])}, hi{unord(w[5]), unord(w[6]), unord(w[7])};
+        const V c = (lo + hi) * 0.5;
+        st(s->center, c);
+        if ((e = launch_radius(s->d_vtx, nv, s->center, d_w + 8, s->sms, s->stream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(&w[8], d_w + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream)) !=
+                cudaSuccess ||
+            (e = cudaStreamSynchronize(s->stream)) != cudaSuccess) {
+            release();
+            return fail(e, "scene preparation");
+        }
+        ++g_launches;
+        release();
+        const double r = unord(w[8]);
+        s->radius = r;
+        s->diameter = 2.0 * r;
+        s->scene_lo[0] = lo.x;
+        s->scene_lo[1] = lo.y;
+        s->scene_lo[2] = lo.z;
+        s->scene_hi[0] = hi.x;
+        s->scene_hi[1] = hi.y;
+        s->scene_hi[2] = hi.z;
+    }
+    if (!(s->diameter > 0.0)) {
+        mcsbr_gpu_scene_destroy(s);
+        return set_err(MCSBR_ESCENE, "scene is degenerate (zero extent)");
+    }
+    const double* lo3 = s->scene_lo;
+    const double* hi3 = s->scene_hi;
     // boxes: outward-rounded fp64 AABBs; the pad only absorbs the fp64
     // rounding of the centring (the slab test's margin lives on the ray)
-    const double box_pad = 1e-12 * r + 1e-30;
+    const double box_pad = 1e-12 * s->radius + 1e-30;
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
         return fail(e, "BVH build");
     g_launches += 7;
@@ -1035,7 +1097,6 @@ static int make_replica(mcsbr_scene* p, int device, mcsbr_scene** out) {
     CK(cudaSetDevice(device), "cudaSetDevice");
     auto* r = new mcsbr_scene();
     r->device = device;
-    r->vtx = p->vtx;
     r->nv = p->nv;
     r->nt = p->nt;
     r->nm = p->nm;
@@ -1067,6 +1128,7 @@ static int make_replica(mcsbr_scene* p, int device, mcsbr_scene** out) {
         (e = copy(&r->d_info, p->d_info, sizeof(double2) * 2 * p->nt)) != cudaSuccess ||
         (e = copy(&r->d_mat, p->d_mat, sizeof(double2) * p->nm)) != cudaSuccess ||
         (e = copy(&r->d_tri32, p->d_tri32, sizeof(float) * 9 * p->nt)) != cudaSuccess ||
+        (e = copy(&r->d_vtx, p->d_vtx, sizeof(double) * 3 * p->nv)) != cudaSuccess ||
         (p->d_nim && (e = copy(&r->d_nim, p->d_nim, sizeof(double) * p->nm)) != cudaSuccess))
         return fail(e, "replica copy");
     if ((e = cudaStreamSynchronize(r->stream)) != cudaSuccess) return fail(e, "replica copy");
@@ -1120,28 +1182,33 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     for (mcsbr_scene* r : s->replicas) mcsbr_gpu_scene_destroy(r);
     s->replicas.clear();
     cudaSetDevice(s->device);
-    if (s->stream) cudaStreamSynchronize(s->stream);
-    dev_free(s->d_vtx);
-    dev_free(s->d_tri);
-    dev_free(s->d_info);
-    dev_free(s->d_mat);
-    dev_free(s->d_nim);
-    dev_free(s->d_tri32);
-    dev_free(s->bvh.nodes);
-    dev_free(s->bvh.tri64);
-    s->inc.release();
-    s->rx.release();
-    s->k0.release();
-    s->sums.release();
-    s->counters.release();
-    s->tile.release();
-    s->recs.release();
-    s->cover.release();
-    s->xsums.release();
-    s->limbs.release();
-    s->wf_pool.release();
-    s->wf_u32.release();
-    s->wf_ctl.release();
+    // every stream that used the scene's buffers (its own, and callers' of
+    // trace_device / intersect_device) must be done: one device sync, then
+    // the frees need none each
+    cudaDeviceSynchronize();
+    dev_free(s->d_vtx, true);
+    dev_free(s->d_tri, true);
+    dev_free(s->d_info, true);
+    dev_free(s->d_mat, true);
+    dev_free(s->d_nim, true);
+    dev_free(s->d_tri32, true);
+    dev_free(s->bvh.nodes, true);
+    dev_free(s->bvh.tri64, true);
+    s->inc.release(true);
+    s->rx.release(true);
+    s->k0.release(true);
+    s->sums.release(true);
+    s->counters.release(true);
+    s->tile.release(true);
+    s->recs.release(true);
+    s->cover.release(true);
+    s->plan_axes.release(true);
+    s->plan_ext.release(true);
+    s->xsums.release(true);
+    s->limbs.release(true);
+    s->wf_pool.release(true);
+    s->wf_u32.release(true);
+    s->wf_ctl.release(true);
     if (s->wf_host) cudaFreeHost(s->wf_host);
     if (s->wf_ev) cudaEventDestroy(s->wf_ev);
     if (s->ev0) cudaEventDestroy(s->ev0);

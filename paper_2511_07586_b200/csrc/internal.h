@@ -161,7 +161,7 @@ constexpr int kDetFields = 24;  // origin 3, dir 3, e0 6, e1 6, phi 2, medium 2,
 // freed blocks are kept per device (bounded) and handed out again.  A free
 // synchronises the device first, so a cached block is never still in use.
 cudaError_t dev_malloc(void** p, size_t bytes);
-void dev_free(void* p);
+void dev_free(void* p, bool synced = false);
 template <typename T>
 inline cudaError_t dev_malloc(T** p, size_t bytes) {
     return dev_malloc(reinterpret_cast<void**>(p), bytes);
@@ -198,6 +198,21 @@ struct WfParams {
 constexpr int kWfFieldsHost = 41;
 cudaError_t launch_wavefront_iteration(const TraceParams& p, const WfParams& w, uint32_t iter, int device_sms,
                                        cudaStream_t stream);
+
+// prep.cu: scene preparation and launch planning on the device
+}  // namespace mcsbr_int
+struct mcsbr_triangle;
+namespace mcsbr_int {
+double unord(unsigned long long o);  // inverse of the order-preserving double -> uint64 map
+cudaError_t launch_pack(const mcsbr_triangle* d_raw, uint32_t nt, uint32_t nv, uint32_t nm, const uint8_t* d_is_pec,
+                        uint4* d_tri, double2* d_info, unsigned long long* d_first_bad, unsigned int* d_not_all_pec,
+                        cudaStream_t stream);
+cudaError_t launch_bounds(const double* d_vtx, uint32_t nv, unsigned long long* d_out, int device_sms,
+                          cudaStream_t stream);
+cudaError_t launch_radius(const double* d_vtx, uint32_t nv, const double c[3], unsigned long long* d_out,
+                          int device_sms, cudaStream_t stream);
+cudaError_t launch_extents(const double* d_vtx, uint32_t nv, const double* d_axes, uint32_t n_inc,
+                           unsigned long long* d_out, int device_sms, cudaStream_t stream);
 
 // cover.cu: launch-ray coverage bitmaps
 cudaError_t build_tri32(const double* d_vtx, const uint4* d_tri, uint32_t n, const double center[3], float* out,
