@@ -218,9 +218,11 @@ MCSBR_API int mcsbr_gpu_validate_config(const mcsbr_mc_config* cfg);
 typedef struct mcsbr_scene mcsbr_scene;
 
 /* Upload a finalized scene (the public data of mcsbr::Scene,
- * geometry.hpp:55-60) to `device` and build its BVH on the GPU (LBVH:
- * Morton codes, radix sort, Karras hierarchy, bottom-up fp64->fp32
- * outward-rounded refit).  `eps_imag` may be NULL (lossless, the reference
+ * geometry.hpp:55-60) to `device` and build its BVH on the GPU (binned-SAH
+ * top-down build from a Morton order with early split clipping of sliver
+ * triangles, collapsed to a 4-wide tree of outward-rounded fp32 boxes; the
+ * Karras LBVH is the fallback for trees deeper than the traversal stack).
+ * `eps_imag` may be NULL (lossless, the reference
  * model) or hold nm values of Im(eps_r) (e^{+jwt}: eps = eps_r - j eps_imag,
  * the GPU-only lossy extension).  Validates as Scene::finalize does
  * (geometry.cpp:146-162): empty or zero-extent scenes are rejected. */

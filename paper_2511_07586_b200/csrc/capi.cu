@@ -206,6 +206,23 @@ inline void st(double* p, V v) {
     p[2] = v.z;
 }
 
+// device temporaries of one call, freed on every exit path
+struct TempBufs {
+    std::vector<void*> p;
+    TempBufs() = default;
+    TempBufs(const TempBufs&) = delete;
+    TempBufs& operator=(const TempBufs&) = delete;
+    ~TempBufs() {
+        for (void* q : p) dev_free(q);
+    }
+    template <class T>
+    cudaError_t alloc(T** q, size_t bytes) {
+        const cudaError_t e = dev_malloc(q, bytes);
+        if (e == cudaSuccess) p.push_back(*q);
+        return e;
+    }
+};
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -707,8 +724,9 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // 4096 to 256); a small scene's BVH stays cache-resident whatever the
     // window, and fewer, longer chunks there save the per-chunk scheduling
     // and incidence changes (c2 -2.7% at 1024, -3.3% at 2048; c4 +4% at 512).
-    p.chunk_max = env_u32("MCSBR_CHUNK_MAX", s->nt <= kSmallSceneTris ? 2048u : 256u);
-    p.chunk_min = env_u32("MCSBR_CHUNK_MIN", 32);
+    // (A/B knobs sanitised: chunk sizes non-zero multiples of 32, min <= max)
+    p.chunk_max = std::max(32u, env_u32("MCSBR_CHUNK_MAX", s->nt <= kSmallSceneTris ? 2048u : 256u) / 32u * 32u);
+    p.chunk_min = std::min(p.chunk_max, std::max(32u, env_u32("MCSBR_CHUNK_MIN", 32) / 32u * 32u));
     p.gss_div = env_u32("MCSBR_GSS", 16);
     // band height of the launch-entry dispatch order (0 = linear; a power of two)
     {
@@ -1440,15 +1458,16 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     CK(cudaMemsetAsync(s->sums.p, 0, sizeof(double) * nsum, s->stream), "memset sums");
     CK(cudaMemsetAsync(s->counters.p, 0, sizeof(unsigned long long) * kCntWords, s->stream), "memset counters");
     TraceParams extra{};
+    TempBufs temps;  // instrumentation / deterministic-solver temporaries, freed on every exit
     mcsbr_contribution* d_out = nullptr;
     mcsbr_contribution* d_scratch = nullptr;
     unsigned long long* d_cnt = nullptr;
     if (contribs) {
         if (n_inc != 1 || n_rx != 1) return set_err(MCSBR_EINVAL, "contributions_out needs one incidence");
         const size_t scratch_n = static_cast<size_t>(s->sms) * 32 * 128;  // >= resident threads
-        CK(dev_malloc(&d_out, sizeof(mcsbr_contribution) * std::max<uint64_t>(capacity, 1)), "dev_malloc(contribs)");
-        CK(dev_malloc(&d_scratch, sizeof(mcsbr_contribution) * scratch_n), "dev_malloc(scratch)");
-        CK(dev_malloc(&d_cnt, sizeof(unsigned long long)), "dev_malloc(count)");
+        CK(temps.alloc(&d_out, sizeof(mcsbr_contribution) * std::max<uint64_t>(capacity, 1)), "dev_malloc(contribs)");
+        CK(temps.alloc(&d_scratch, sizeof(mcsbr_contribution) * scratch_n), "dev_malloc(scratch)");
+        CK(temps.alloc(&d_cnt, sizeof(unsigned long long)), "dev_malloc(count)");
         CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s->stream), "memset count");
         extra.contrib_out = d_out;
         extra.contrib_cap = capacity;
@@ -1460,9 +1479,9 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     unsigned long long* d_pbr = nullptr;
     if (plog && plog->n) {
         const size_t nt = plog->n * plog->stride;
-        CK(dev_malloc(&d_ptri, sizeof(uint32_t) * nt), "dev_malloc(plog)");
-        CK(dev_malloc(&d_pterm, plog->n), "dev_malloc(plog)");
-        CK(dev_malloc(&d_pbr, sizeof(unsigned long long) * plog->n), "dev_malloc(plog)");
+        CK(temps.alloc(&d_ptri, sizeof(uint32_t) * nt), "dev_malloc(plog)");
+        CK(temps.alloc(&d_pterm, plog->n), "dev_malloc(plog)");
+        CK(temps.alloc(&d_pbr, sizeof(unsigned long long) * plog->n), "dev_malloc(plog)");
         CK(cudaMemsetAsync(d_ptri, 0xff, sizeof(uint32_t) * nt, s->stream), "memset plog");
         CK(cudaMemsetAsync(d_pterm, 0, plog->n, s->stream), "memset plog");
         CK(cudaMemsetAsync(d_pbr, 0, sizeof(unsigned long long) * plog->n, s->stream), "memset plog");
@@ -1481,16 +1500,11 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         const uint32_t depth = static_cast<uint32_t>(det->max_bounce);
         stack_bytes = sizeof(double) * kDetFields * depth * threads;
         det_nblocks = (job.total_entries + det->block_size - 1) / static_cast<uint64_t>(det->block_size);
-        cudaError_t e0 = dev_malloc(&d_stack, stack_bytes);
-        if (e0 == cudaSuccess) e0 = dev_malloc(&d_blocks, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1));
+        cudaError_t e0 = temps.alloc(&d_stack, stack_bytes);
+        if (e0 == cudaSuccess) e0 = temps.alloc(&d_blocks, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1));
         if (e0 == cudaSuccess)
             e0 = cudaMemsetAsync(d_blocks, 0, sizeof(unsigned long long) * 2 * std::max<uint64_t>(det_nblocks, 1), s->stream);
         if (e0 != cudaSuccess) {
-            dev_free(d_stack);
-            dev_free(d_blocks);
-            dev_free(d_out);
-            dev_free(d_scratch);
-            dev_free(d_cnt);
             return cuda_err(e0, "dev_malloc(branch stacks)");
         }
         extra.det = 1;
@@ -1515,8 +1529,6 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
                                           cudaMemcpyDeviceToHost);
         if (e2 != cudaSuccess) rc = cuda_err(e2, "branch accounting readback");
     }
-    dev_free(d_stack);
-    dev_free(d_blocks);
     if (rc == MCSBR_OK && plog && plog->n) {
         cudaError_t e2 = cudaMemcpy(plog->tri, d_ptri, sizeof(uint32_t) * plog->n * plog->stride,
                                     cudaMemcpyDeviceToHost);
@@ -1525,13 +1537,7 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
             e2 = cudaMemcpy(plog->branch, d_pbr, sizeof(uint64_t) * plog->n, cudaMemcpyDeviceToHost);
         if (e2 != cudaSuccess) rc = cuda_err(e2, "path log readback");
     }
-    dev_free(d_ptri);
-    dev_free(d_pterm);
-    dev_free(d_pbr);
     if (rc) {
-        dev_free(d_out);
-        dev_free(d_scratch);
-        dev_free(d_cnt);
         return rc;
     }
     std::vector<double> raw(exact ? 0 : nsum);
@@ -1555,9 +1561,6 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         });
         if (n_contribs) *n_contribs = ncol;
     }
-    dev_free(d_out);
-    dev_free(d_scratch);
-    dev_free(d_cnt);
     if (e != cudaSuccess) return cuda_err(e, "estimate readback");
     rc = fault_check(cnt);
     if (rc) return rc;

@@ -16,6 +16,7 @@
 // One thread per output bin: the IDFTs are O(rows x M x N) with N, M <= a few
 // thousand, trivially parallel and L1-resident (the input row is shared by
 // all threads of a block).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -41,33 +42,34 @@ int sig_err(const std::string& m) {
 __global__ void idft_rows(const double2* __restrict__ in, uint32_t rows, uint32_t n, uint32_t m,
                           bool conjugate, double2* __restrict__ out) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;  // output bin (after the shift)
-    const uint32_t row = blockIdx.y;
-    if (j >= m || row >= rows) return;
+    if (j >= m) return;
     // center_shift rotates left by (m - m/2): shifted[j] = raw[(j + m - m/2) % m]
     const uint32_t mm = (j + (m - m / 2)) % m;
-    const double2* x = in + static_cast<size_t>(row) * n;
-    double re = 0.0, im = 0.0;
-    for (uint32_t k = 0; k < n; ++k) {
-        const double2 v = x[k];
-        if (v.x == 0.0 && v.y == 0.0) continue;
-        const uint64_t km = (static_cast<uint64_t>(k) * mm) % m;
-        double s, c;
-        sincospi(2.0 * static_cast<double>(km) / static_cast<double>(m), &s, &c);
-        if (conjugate) s = -s;
-        re += v.x * c - v.y * s;
-        im += v.x * s + v.y * c;
+    for (uint32_t row = blockIdx.y; row < rows; row += gridDim.y) {  // rows beyond the 65535 grid limit
+        const double2* x = in + static_cast<size_t>(row) * n;
+        double re = 0.0, im = 0.0;
+        for (uint32_t k = 0; k < n; ++k) {
+            const double2 v = x[k];
+            if (v.x == 0.0 && v.y == 0.0) continue;
+            const uint64_t km = (static_cast<uint64_t>(k) * mm) % m;
+            double s, c;
+            sincospi(2.0 * static_cast<double>(km) / static_cast<double>(m), &s, &c);
+            if (conjugate) s = -s;
+            re += v.x * c - v.y * s;
+            im += v.x * s + v.y * c;
+        }
+        const double scale = 1.0 / static_cast<double>(m);
+        out[static_cast<size_t>(row) * m + j] = make_double2(re * scale, im * scale);
     }
-    const double scale = 1.0 / static_cast<double>(m);
-    out[static_cast<size_t>(row) * m + j] = make_double2(re * scale, im * scale);
 }
 
 // transpose a (rows x cols) complex matrix
 __global__ void transpose_c(const double2* __restrict__ in, uint32_t rows, uint32_t cols,
                             double2* __restrict__ out) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t r = blockIdx.y;
-    if (c >= cols || r >= rows) return;
-    out[static_cast<size_t>(c) * rows + r] = in[static_cast<size_t>(r) * cols + c];
+    if (c >= cols) return;
+    for (uint32_t r = blockIdx.y; r < rows; r += gridDim.y)
+        out[static_cast<size_t>(c) * rows + r] = in[static_cast<size_t>(r) * cols + c];
 }
 
 __global__ void magnitude(const double2* __restrict__ in, size_t n, double* __restrict__ mag) {
@@ -153,9 +155,11 @@ int mcsbr_gpu_range_profile(const double* values, const double* freqs, uint32_t 
     double2* dout = d.alloc<double2>(m);
     double* dmag = d.alloc<double>(m);
     if (!din || !dout || !dmag) return finish(cuda_fail("range_profile alloc"));
-    cudaMemcpy(din, data.data(), sizeof(double2) * nf, cudaMemcpyHostToDevice);
+    if (cudaMemcpy(din, data.data(), sizeof(double2) * nf, cudaMemcpyHostToDevice) != cudaSuccess)
+        return finish(cuda_fail("range_profile upload"));
     idft_rows<<<dim3((m + 127) / 128, 1), 128>>>(din, 1, nf, m, false, dout);
     magnitude<<<(m + 255) / 256, 256>>>(dout, m, dmag);
+    if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail("range_profile launch"));
     std::vector<double> mag(m);
     if (cudaMemcpy(mag.data(), dmag, sizeof(double) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
         return finish(cuda_fail("range_profile"));
@@ -199,12 +203,15 @@ int mcsbr_gpu_isar(const double* values, const double* freqs, uint32_t nf, const
     double2* img = d.alloc<double2>(static_cast<size_t>(mr) * mc);    // [r][c]
     double* dmag = d.alloc<double>(static_cast<size_t>(mr) * mc);
     if (!din || !cols || !rows || !img || !dmag) return finish(cuda_fail("isar alloc"));
-    cudaMemcpy(din, data.data(), sizeof(double2) * na * nf, cudaMemcpyHostToDevice);
-    idft_rows<<<dim3((mr + 127) / 128, na), 128>>>(din, na, nf, mr, false, cols);     // down-range
-    transpose_c<<<dim3((mr + 127) / 128, na), 128>>>(cols, na, mr, rows);
-    idft_rows<<<dim3((mc + 127) / 128, mr), 128>>>(rows, mr, na, mc, true, img);      // cross-range
+    if (cudaMemcpy(din, data.data(), sizeof(double2) * na * nf, cudaMemcpyHostToDevice) != cudaSuccess)
+        return finish(cuda_fail("isar upload"));
+    auto gy = [](uint32_t rows_) { return std::min<uint32_t>(rows_, 65535u); };  // kernels stride over rows
+    idft_rows<<<dim3((mr + 127) / 128, gy(na)), 128>>>(din, na, nf, mr, false, cols);     // down-range
+    transpose_c<<<dim3((mr + 127) / 128, gy(na)), 128>>>(cols, na, mr, rows);
+    idft_rows<<<dim3((mc + 127) / 128, gy(mr)), 128>>>(rows, mr, na, mc, true, img);      // cross-range
     const size_t npx = static_cast<size_t>(mr) * mc;
     magnitude<<<static_cast<unsigned>((npx + 255) / 256), 256>>>(img, npx, dmag);
+    if (cudaGetLastError() != cudaSuccess) return finish(cuda_fail("isar launch"));
     std::vector<double> mag(npx);
     if (cudaMemcpy(mag.data(), dmag, sizeof(double) * npx, cudaMemcpyDeviceToHost) != cudaSuccess)
         return finish(cuda_fail("isar"));

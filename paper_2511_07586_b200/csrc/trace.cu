@@ -1,16 +1,16 @@
 // K2/K3/K4: the persistent Monte Carlo SBR path kernel.
 //
 // Replaces the body of mcsbr::estimate (proj/src/solver_mc.cpp:105-210) and
-// its callees.  One thread owns one path at a time; a warp pulls tiles of
-// launch entries (all from one incidence) from a global atomic tile counter
-// and refills lanes as their paths terminate (path regeneration), so the SIMT
-// lanes stay busy even though path lengths differ.  Per lane and event:
+// its callees.  One thread owns one path at a time; a warp pulls chunks of
+// launch entries from a global cursor (guided self-scheduling) and refills
+// lanes as their paths terminate (path regeneration), so the SIMT lanes stay
+// busy even though path lengths differ.  Per lane and event:
 //
-//   closest hit (K2, fp32 conservative BVH2 descent + fp64 Moller-Trumbore in
-//   the reference's arithmetic)  -> advance -> branch_outcomes (GO Fresnel /
-//   PEC transport) -> MECA currents + contribution -> branch choice and
-//   Russian roulette -> occlusion any-hit toward the receiver (K3) -> phasor
-//   accumulation (K4).
+//   closest hit (K2, fp32 conservative BVH4 descent + fp64 Moller-Trumbore in
+//   the reference's arithmetic, pathcore.cuh traverse)  -> advance ->
+//   branch_outcomes (GO Fresnel / PEC transport) -> MECA currents +
+//   contribution -> branch choice and Russian roulette -> occlusion any-hit
+//   toward the receiver (K3) -> phasor accumulation (K4).
 //
 // The wavefront order of the reference (all first hits of a block, then all
 // second hits, ...) only changes the ORDER in which contributions are summed;
@@ -19,12 +19,14 @@
 // reproduces the reference's per-path events bit for bit.
 //
 // Accumulation (K4): F = 1 keeps the 4 channel phasor sums of the lane's
-// current incidence in registers and reduces them across the warp (shuffles)
-// once per tile before one fp64 atomicAdd per channel.  F > 1 stages a
-// per-warp [F][4] complex accumulator in shared memory: each visible
-// contribution is broadcast across the warp and lane l evaluates frequencies
-// l, l+32, ... (fp64 phase, sincos) into its own slots, flushed with atomics
-// once per tile.
+// current incidence in its shared-memory slot and reduces them across the
+// warp (shuffles) when the warp changes incidence, then one fp64 atomicAdd
+// per channel (register mode); bistatic fans give lane l receiver l (fan
+// mode).  F > 1 (and every MCSBR_REDUCE_EXACT job) appends each visible
+// contribution as a 96-byte record to HBM; accumulate_kernel (or
+// accumulate_exact_kernel) turns the records into the [F][4] sums after the
+// launch (deferred mode).  Launch entries of deferred-mode kernels are
+// culled by the coverage bitmaps of cover.cu.
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>

@@ -8,7 +8,7 @@ pins for the extension):
    transfer-matrix slab reflection with a COMPLEX index (the reference's
    slab oracle, proj/src/oracles.cpp:32-64, with n complex), i.e. the
    reference's own "MC estimator converges to the slab oracle" test
-   (tests/test_solvers.cpp:480-499) extended to loss;
+   (tests/test_solvers.cpp:276-295) extended to loss;
 3. continuity: Im eps -> 0 recovers the lossless sweep.
 """
 import numpy as np
