@@ -284,6 +284,7 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
+    DevBuf<float4> leaf32;                 // statistical-mode fp32 leaf triangle records (built on first use)
     DevBuf<double> plan_axes;              // launch planning (prep.cu): axes in,
     DevBuf<unsigned long long> plan_ext;   // projection extents out
     DevBuf<unsigned long long> xsums;  // MCSBR_REDUCE_EXACT: 192-bit sums of the current job
@@ -310,6 +311,7 @@ struct mcsbr_scene {
         s.all_pec = all_pec ? 1 : 0;
         s.lossy = lossy ? 1 : 0;
         s.mat_nim = d_nim;
+        s.tri32 = leaf32.n ? leaf32.p : nullptr;
         s.center[0] = center[0];
         s.center[1] = center[1];
         s.center[2] = center[2];
@@ -619,6 +621,7 @@ void fill_config(TraceParams& p, const mcsbr_mc_config* cfg) {
     p.roulette_q = cfg->roulette_q;
     p.jitter = cfg->jitter != 0;
     p.rng_mode = cfg->rng_mode;
+    p.fast_tri = cfg->parity_fp64_refine == 0 ? 1 : 0;
 }
 
 // One launch group through the wavefront kernels: shade + trace per
@@ -706,6 +709,12 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
        "upload receivers");
     CK(cudaMemcpyAsync(s->k0.p, job.k0.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, stream),
        "upload wavenumbers");
+    // statistical-mode fast path: fp32 leaf records (prep.cu), once per scene
+    if (cfg->parity_fp64_refine == 0 && !(extra && extra->det) && !s->leaf32.n) {
+        CK(s->leaf32.reserve(3ull * s->bvh.n_leaves), "dev_malloc(fp32 triangles)");
+        CK(launch_leaf32(s->bvh.tri64, s->bvh.n_leaves, s->center, s->radius, s->leaf32.p, stream), "fp32 triangles launch");
+        ++g_launches;
+    }
     TraceParams p = extra ? *extra : TraceParams{};
     p.scene = s->view();
     p.cover = cover_words ? s->cover.p : nullptr;
@@ -1220,6 +1229,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->tile.release(true);
     s->recs.release(true);
     s->cover.release(true);
+    s->leaf32.release(true);
     s->plan_axes.release(true);
     s->plan_ext.release(true);
     s->xsums.release(true);

@@ -46,6 +46,8 @@ struct SceneView {
     int32_t all_pec;   // every triangle has a PEC side: dielectric code compiled out
     int32_t lossy;     // complex-permittivity transport (eps_imag given at scene creation)
     const double* mat_nim;  // per material Im(n) (lossy scenes), else nullptr
+    const float4* tri32;    // leaf-ordered fp32 triangle records (3 float4: a - centre, e1, e2, id) for the
+                            // statistical-mode fast path, built on first use; else nullptr
     double center[3];  // bounding-sphere centre: origin of the fp32 box frame
     double skip_radius;  // bounding radius + margin (traversal origin advance)
     float margin_r;      // bounding radius (fp32): scale of the slab-test ray margin
@@ -131,6 +133,7 @@ struct TraceParams {
     double roulette_q;
     int32_t jitter;
     int32_t rng_mode;
+    int32_t fast_tri;       // statistical-mode fp32 triangle tests (parity_fp64_refine = 0)
     // debug / parity instrumentation (all optional)
     void* contrib_out;                       // mcsbr_contribution[contrib_cap]
     unsigned long long* contrib_count;
@@ -211,6 +214,9 @@ cudaError_t launch_bounds(const double* d_vtx, uint32_t nv, unsigned long long* 
                           cudaStream_t stream);
 cudaError_t launch_radius(const double* d_vtx, uint32_t nv, const double c[3], unsigned long long* d_out,
                           int device_sms, cudaStream_t stream);
+// leaf-ordered fp32 triangle records for the statistical-mode fast path
+cudaError_t launch_leaf32(const double2* tri64, uint32_t n, const double center[3], double radius, float4* out,
+                         cudaStream_t stream);
 cudaError_t launch_extents(const double* d_vtx, uint32_t nv, const double* d_axes, uint32_t n_inc,
                            unsigned long long* d_out, int device_sms, cudaStream_t stream);
 

@@ -185,6 +185,52 @@ __device__ unsigned long long g_visits[9];
 #define MCSBR_STAT(i) ((void)0)
 #endif
 
+// Statistical-mode fast path (mcsbr_mc_config.parity_fp64_refine = 0): the
+// triangle tests run in fp32 on leaf-ordered fp32 records (vertex a relative
+// to the scene centre, e1, e2, id and two error numerators; 48 B instead of
+// the fp64 record's 80 B) with the ray's origin advanced into the bounding
+// sphere, so every operand is O(R).  The fp32 test only classifies: a hit
+// or miss by more than its rounding bound (prep.cu leaf32_kernel: K / |det|
+// on u, v, u + v and t) is taken as is; anything within the bound of an edge,
+// of t_min, or of a degenerate det is decided by the fp64 test of that
+// triangle.  Edge and self-hit decisions are therefore the fp64 test's (no
+// cracks between neighbours, no re-hit of the origin triangle); only
+// near-ties in t between two clear hits can resolve differently from the
+// reference, and the closest hit's t is refined in fp64.  Statistical mode
+// only (the host rejects it with the parity RNG stream).
+// Measured (r02, Philox stream, path kernel): c4 2.68-2.96 ms fp64 vs
+// 3.32-3.76 ms here, c5 (4 azimuths) 17.1-17.3 vs 20.4-20.6 ms; without the
+// final fp64 refine 3.52-4.09 / 19.3-19.5 ms.  The fp64 test with its exact
+// early outs is not the limiter, so the switch exists
+// for the API and is off by default.
+constexpr int kTri32Miss = 0, kTri32Hit = 1, kTri32Maybe = 2;
+__device__ __forceinline__ int tri_test32(const float4* __restrict__ rec, float ox, float oy, float oz, float dx,
+                                          float dy, float dz, float t_min, float& t_out, uint32_t& id_out) {
+    const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
+    const float ax = r0.x, ay = r0.y, az = r0.z, e1x = r0.w, e1y = r1.x, e1z = r1.y, e2x = r1.z, e2y = r1.w,
+                e2z = r2.x;
+    const float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
+    const float det = e1x * px + e1y * py + e1z * pz;
+    float inv;  // MUFU.RCP (its ~1 ulp is inside the 8x margin); det = 0 or nan: tol is inf / nan
+    asm("rcp.approx.f32 %0, %1;" : "=f"(inv) : "f"(det));
+    const float tol = r2.z * fabsf(inv);
+    if (!(tol < 0.25f)) return kTri32Maybe;
+    const float sx = ox - ax, sy = oy - ay, sz = oz - az;
+    const float u = (sx * px + sy * py + sz * pz) * inv;
+    if (u < -tol || u > 1.0f + tol) return kTri32Miss;
+    const float qx = sy * e1z - sz * e1y, qy = sz * e1x - sx * e1z, qz = sx * e1y - sy * e1x;
+    const float v = (dx * qx + dy * qy + dz * qz) * inv;
+    if (v < -tol || u + v > 1.0f + 2.0f * tol) return kTri32Miss;
+    const float t = (e2x * qx + e2y * qy + e2z * qz) * inv;
+    const float ttol = r2.w * fabsf(inv);
+    if (t <= t_min - ttol) return kTri32Miss;
+    id_out = __float_as_uint(r2.y);
+    if (u < tol || v < tol || u + v > 1.0f - 2.0f * tol || t <= t_min + ttol) return kTri32Maybe;
+    t_out = t;
+    return kTri32Hit;
+}
+
+template <bool kFastTri = false>
 __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double t_min, double& best_t,
                                          uint32_t& best_id, uint32_t& fault, bool kAny, bool outside) {
 #ifdef MCSBR_TRAVERSAL_STATS
@@ -202,6 +248,19 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
     const FRay r = make_fray(S, o, d, outside, t_min);
     best_t = __longlong_as_double(0x7ff0000000000000ll);
     best_id = 0xffffffffu;
+    // fast path: the ray in fp32, relative to the scene centre, from the
+    // box tests' advanced origin (t measured from t_skip)
+    float of[3] = {0.f, 0.f, 0.f}, df[3] = {0.f, 0.f, 0.f}, tmin32 = 0.f;
+    uint32_t best_slot = 0xffffffffu;  // the closest hit if it came from a clear fp32 test
+    if constexpr (kFastTri) {
+        of[0] = __double2float_rn(o.x - S.center[0] + d.x * r.t_skip);
+        of[1] = __double2float_rn(o.y - S.center[1] + d.y * r.t_skip);
+        of[2] = __double2float_rn(o.z - S.center[2] + d.z * r.t_skip);
+        df[0] = __double2float_rn(d.x);
+        df[1] = __double2float_rn(d.y);
+        df[2] = __double2float_rn(d.z);
+        tmin32 = __double2float_rn(t_min - r.t_skip);
+    }
     float tmax = __int_as_float(0x7f800000);
     int stack[kStackSize];
     int sp = 0;
@@ -282,21 +341,49 @@ __device__ __forceinline__ bool traverse(const SceneView& S, V3 o, V3 d, double 
             const uint32_t code = static_cast<uint32_t>(~ref);
             const uint32_t first = code >> 3, count = code & 7u;
             for (uint32_t k = 0; k < count; ++k) {
-                double t;
-                uint32_t id;
                 MCSBR_STAT(1);
-                if (tri_test(S.tri64 + 5ull * (first + k), o, d, t_min, t, id)) {
+                if constexpr (kFastTri) {
+                    float t32;
+                    uint32_t id;
+                    const int c = tri_test32(S.tri32 + 3ull * (first + k), of[0], of[1], of[2], df[0], df[1], df[2],
+                                             tmin32, t32, id);
+                    if (c == kTri32Miss) continue;
+                    double t;
+                    if (c == kTri32Maybe) {
+                        if (!tri_test(S.tri64 + 5ull * (first + k), o, d, t_min, t, id)) continue;
+                    } else {
+                        t = r.t_skip + static_cast<double>(t32);
+                    }
                     if (t < best_t || (t == best_t && id < best_id)) {
                         best_t = t;
                         best_id = id;
+                        best_slot = c == kTri32Hit ? first + k : 0xffffffffu;
                         if (kAny) return true;
-                        tmax = __double2float_ru((t - r.t_skip) * (1.0 + 1e-9));
+                        tmax = __double2float_ru((t - r.t_skip) * (1.0 + 1e-5));
+                    }
+                } else {
+                    double t;
+                    uint32_t id;
+                    if (tri_test(S.tri64 + 5ull * (first + k), o, d, t_min, t, id)) {
+                        if (t < best_t || (t == best_t && id < best_id)) {
+                            best_t = t;
+                            best_id = id;
+                            if (kAny) return true;
+                            tmax = __double2float_ru((t - r.t_skip) * (1.0 + 1e-9));
+                        }
                     }
                 }
             }
         }
         if (sp == 0) break;
         ref = stack[--sp];
+    }
+    if constexpr (kFastTri) {
+        if (best_slot != 0xffffffffu) {  // the winner's t in fp64 (kept from fp32 if fp64 rejects it)
+            double t;
+            uint32_t id;
+            if (tri_test(S.tri64 + 5ull * best_slot, o, d, t_min, t, id)) best_t = t;
+        }
     }
     return best_id != 0xffffffffu;
 }

@@ -138,6 +138,31 @@ __global__ void extents_kernel(const double* __restrict__ v, uint32_t nv, const 
     }
 }
 
+// tri64 record k = (a.x, a.y) (a.z, e1.x) (e1.y, e1.z) (e2.x, e2.y) (e2.z, id)
+__global__ void leaf32_kernel(const double2* __restrict__ t64, uint32_t n, double cx, double cy, double cz,
+                              double radius, float4* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2* r = t64 + 5ull * k;
+    const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4];
+    const uint32_t id = static_cast<uint32_t>(__double_as_longlong(r4.y));
+    // error numerators of pathcore.cuh tri_test32: with every fp32 operand
+    // O(R) (|s| <= 2.02 R) and L the longest edge, the rounding of s . p,
+    // d . q and e2 . q moves u, v by <= ~8 eps 2R L / |det| and t by <=
+    // ~8 eps 2R L^2 / |det|; 8x margin on top (eps = 2^-24)
+    const double e1x = r1.y, e1y = r2.x, e1z = r2.y, e2x = r3.x, e2y = r3.y, e2z = r4.x;
+    const double l1 = e1x * e1x + e1y * e1y + e1z * e1z, l2 = e2x * e2x + e2y * e2y + e2z * e2z;
+    const double l3 = (e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y) + (e2z - e1z) * (e2z - e1z);
+    const double lmax = sqrt(fmax(l1, fmax(l2, l3)));
+    const double kb = 64.0 * 0x1p-24 * 2.02 * radius * lmax;
+    out[3ull * k] = make_float4(__double2float_rn(r0.x - cx), __double2float_rn(r0.y - cy),
+                                __double2float_rn(r1.x - cz), __double2float_rn(e1x));
+    out[3ull * k + 1] = make_float4(__double2float_rn(e1y), __double2float_rn(e1z), __double2float_rn(e2x),
+                                    __double2float_rn(e2y));
+    out[3ull * k + 2] = make_float4(__double2float_rn(e2z), __uint_as_float(id), __double2float_ru(kb),
+                                    __double2float_ru(kb * lmax));
+}
+
 __global__ void init_minmax_kernel(unsigned long long* out, uint32_t n_pairs) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n_pairs) {
@@ -179,6 +204,13 @@ cudaError_t launch_radius(const double* d_vtx, uint32_t nv, const double c[3], u
     if (e != cudaSuccess) return e;
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((nv + 255) / 256, 4ull * device_sms));
     radius_kernel<<<blocks, 256, 0, stream>>>(d_vtx, nv, c[0], c[1], c[2], d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_leaf32(const double2* tri64, uint32_t n, const double center[3], double radius, float4* out,
+                         cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    leaf32_kernel<<<(n + 255) / 256, 256, 0, stream>>>(tri64, n, center[0], center[1], center[2], radius, out);
     return cudaGetLastError();
 }
 

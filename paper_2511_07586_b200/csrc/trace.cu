@@ -92,7 +92,7 @@ struct MinBlocks {
 // reflect child continues in registers and the transmit child goes on the
 // lane's branch stack; a dead lane pops its own stack before it takes a new
 // entry, which reproduces the reference's depth-first, reflect-first order.
-template <int kMode, bool kDiel, bool kLossy, bool kDet>
+template <int kMode, bool kDiel, bool kLossy, bool kDet, bool kFast>
 __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value)) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeDefer;
     // launch-ray culling by the coverage bitmaps (cover.cu): the deferred-
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                 else if (!kDet) atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
                 // closest hit: solver_mc.cpp:142-144; occlusion: farfield.cpp:63-68 /
                 // geometry.cpp:242-244 from the exit point (= origin after advance)
-                hit = traverse(S, s.origin, pend ? ld3(R.k_s) : s.dir,
+                hit = traverse<kFast>(S, s.origin, pend ? ld3(R.k_s) : s.dir,
                                (pend || s.bounce != 0) ? S.t_eps : 0.0, t, id, fault, pend,
                                !pend && s.bounce == 0);
             }
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                             double t2;
                             uint32_t id2;
                             ++n_occ;
-                            vis = !traverse(S, pt, ks, S.t_eps, t2, id2, fault, true, false);
+                            vis = !traverse<kFast>(S, pt, ks, S.t_eps, t2, id2, fault, true, false);
                         }
                         if (vis) {
                             ++n_contrib;
@@ -991,10 +991,10 @@ bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1 &&
 
 bool trace_fan_supported(uint32_t nf) { return nf == 1; }
 
-template <int kMode, bool kDiel, bool kLossy, bool kDet>
+template <int kMode, bool kDiel, bool kLossy, bool kDet, bool kFast>
 static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
                                cudaStream_t stream) {
-    auto* k = path_kernel<kMode, kDiel, kLossy, kDet>;
+    auto* k = path_kernel<kMode, kDiel, kLossy, kDet, kFast>;
     if (smem > 0) {  // static state slots + dynamic accumulators may pass 48 KB: opt in
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -1017,11 +1017,15 @@ template <bool kDiel, bool kLossy>
 static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int threads, size_t smem,
                                cudaStream_t stream) {
     if (p.det)  // one receiver per launch (the deterministic solver has no fan mode)
-        return mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, true>(p, sms, threads, smem, stream)
-                                : launch_mode<kModeDefer, kDiel, kLossy, true>(p, sms, threads, smem, stream);
-    return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false>(p, sms, threads, smem, stream)
-           : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false>(p, sms, threads, smem, stream)
-                              : launch_mode<kModeDefer, kDiel, kLossy, false>(p, sms, threads, smem, stream);
+        return mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, true, false>(p, sms, threads, smem, stream)
+                                : launch_mode<kModeDefer, kDiel, kLossy, true, false>(p, sms, threads, smem, stream);
+    if (p.fast_tri)  // statistical-mode fp32 triangle tests
+        return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false, true>(p, sms, threads, smem, stream)
+               : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false, true>(p, sms, threads, smem, stream)
+                                  : launch_mode<kModeDefer, kDiel, kLossy, false, true>(p, sms, threads, smem, stream);
+    return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false, false>(p, sms, threads, smem, stream)
+           : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false, false>(p, sms, threads, smem, stream)
+                              : launch_mode<kModeDefer, kDiel, kLossy, false, false>(p, sms, threads, smem, stream);
 }
 
 cudaError_t launch_exact_limbs(const unsigned long long* xsums, uint64_t n_values, long long* limbs,

@@ -164,3 +164,30 @@ def test_philox_sweep_matches_reference_stream(name):
         assert r["philox_vs_reference_" + k] < 1.3 * r["reference_seed_to_seed_" + k] + 0.01, (k, r)
     if r["reference_seed_to_seed_rms_db_within_20db"] < 0.25:
         assert r["philox_vs_reference_rms_db_within_20db"] < 0.5, r
+
+
+def test_fast_path_needs_the_statistical_stream():
+    with pytest.raises(ValueError, match="parity_fp64_refine"):
+        M.McConfig(parity_fp64_refine=False).validate()
+    M.McConfig(parity_fp64_refine=False, rng_mode=PHILOX).validate()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_fp32_fast_path_matches_fp64_statistical_mode(name):
+    """parity_fp64_refine = 0 (fp32 triangle tests, fp64 refinement of the
+    winner) against the fp64 statistical mode with the same Philox stream:
+    the same estimator on the same samples -- only near-tie hits can resolve
+    differently -- so the sweeps must agree far inside the seed-to-seed
+    spread, the segments to 0.1% and the contributions to 1% (fp32
+    occlusion tests of grazing bistatic receivers decide a few more
+    near-tangent rays differently)."""
+    s, incs, rxs, freqs, kw, ch = config_sweeps(name)
+    run = lambda refine, sd: M.estimate_batch(s, incs, rxs, freqs, M.McConfig(
+        seed=sd, rng_mode=PHILOX, parity_fp64_refine=refine, **kw))
+    (v64, st64), (v32, st32) = run(True, 11), run(False, 11)
+    other, _ = run(True, 12)
+    a, b, c = v64[..., ch, :], v32[..., ch, :], other[..., ch, :]
+    assert st32.rays_launched == st64.rays_launched
+    assert abs(st32.segments_traced - st64.segments_traced) <= 1e-3 * st64.segments_traced
+    assert abs(st32.contributions - st64.contributions) <= 1e-2 * st64.contributions
+    assert rel_l2(b, a) < 0.1 * rel_l2(c, a) + 1e-6, (rel_l2(b, a), rel_l2(c, a))

@@ -26,6 +26,8 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lossless", action="store_true", help="c5 skins with real permittivity (the reference's model)")
 ap.add_argument("--pec", action="store_true", help="c5 airframe without the dielectric skins")
 ap.add_argument("--nf", type=int, default=0, help="override the number of frequencies")
+ap.add_argument("--philox", action="store_true", help="statistical mode (Philox stream)")
+ap.add_argument("--fast", action="store_true", help="statistical mode with fp32 triangle tests (parity_fp64_refine off)")
 a = ap.parse_args()
 if a.config == "c4":
     sd, _ = airframe(200_000, seed=4)
@@ -40,6 +42,9 @@ else:
     freqs, n_az, half, rays = np.linspace(8e9, 12e9, 128), 128, 5.0, 16e6
 if a.nf:
     freqs = np.linspace(freqs[0], freqs[-1], a.nf) if a.nf > 1 else freqs[-1:]
+if a.philox or a.fast:
+    cfg.rng_mode = M.RngMode.PHILOX
+    cfg.parity_fp64_refine = not a.fast
 s = M.Scene(sd)
 lam = B.C0 / freqs[-1]
 az = np.linspace(-half, half, n_az)
