@@ -90,6 +90,8 @@ cudaError_t dev_malloc(void** p, size_t bytes) {
         }
     }
     e = cudaMalloc(p, n);
+    if (getenv("MCSBR_ALLOC_DEBUG") && n >= (size_t{16} << 20))
+        fprintf(stderr, "[alloc] cudaMalloc %zu MB (cached %zu MB)\n", n >> 20, cacheable ? c.cached[dev] >> 20 : 0);
     if (e != cudaSuccess && cacheable) {
         // out of memory: hand this device's cache back to the driver and retry once
         cudaGetLastError();
@@ -120,6 +122,8 @@ void dev_free(void* p, bool synced) {
     const int dev = it->second.first;
     const size_t n = it->second.second;
     if (dev < 0 || dev >= 64 || c.cached[dev] + n > cache_limit(c, dev)) {
+        if (getenv("MCSBR_ALLOC_DEBUG") && n >= (size_t{16} << 20))
+            fprintf(stderr, "[alloc] cudaFree %zu MB (cached %zu MB)\n", n >> 20, c.cached[dev] >> 20);
         c.size_of.erase(it);
         cudaFree(p);
         return;

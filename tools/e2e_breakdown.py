@@ -30,7 +30,7 @@ import ctypes as C  # noqa: E402
 from paper_2511_07586_b200 import _abi as A  # noqa: E402
 
 L = A.lib()
-for k in range(4):
+for k in range(int(os.environ.get("REPS", "4"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s2 = M.Scene(sd)
