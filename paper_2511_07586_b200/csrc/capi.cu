@@ -140,6 +140,64 @@ constexpr double kC = 299792458.0;
 constexpr double kPi = 3.14159265358979323846;
 
 thread_local std::string g_err;
+
+// Pinned 8-byte host slots for the asynchronous readbacks (record peak,
+// wavefront work-list length), handed out from one process-wide pool of
+// pinned pages that is never freed: a per-scene cudaMallocHost /
+// cudaFreeHost pair cost up to ~0.5 s in scene destroy on a busy host.
+struct PinnedSlots {
+    std::mutex m;
+    std::vector<unsigned long long*> free;
+};
+PinnedSlots& pinned_slots() {
+    static PinnedSlots* p = new PinnedSlots();  // never destroyed (used during process exit)
+    return *p;
+}
+cudaError_t pinned_slot(unsigned long long** out) {
+    PinnedSlots& P = pinned_slots();
+    std::lock_guard<std::mutex> g(P.m);
+    if (P.free.empty()) {
+        void* page = nullptr;
+        const cudaError_t e = cudaMallocHost(&page, 4096);
+        if (e != cudaSuccess) return e;
+        unsigned long long* q = static_cast<unsigned long long*>(page);
+        for (int i = 511; i >= 0; --i) P.free.push_back(q + i);
+    }
+    *out = P.free.back();
+    P.free.pop_back();
+    return cudaSuccess;
+}
+void pinned_release(unsigned long long* p) {
+    if (!p) return;
+    PinnedSlots& P = pinned_slots();
+    std::lock_guard<std::mutex> g(P.m);
+    P.free.push_back(p);
+}
+
+// MCSBR_HOST_TIMING=1: host-side phase times of scene create / estimate /
+// destroy on stderr (diagnostics for the e2e measurement)
+struct HostPhases {
+    const char* what;
+    bool on;
+    std::chrono::steady_clock::time_point t0, t;
+    std::string log;
+    explicit HostPhases(const char* w) : what(w), on(std::getenv("MCSBR_HOST_TIMING") != nullptr) {
+        if (on) t0 = t = std::chrono::steady_clock::now();
+    }
+    void mark(const char* phase) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        char b[96];
+        std::snprintf(b, sizeof b, " %s %.2f", phase, std::chrono::duration<double, std::milli>(n - t).count());
+        log += b;
+        t = n;
+    }
+    ~HostPhases() {
+        if (on)
+            std::fprintf(stderr, "[host] %s%s | total %.2f ms\n", what, log.c_str(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 thread_local uint64_t g_launches = 0;
 
 // Per-kernel device timing (mcsbr_gpu_kernel_timing): while enabled, run_job
@@ -468,8 +526,12 @@ constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: 
 // readback has landed) into the records-per-entry estimate.
 void learn_rec_ratio(mcsbr_scene* s) {
     if (!s->peak_host) {
-        if (cudaMallocHost(&s->peak_host, sizeof(unsigned long long)) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s->peak_ev, cudaEventDisableTiming) != cudaSuccess) {
+        if (pinned_slot(&s->peak_host) != cudaSuccess) {
+            s->peak_host = nullptr;
+            return;
+        }
+        if (cudaEventCreateWithFlags(&s->peak_ev, cudaEventDisableTiming) != cudaSuccess) {
+            pinned_release(s->peak_host);
             s->peak_host = nullptr;
             return;
         }
@@ -781,7 +843,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         CK(s->wf_u32.reserve(3ull * w.np), "dev_malloc(path pool)");
         CK(s->wf_ctl.reserve(6 + 2ull * (w.np / 32)), "dev_malloc(path pool)");
         if (!s->wf_host) {
-            CK(cudaMallocHost(&s->wf_host, sizeof(unsigned long long)), "cudaMallocHost");
+            CK(pinned_slot(&s->wf_host), "cudaMallocHost");
             CK(cudaEventCreateWithFlags(&s->wf_ev, cudaEventDisableTiming), "cudaEventCreate");
         }
         w.pool = s->wf_pool.p;
@@ -972,6 +1034,7 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
                                 !std::isfinite(mats[i].eps_r) || !std::isfinite(mats[i].mu_r)))
             return set_err(MCSBR_ESCENE, "material: eps_r and mu_r must be positive");
     }
+    HostPhases hp("scene_create");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -1033,6 +1096,7 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
             cudaSuccess)
             return fail(e, "upload Im n");
     }
+    hp.mark("setup+upload");
     // Triangle checks + device layout, vertex bounds and the bounding sphere
     // on the device (prep.cu): Scene::finalize (geometry.cpp:146-162)
     {
@@ -1102,9 +1166,11 @@ int mcsbr_gpu_scene_create(const double* xyz, uint32_t nv, const mcsbr_triangle*
     // boxes: outward-rounded fp64 AABBs; the pad only absorbs the fp64
     // rounding of the centring (the slab test's margin lives on the ray)
     const double box_pad = 1e-12 * s->radius + 1e-30;
+    hp.mark("prep");
     if ((e = build_bvh(s->d_vtx, s->d_tri, nt, lo3, hi3, s->center, box_pad, s->stream, &s->bvh)) != cudaSuccess)
         return fail(e, "BVH build");
     g_launches += 7;
+    hp.mark("bvh");
     if ((e = dev_malloc(&s->d_tri32, sizeof(float) * 9 * nt)) != cudaSuccess) return fail(e, "dev_malloc(tri32)");
     if ((e = build_tri32(s->d_vtx, s->d_tri, nt, s->center, s->d_tri32, s->stream)) != cudaSuccess)
         return fail(e, "fp32 triangle copy");
@@ -1210,6 +1276,7 @@ int mcsbr_gpu_device_count(int* n) {
 
 void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     if (!s) return;
+    HostPhases hp("destroy");
     for (mcsbr_scene* r : s->replicas) mcsbr_gpu_scene_destroy(r);
     s->replicas.clear();
     cudaSetDevice(s->device);
@@ -1217,6 +1284,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     // trace_device / intersect_device) must be done: one device sync, then
     // the frees need none each
     cudaDeviceSynchronize();
+    hp.mark("sync");
     dev_free(s->d_vtx, true);
     dev_free(s->d_tri, true);
     dev_free(s->d_info, true);
@@ -1241,13 +1309,16 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->wf_pool.release(true);
     s->wf_u32.release(true);
     s->wf_ctl.release(true);
-    if (s->wf_host) cudaFreeHost(s->wf_host);
+    hp.mark("frees");
+    pinned_release(s->wf_host);
     if (s->wf_ev) cudaEventDestroy(s->wf_ev);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->peak_ev) cudaEventDestroy(s->peak_ev);
-    if (s->peak_host) cudaFreeHost(s->peak_host);
+    pinned_release(s->peak_host);
     if (s->ev1) cudaEventDestroy(s->ev1);
+    hp.mark("host-frees/events");
     if (s->stream) cudaStreamDestroy(s->stream);
+    hp.mark("stream");
     delete s;
 }
 
@@ -1462,9 +1533,11 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
         if (rc) return rc;
         return estimate_multi(s, ndev, incs, n_inc, rxs, n_rx, occlusion, freqs, nf, cfg, values, stats, t0);
     }
+    HostPhases hp("estimate");
     Job job;
     rc = plan_job(s, incs, n_inc, rxs, n_rx, freqs, nf, cfg, 0, 1, s->sms * 16, &job, det != nullptr);
     if (rc) return rc;
+    hp.mark("plan");
     if (det && (n_inc != 1 || n_rx != 1)) return set_err(MCSBR_EINVAL, "solve: one excitation per call");
     const size_t nsum = static_cast<size_t>(n_inc) * n_rx * nf * 8;
     CK(s->sums.reserve(nsum), "dev_malloc(sums)");
@@ -1537,6 +1610,7 @@ static int estimate_common(mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t
     }
     rc = run_job(s, job, nf, cfg, occlusion, s->sums.p, s->counters.p, s->stream, &extra, &kms,
                  exact ? s->limbs.p : nullptr);
+    hp.mark("run");
     std::vector<unsigned long long> det_acc(2 * det_nblocks);
     if (rc == MCSBR_OK && det && det_nblocks) {
         const cudaError_t e2 = cudaMemcpy(det_acc.data(), d_blocks, sizeof(unsigned long long) * det_acc.size(),
