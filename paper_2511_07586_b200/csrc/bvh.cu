@@ -3,7 +3,7 @@
 //
 //   1. prim_kernel      per triangle: fp64 AABB padded by box_pad and rounded
 //                       outward to fp32; 63-bit Morton code of the centroid.
-//   2. cub radix sort   (morton, id) pairs.
+//   2. radix sort       (morton, id) pairs, stable (sort.cu).
 //   3. sah_build_kernel binned-SAH top-down build from the Morton order, one
 //                       persistent launch: block tasks for nodes of > 32
 //                       triangles, one warp per smaller subtree (default);
@@ -22,8 +22,6 @@
 // + padding), the triangle test that decides hits runs in fp64 with the
 // reference's arithmetic, so closest hits equal brute force
 // (Scene::intersect_brute_force, geometry.cpp:218-240) for ANY tree shape.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -992,9 +990,9 @@ static cudaError_t esc_references(const double* d_vertices, const uint4* d_tri_i
         esc_count_kernel<<<(n_tri + 255) / 256, 256, 0, stream>>>(d_vertices, d_tri_idx, n_tri, extra);
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, extra, off, n_tri, stream);
+    tmp_bytes = scan_temp_bytes(n_tri);
     if (e == cudaSuccess) e = dev_malloc(&tmp, tmp_bytes);
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, extra, off, n_tri, stream);
+    if (e == cudaSuccess) e = exclusive_scan_u32(extra, off, n_tri, tmp, stream);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(&last[0], off + (n_tri - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess)
@@ -1094,11 +1092,18 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                                      s[0], s[1], s[2], center[0], center[1], center[2], box_pad, keys,
                                      ids, blo, bhi);
     BVH_CHECK(cudaGetLastError());
-    BVH_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
-                                              stream));
+    // stable LSD radix sort of the (Morton key, reference) pairs (sort.cu);
+    // the sorted pairs end up in keys_s / ids_s
+    tmp_bytes = radix_sort_temp_bytes(n);
     BVH_CHECK(dev_malloc(&tmp, tmp_bytes));
-    BVH_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, ids, ids_s, n, 0, 64,
-                                              stream));
+    {
+        bool in_alt = false;
+        BVH_CHECK(radix_sort_pairs(keys, keys_s, ids, ids_s, n, 64, tmp, stream, &in_alt));
+        if (!in_alt) {
+            std::swap(keys, keys_s);
+            std::swap(ids, ids_s);
+        }
+    }
     order = ids_s;
     if (n > 1) {
         // binned SAH from the Morton order (locality), unless MCSBR_BVH=lbvh or
@@ -1168,9 +1173,9 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         BVH_CHECK(cudaGetLastError());
         parity_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, range, par_i, is4);
         BVH_CHECK(cudaGetLastError());
-        BVH_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, is4, idx4, n - 1, stream));
+        scan_bytes = scan_temp_bytes(n - 1);
         BVH_CHECK(dev_malloc(&scan_tmp, scan_bytes));
-        BVH_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, is4, idx4, n - 1, stream));
+        BVH_CHECK(exclusive_scan_u32(is4, idx4, n - 1, scan_tmp, stream));
         emit4_kernel<<<(n - 1 + B - 1) / B, B, 0, stream>>>(n, child, range, is4, idx4, ilo, ihi, blo_s,
                                                             bhi_s, out->nodes);
         BVH_CHECK(cudaGetLastError());

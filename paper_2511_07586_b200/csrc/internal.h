@@ -215,6 +215,14 @@ cudaError_t launch_bounds(const double* d_vtx, uint32_t nv, unsigned long long* 
 cudaError_t launch_radius(const double* d_vtx, uint32_t nv, const double c[3], unsigned long long* d_out,
                           int device_sms, cudaStream_t stream);
 // leaf-ordered fp32 triangle records for the statistical-mode fast path
+// sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs over the low
+// key_bits bits (8 per pass; *result_in_alt: the sorted pairs are in the
+// *_alt buffers), and an exclusive u32 prefix sum; temp of the *_temp_bytes size
+size_t radix_sort_temp_bytes(uint32_t n);
+cudaError_t radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint32_t n,
+                             int key_bits, void* temp, cudaStream_t stream, bool* result_in_alt);
+size_t scan_temp_bytes(uint32_t n);
+cudaError_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, void* temp, cudaStream_t stream);
 cudaError_t launch_leaf32(const double2* tri64, uint32_t n, const double center[3], double radius, float4* out,
                          cudaStream_t stream);
 cudaError_t launch_extents(const double* d_vtx, uint32_t nv, const double* d_axes, uint32_t n_inc,

@@ -136,3 +136,16 @@ if len(sys.argv) > 4:  # top SASS instructions of one region
     for s, i, a in top[:60]:
         f, ln, tl = ctx_line.get(a - base, (None, None, 0))
         print(f"{100 * s / ts:5.2f}% {i:>11d} {a - base:6x} {f}:{ln} ({tl})  {sass_text[a][:70]}")
+
+if len(sys.argv) > 5 and sys.argv[5] == "lines":  # samples / instructions / code bytes per trace.cu line
+    per = {}
+    for a, s, i in data:
+        tl = ctx_line.get(a - base, (None, None, 0))[2]
+        x = per.setdefault(tl, [0, 0, 0])
+        x[0] += s
+        x[1] += i
+        x[2] += 1
+    print("trace.cu line: samples% inst% sass")
+    for tl, (s, i, n) in sorted(per.items(), key=lambda kv: -kv[1][0])[:40]:
+        txt = src[tl - 1].strip()[:70] if 0 < tl <= len(src) else ""
+        print(f"{tl:5d} {100 * s / ts:5.1f} {100 * i / ti:5.1f} {n:5d}  {txt}")
