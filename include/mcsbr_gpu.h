@@ -318,14 +318,19 @@ MCSBR_API int mcsbr_gpu_estimate_batch(mcsbr_scene* scene, const mcsbr_incidence
                              uint32_t n_frequencies, const mcsbr_mc_config* config,
                              double* values, mcsbr_stats* stats);
 
-/* Device-resident variant for multi-GPU sharding and benchmarking: traces the
- * entry range [shard_index/shard_count] of every incidence and ADDS raw
+/* Device-resident variant for multi-GPU sharding and benchmarking: traces
+ * shard shard_index of shard_count of every incidence's launch entries and
+ * ADDS raw
  * (un-finalized) sums into the caller's device buffer d_sums
  * ([n_inc][n_rx][nf][4] complex; for MCSBR_REDUCE_EXACT configs int64 limbs
  * [n_inc][n_rx][nf][8][MCSBR_EXACT_LIMBS]) and counters into d_counters
  * (MCSBR_COUNTER_WORDS uint64), on `stream` (a cudaStream_t, NULL = legacy
  * default).  Asynchronous: no host synchronisation.  The caller all-reduces
- * the buffers (NCCL) and finalizes with mcsbr_gpu_finalize. */
+ * the buffers (NCCL) and finalizes with mcsbr_gpu_finalize.  A shard is
+ * every shard_count-th stripe of the incidence's dispatch indices (stripes
+ * of S = max(1024, ceil(entries / (32 shard_count)) rounded up to 1024),
+ * stripe k to shard k mod shard_count), so the shards balance whatever the
+ * target's silhouette; paths do not depend on the shard count. */
 #define MCSBR_COUNTER_WORDS 256
 MCSBR_API int mcsbr_gpu_trace_device(mcsbr_scene* scene, const mcsbr_incidence* incidences,
                            uint32_t n_inc, const mcsbr_receiver* receivers, uint32_t n_rx,

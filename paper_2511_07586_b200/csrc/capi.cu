@@ -544,16 +544,19 @@ void learn_rec_ratio(mcsbr_scene* s) {
 }  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
 
 struct Job {
-    std::vector<IncDev> inc;
+    std::vector<IncDev> inc;      // launch units, incidence-major (IncDev::row set per group)
+    std::vector<uint32_t> unit0;  // [n_inc + 1]: first unit of each incidence
+    uint32_t n_inc = 0;
     std::vector<RxDev> rx;
     std::vector<double> k0;
     uint32_t n_rx = 1;
     uint64_t total_entries = 0;
-    // launch groups [a0, a1) of incidences; IncDev::g_begin restarts at 0 in
-    // each.  F > 1 jobs are split into groups of <= kGroupEntries entries so a
-    // launch's contribution records fit the record buffer.
+    // launch groups: incidences [a0, a1) = units [u0, u1); IncDev::g_begin
+    // restarts at 0 in each.  F > 1 jobs are split into groups of <=
+    // kGroupEntries entries so a launch's contribution records fit the
+    // record buffer.
     struct Group {
-        uint32_t a0, a1;
+        uint32_t a0, a1, u0, u1;
         uint64_t entries;
     };
     std::vector<Group> groups;
@@ -575,7 +578,9 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     if (nshard == 0 || shard >= nshard) return set_err(MCSBR_EINVAL, "estimate: bad shard");
     double lambda_ref = cfg->reference_wavelength;
     if (lambda_ref <= 0.0) lambda_ref = kC / freqs[nf - 1];
-    job->inc.resize(n_inc);
+    job->inc.clear();
+    job->unit0.assign(n_inc + 1, 0);
+    job->n_inc = n_inc;
     job->rx.resize(static_cast<size_t>(n_inc) * n_rx);
     job->n_rx = n_rx;
     job->k0.resize(nf);
@@ -608,7 +613,7 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
         const mcsbr_incidence& in = incs[a];
         mcsbr_launch_plan lp = plans[a];
         if (lp.entries == 0) return set_err(MCSBR_EINVAL, "estimate: empty strata grid");
-        IncDev& d = job->inc[a];
+        IncDev d;
         std::memset(&d, 0, sizeof(d));
         std::memcpy(d.center, lp.center, sizeof(d.center));
         std::memcpy(d.u, lp.u_axis, sizeof(d.u));
@@ -621,9 +626,29 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
         d.area_weight = lp.cell_area / static_cast<double>(static_cast<uint64_t>(cfg->samples_per_stratum));
         d.nu = lp.nu;
         d.nv = lp.nv;
-        d.entry_begin = lp.entries * shard / nshard;
-        d.entry_end = lp.entries * (shard + 1) / nshard;
-        total += d.entry_end - d.entry_begin;
+        // Shards: the incidence's dispatch indices in stripes of S, stripe k
+        // to shard k mod nshard (about 32 stripes per shard), so every shard
+        // samples the whole aperture.  Contiguous shards put all of an
+        // airframe's silhouette on the middle ranks: c5 at 8 shards ran its
+        // slowest shard 2.1x the mean (tools/shard_balance.py).  Every entry
+        // keeps its dispatch index, RNG key and contribution.
+        job->unit0[a] = static_cast<uint32_t>(job->inc.size());
+        if (nshard == 1) {
+            d.entry_begin = 0;
+            d.entry_end = lp.entries;
+            job->inc.push_back(d);
+            total += lp.entries;
+        } else {
+            uint64_t S = (lp.entries + 32ull * nshard - 1) / (32ull * nshard);
+            S = std::max<uint64_t>(1024, (S + 1023) / 1024 * 1024);
+            const uint64_t stripes = (lp.entries + S - 1) / S;
+            for (uint64_t k = shard; k < stripes; k += nshard) {
+                d.entry_begin = k * S;
+                d.entry_end = std::min(lp.entries, (k + 1) * S);
+                job->inc.push_back(d);
+                total += d.entry_end - d.entry_begin;
+            }
+        }
         for (uint32_t r = 0; r < n_rx; ++r) {
             RxDev& x = job->rx[static_cast<size_t>(a) * n_rx + r];
             const mcsbr_receiver& y = rxs[static_cast<size_t>(a) * n_rx + r];
@@ -632,6 +657,7 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
             std::memcpy(x.rx_h, y.rx_h, sizeof(x.rx_h));
         }
     }
+    job->unit0[n_inc] = static_cast<uint32_t>(job->inc.size());
     job->total_entries = total;
     // F > 1: the launch groups are sized so their records fit kRecCapMax
     uint64_t group_cap = ~uint64_t{0};
@@ -646,18 +672,23 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     uint64_t g = 0;
     uint32_t a0 = 0;
     for (uint32_t a = 0; a < n_inc; ++a) {
-        IncDev& d = job->inc[a];
-        const uint64_t e = d.entry_end - d.entry_begin;
+        uint64_t e = 0;
+        for (uint32_t u = job->unit0[a]; u < job->unit0[a + 1]; ++u)
+            e += job->inc[u].entry_end - job->inc[u].entry_begin;
         if (a > a0 && g + e > group_cap) {
-            job->groups.push_back({a0, a, g});
+            job->groups.push_back({a0, a, job->unit0[a0], job->unit0[a], g});
             job->max_group_entries = std::max(job->max_group_entries, g);
             a0 = a;
             g = 0;
         }
-        d.g_begin = g;
-        g += e;
+        for (uint32_t u = job->unit0[a]; u < job->unit0[a + 1]; ++u) {
+            IncDev& d = job->inc[u];
+            d.g_begin = g;
+            d.row = a - a0;
+            g += d.entry_end - d.entry_begin;
+        }
     }
-    job->groups.push_back({a0, n_inc, g});
+    job->groups.push_back({a0, n_inc, job->unit0[a0], job->unit0[n_inc], g});
     job->max_group_entries = std::max(job->max_group_entries, g);
     // uniform grid test of SweepAccumulator (farfield.cpp:87-104)
     job->uniform_f = 0;
@@ -726,12 +757,14 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // (no fan), and the 192-bit sums are ADDED as limbs into d_limbs
     const bool exact = cfg->reduction == MCSBR_REDUCE_EXACT;
     if (exact && !d_limbs) return set_err(MCSBR_EINVAL, "exact reduction: no limb buffer");
-    const uint64_t n_values = static_cast<uint64_t>(job.inc.size()) * job.n_rx * nf * 8;
+    const uint64_t n_values = static_cast<uint64_t>(job.n_inc) * job.n_rx * nf * 8;
     if (exact) {
         CK(s->xsums.reserve(3 * n_values), "dev_malloc(exact sums)");
         CK(cudaMemsetAsync(s->xsums.p, 0, sizeof(unsigned long long) * 3 * n_values, stream), "memset exact sums");
     }
-    CK(s->inc.reserve(job.inc.size()), "dev_malloc(incidences)");
+    // the launch units, then one unit per incidence for the coverage kernel
+    const size_t n_units = job.inc.size();
+    CK(s->inc.reserve(n_units + job.n_inc), "dev_malloc(incidences)");
     CK(s->rx.reserve(job.rx.size()), "dev_malloc(receivers)");
     CK(s->k0.reserve(nf), "dev_malloc(k0)");
     CK(s->tile.reserve(3), "dev_malloc(tile counter)");  // entry cursor, record count, peak count
@@ -751,25 +784,37 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // deterministic solver's per-root stack accounting needs every root ray,
     // so its jobs are not culled
     std::vector<IncDev> incs = job.inc;
+    incs.resize(n_units + job.n_inc);
     const bool det_job = extra && extra->det;
     // only the deferred-accumulation kernels cull (trace.cu kCull)
     const bool cull = !det_job && (nf > 1 || exact) && env_u32("MCSBR_COVER", 1) != 0;
     uint64_t cover_words = 0;
-    for (IncDev& d : incs) {
-        d.cover_off = kNoCover;
-        d.cover_shift = 0;
-        if (!cull) continue;
-        const uint64_t entries = static_cast<uint64_t>(d.nu) * static_cast<uint64_t>(d.nv) *
-                                 static_cast<uint64_t>(cfg->samples_per_stratum);
-        const uint32_t sh = cover_shift_for(entries);
-        const uint64_t words = (((entries + (uint64_t{1} << sh) - 1) >> sh) + 31) / 32;
-        if (cover_words + words > kCoverBudgetWords) continue;
-        d.cover_off = cover_words;
-        d.cover_shift = sh;
-        cover_words += words;
+    uint32_t n_cover = 0;  // incidences with a bitmap (the coverage kernel's blocks)
+    for (uint32_t a = 0; a < job.n_inc; ++a) {
+        uint64_t off = kNoCover;
+        uint32_t sh = 0;
+        const uint32_t u0 = job.unit0[a], u1 = job.unit0[a + 1];
+        if (cull && u1 > u0) {
+            const IncDev& d = incs[u0];
+            const uint64_t entries = static_cast<uint64_t>(d.nu) * static_cast<uint64_t>(d.nv) *
+                                     static_cast<uint64_t>(cfg->samples_per_stratum);
+            sh = cover_shift_for(entries);
+            const uint64_t words = (((entries + (uint64_t{1} << sh) - 1) >> sh) + 31) / 32;
+            if (cover_words + words <= kCoverBudgetWords) {
+                off = cover_words;
+                cover_words += words;
+            } else {
+                sh = 0;
+            }
+        }
+        for (uint32_t u = u0; u < u1; ++u) {  // every stripe shares the incidence's bitmap
+            incs[u].cover_off = off;
+            incs[u].cover_shift = sh;
+        }
+        if (off != kNoCover) incs[n_units + n_cover++] = incs[u0];
     }
     if (cover_words) CK(s->cover.reserve(cover_words), "dev_malloc(coverage bitmaps)");
-    CK(cudaMemcpyAsync(s->inc.p, incs.data(), sizeof(IncDev) * incs.size(), cudaMemcpyHostToDevice,
+    CK(cudaMemcpyAsync(s->inc.p, incs.data(), sizeof(IncDev) * (n_units + n_cover), cudaMemcpyHostToDevice,
                        stream), "upload incidences");
     CK(cudaMemcpyAsync(s->rx.p, job.rx.data(), sizeof(RxDev) * job.rx.size(), cudaMemcpyHostToDevice, stream),
        "upload receivers");
@@ -826,7 +871,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     p.fan = fan ? 1 : 0;
     if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
     if (cover_words) {
-        CK(launch_cover(s->inc.p, static_cast<uint32_t>(incs.size()), s->d_tri32, s->nt, s->center, s->radius,
+        CK(launch_cover(s->inc.p + n_units, n_cover, s->d_tri32, s->nt, s->center, s->radius,
                         p.spp, static_cast<uint32_t>(p.band_order), s->cover.p, cover_words, s->sms, stream),
            "coverage kernel launch");
         ++g_launches;
@@ -857,8 +902,9 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     for (uint32_t r = 0; r < job.n_rx; r += step) {
         p.rx_index = r;
         for (const Job::Group& gr : job.groups) {
-            p.inc = s->inc.p + gr.a0;
-            p.n_inc = gr.a1 - gr.a0;
+            if (gr.entries == 0) continue;  // no entries of this shard in the group
+            p.inc = s->inc.p + gr.u0;
+            p.n_inc = gr.u1 - gr.u0;
             p.inc_base = gr.a0;
             p.rx = s->rx.p + static_cast<size_t>(gr.a0) * job.n_rx;
             p.sums = d_sums + static_cast<size_t>(gr.a0) * job.n_rx * nf * 8;

@@ -60,12 +60,16 @@ struct IncDev {
     double k_inc[3], pol_v[3], pol_h[3];
     double area_weight;       // cell_area / spp
     int32_t nu, nv;
-    uint64_t entry_begin;     // this shard's entry range [begin, end)
+    // One launch unit: a range of the incidence's dispatch indices.  A
+    // single-shard job has one unit per incidence; a sharded job gives each
+    // shard interleaved stripes of every incidence (capi.cu plan_job), each
+    // stripe a unit with the incidence's geometry.
+    uint64_t entry_begin;     // this unit's dispatch range [begin, end)
     uint64_t entry_end;
-    uint64_t g_begin;         // index of entry_begin in the job's flattened entry space
+    uint64_t g_begin;         // index of entry_begin in the launch's flattened entry space
     uint64_t cover_off;       // launch-ray coverage bitmap (cover.cu): first word, kNoCover = none
     uint32_t cover_shift;     // log2 of the launch entries per coverage bit
-    uint32_t _pad;
+    uint32_t row;             // the incidence, relative to the launch's first (sums, receivers, records)
 };
 constexpr uint64_t kNoCover = ~uint64_t{0};
 constexpr uint64_t kCoverMaxBits = uint64_t{1} << 19;  // 64 KB of shared memory per incidence
@@ -93,9 +97,9 @@ enum : int {
 
 struct TraceParams {
     SceneView scene;
-    const IncDev* inc;      // this launch's incidences (a group of the job)
+    const IncDev* inc;      // this launch's units (the incidences of a group of the job)
     uint32_t n_inc;
-    uint32_t inc_base;      // job index of inc[0] (RNG keys, path log)
+    uint32_t inc_base;      // job index of the launch's first incidence (RNG keys, path log)
     uint32_t n_rx;          // receivers per incidence
     uint32_t rx_index;      // receiver traced by this launch (fan: the first of up to 32)
     int fan;                // bistatic fan mode (nf == 1)

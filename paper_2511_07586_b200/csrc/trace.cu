@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
         }
         __syncwarp();
     };
-    // incidence containing global entry g: last a with g_begin[a] <= g
+    // launch unit containing global entry g: last u with g_begin[u] <= g
     auto find_inc = [&](uint64_t g) {
         uint32_t lo = 0, hi = P.n_inc;
         while (hi - lo > 1) {
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
         if (q[0] >= q[1]) fetch();
         const uint64_t q0 = q[0], q1 = q[1];
         if (q0 >= q1) break;
-        const uint32_t a = find_inc(q0);
-        const IncDev& I = P.inc[a];
+        const IncDev& I = P.inc[find_inc(q0)];  // the launch unit holding q0
+        const uint32_t a = I.row;               // its incidence
         const uint64_t g_end_a = I.g_begin + (I.entry_end - I.entry_begin);
         uint64_t cursor = I.entry_begin + (q0 - I.g_begin);  // warp-uniform
         uint64_t e_end = I.entry_begin + (min(q1, g_end_a) - I.g_begin);

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) amp[ch] = {W.at(kFamp + 2 * ch, k), W.at(kFamp + 2 * ch + 1, k)};
             s_path = load_nt<NT>(W, kFsp, k);
-            rec_inc = static_cast<uint32_t>(meta >> 32);
+            rec_inc = P.inc[static_cast<uint32_t>(meta >> 32)].row;  // the unit's incidence
         }
         if (meta & 0x100ull) {
             dead = true;
@@ -179,8 +179,9 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
         } else {
             const double t = W.at(kFt, k);
             const uint64_t meta = W.u64(kFmeta, k);
-            const uint32_t a = static_cast<uint32_t>(meta >> 32);
-            const IncDev& I = P.inc[a];
+            const uint32_t unit = static_cast<uint32_t>(meta >> 32);  // the path's launch unit
+            const IncDev& I = P.inc[unit];
+            const uint32_t a = I.row;
             const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + P.rx_index];
             Path<NT, EF> s;
             s.origin = W.v3(kFo, k);
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                     W.at(kFamp + 2 * ch + 1, k) = amp[ch].im;
                 }
                 store_nt(W, kFsp, k, s_path);
-                W.setu64(kFmeta, k, pack_meta(s.bounce, !alive, a));
+                W.setu64(kFmeta, k, pack_meta(s.bounce, !alive, unit));
                 next = kQOcclusion;
                 ++n_occ;
             } else {
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                 if (alive) {
                     W.set3(kFo, k, point);
                     W.set3(kFd, k, s.dir);
-                    W.setu64(kFmeta, k, pack_meta(s.bounce, false, a));
+                    W.setu64(kFmeta, k, pack_meta(s.bounce, false, unit));
                     next = kQSurface;
                     atomicAdd(&s_bounce[min(s.bounce, 63)], 1u);
                 }
@@ -425,8 +426,9 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                 const uint32_t mid = (lo + hi) >> 1;
                 if (P.inc[mid].g_begin <= cur) lo = mid; else hi = mid;
             }
-            const uint32_t a = lo;
-            const IncDev& I = P.inc[a];
+            const uint32_t u = lo;  // launch unit
+            const IncDev& I = P.inc[u];
+            const uint32_t a = I.row;
             const uint64_t g_end_a = I.g_begin + (I.entry_end - I.entry_begin);
             const uint64_t sub_end = min(end, g_end_a);
             uint64_t dcur = I.entry_begin + (cur - I.g_begin);
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                         store_nt(W, kFmed, k, s.medium_n);
                         W.setu64(kFkey, k, s.key);
                         W.setu64(kFcs, k, static_cast<uint64_t>(s.cell) | (static_cast<uint64_t>(s.sample) << 32));
-                        W.setu64(kFmeta, k, pack_meta(0, false, a));
+                        W.setu64(kFmeta, k, pack_meta(0, false, u));
                         next = kQLaunch;
                         dead = false;
                         ++n_launched;

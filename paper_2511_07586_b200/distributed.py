@@ -4,12 +4,14 @@ One process per GPU (torch.distributed, NCCL over NVLink / NVSwitch).  Every
 rank holds a replica of the scene (uploaded + BVH built on its own GPU) and
 traces a disjoint range of EVERY incidence's launch entries,
 
-    [entries * rank / world, entries * (rank + 1) / world)      (shard_range)
+    stripes k = rank, rank + world, rank + 2 world, ... of S dispatch
+    indices each, S ~ entries / (32 world) rounded up to 1024    (shard_stripes)
 
 of the dispatch order (4-row bands of strata, trace.cu locate(); the same
-integer partition the C ABI applies in mcsbr_gpu_trace_device), so
-per-angle work is balanced and the counter-RNG keys (seed, cell, sample) --
-hence every path -- are independent of the GPU count.  The raw complex
+integer partition the C ABI applies in mcsbr_gpu_trace_device, capi.cu
+plan_job).  Interleaving balances the ranks whatever the target's silhouette
+(contiguous shards put an airframe's whole silhouette on the middle ranks),
+and the counter-RNG keys (seed, cell, sample) -- hence every path -- are independent of the GPU count.  The raw complex
 phasor sums ([n_inc][n_rx][nf][4] fp64) and the uint64 counters are then
 summed with one all-reduce each; the j k0 / (2 sqrt(pi)) finalisation runs
 on the host.  This mirrors the reference's own fixed-order block merge
@@ -29,9 +31,17 @@ import numpy as np
 from . import _abi as A
 
 
-def shard_range(entries: int, rank: int, world: int) -> tuple[int, int]:
-    """Launch-entry range of `rank` (identical to capi.cu plan_job)."""
-    return entries * rank // world, entries * (rank + 1) // world
+def shard_stripes(entries: int, rank: int, world: int) -> list[tuple[int, int]]:
+    """Dispatch-index ranges of `rank` (identical to capi.cu plan_job): one
+    range [0, entries) for world 1, else stripes of S indices, stripe k to
+    rank k mod world, S = max(1024, ceil(entries / (32 world)) rounded up to
+    a multiple of 1024)."""
+    if world == 1:
+        return [(0, entries)] if entries else []
+    s = -(-entries // (32 * world))
+    s = max(1024, -(-s // 1024) * 1024)
+    n = -(-entries // s)
+    return [(k * s, min(entries, (k + 1) * s)) for k in range(rank, n, world)]
 
 
 def allreduce_finalize(sums, counters, freqs, n: int, group=None):

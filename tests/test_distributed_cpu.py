@@ -1,7 +1,7 @@
 """CPU, world_size 2 (gloo): the multi-rank reduction path.
 
 Each rank computes the raw accumulators of ITS launch-entry shard
-(distributed.shard_range, the partition mcsbr_gpu_trace_device applies) with
+(distributed.shard_stripes, the partition mcsbr_gpu_trace_device applies) with
 the oracle standing in for the device trace, then runs the product's
 allreduce_finalize (the same code the NCCL path runs).  The reduced result
 must equal the single-process estimate to fp64 rounding, and the counters
@@ -46,17 +46,21 @@ def _worker(rank, world, port, out):
         sd, exc, freqs, cfg = _case()
         ps = oracle.port_scene(sd)
         _, _, total = oracle.port_estimate_range(ps, exc.to_c(), freqs, cfg.to_c(), 0, 0)
-        b, e = D.shard_range(total, rank, world)
-        raw, st, _ = oracle.port_estimate_range(ps, exc.to_c(), freqs, cfg.to_c(), b, e)
-        sums = torch.from_numpy(raw.reshape(-1).copy())
+        stripes = D.shard_stripes(total, rank, world)
+        assert stripes, "the test case gives every rank a stripe"
+        sums = None
         counters = torch.zeros(256, dtype=torch.int64)
-        counters[0] = st.rays_launched
-        counters[2] = st.contributions
-        counters[4] = st.cap_kills
-        for i in range(64):
-            counters[8 + i] = st.rays_per_bounce[i]
-            counters[72 + i] = st.roulette_candidates[i]
-            counters[136 + i] = st.roulette_survivors[i]
+        for b, e in stripes:
+            raw, st, _ = oracle.port_estimate_range(ps, exc.to_c(), freqs, cfg.to_c(), b, e)
+            part = torch.from_numpy(raw.reshape(-1).copy())
+            sums = part if sums is None else sums + part
+            counters[0] += st.rays_launched
+            counters[2] += st.contributions
+            counters[4] += st.cap_kills
+            for i in range(64):
+                counters[8 + i] += st.rays_per_bounce[i]
+                counters[72 + i] += st.roulette_candidates[i]
+                counters[136 + i] += st.roulette_survivors[i]
         values, stats = D.allreduce_finalize(sums, counters, freqs, 1)
         if rank == 0:
             np.save(out, values.reshape(4, len(freqs)))
@@ -66,13 +70,20 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_shard_range_partition():
-    for entries in (0, 1, 7, 1000, 4_008_004, 10**12 + 3):
+def test_shard_stripes_partition():
+    """The stripes of all ranks tile [0, entries) exactly once, and every
+    rank holds a share within one stripe of the mean."""
+    for entries in (0, 1, 7, 1000, 4_008_004, 16_777_216, 10**9 + 3):
         for world in (1, 2, 3, 8):
-            r = [D.shard_range(entries, k, world) for k in range(world)]
-            assert r[0][0] == 0 and r[-1][1] == entries
-            assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
-            assert max(e - b for b, e in r) - min(e - b for b, e in r) <= 1
+            per = [D.shard_stripes(entries, k, world) for k in range(world)]
+            allr = sorted(r for p in per for r in p)
+            assert sum(e - b for b, e in allr) == entries
+            assert all(allr[k][1] == allr[k + 1][0] for k in range(len(allr) - 1))
+            if allr:
+                assert allr[0][0] == 0 and allr[-1][1] == entries
+                width = max(e - b for b, e in allr)
+                share = [sum(e - b for b, e in p) for p in per]
+                assert max(share) - min(share) <= width
 
 
 @pytest.mark.timeout(300)

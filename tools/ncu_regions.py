@@ -64,6 +64,11 @@ rows.insert(0, ["Kernel Name"])
 hdr = rows[1]
 ai, si, ii = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 data = [(int(r[ai], 16), int(r[si] or 0), int(r[ii] or 0)) for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")]
+ti_col = hdr.index("Thread Instructions Executed") if "Thread Instructions Executed" in hdr else None
+loc_col = hdr.index("L2 Theoretical Sectors Local") if "L2 Theoretical Sectors Local" in hdr else None
+extra_by_addr = {int(r[ai], 16): (int(r[ti_col] or 0) if ti_col is not None else 0,
+                                  int(float(r[loc_col] or 0)) if loc_col is not None else 0)
+                 for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")}
 stall_cols = [(h, hdr.index(h)) for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 stall_by_addr = {int(r[ai], 16): {h: int(r[c] or 0) for h, c in stall_cols}
                  for r in rows[2:] if len(r) > ii and r[ai].startswith("0x")}
@@ -118,8 +123,16 @@ for a, s_, i in data:
     d = stall_reg.setdefault(r, {})
     for h, v in stall_by_addr.get(a, {}).items():
         d[h] = d.get(h, 0) + v
+thr_reg, loc_reg = {}, {}
+for a, s_, i in data:
+    r = region(ctx_line.get(a - base, (None, None, 0))[2])
+    t_, l_ = extra_by_addr.get(a, (0, 0))
+    thr_reg[r] = thr_reg.get(r, 0) + t_
+    loc_reg[r] = loc_reg.get(r, 0) + l_
 for r, (s, i, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
-    print(f"{r:22s} {100 * s / ts:5.1f}% samples  {100 * i / ti:5.1f}% inst  {n:5d} sass ({n * 16 / 1024:.1f} KB)")
+    simt = thr_reg.get(r, 0) / i if i else 0.0
+    print(f"{r:22s} {100 * s / ts:5.1f}% samples  {100 * i / ti:5.1f}% inst  {n:5d} sass ({n * 16 / 1024:.1f} KB)"
+          f"  simt {simt:4.1f}  local sectors {loc_reg.get(r, 0):.3g}")
     d = stall_reg.get(r, {})
     tot = sum(d.values()) or 1
     top = sorted(d.items(), key=lambda kv: -kv[1])[:6]
