@@ -135,7 +135,17 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
     }
     const double x = 1.0 - cos_i * cos_i;
     const double sin2_i = (0.0 < x) ? x : 0.0;
-    const Cx q = cdiv(n1, n2);
+    // An interface with a lossy side has no reference counterpart (the
+    // reference is lossless), so its quotients use one reciprocal per
+    // denominator (1 / |den|^2 times conj(den): one fp64 division instead of
+    // the three of the Smith division, a few ulps from it for |n| ~ 1..1e3);
+    // real indices keep cdiv, the reference's __divdc3, bit for bit.
+    const bool lossy_if = n1.im != 0.0 || n2.im != 0.0;
+    auto inv = [](Cx d) {
+        const double s = 1.0 / (d.re * d.re + d.im * d.im);
+        return Cx{d.re * s, -(d.im * s)};
+    };
+    const Cx q = lossy_if ? n1 * inv(n2) : cdiv(n1, n2);
     const Cx s2 = (q * q) * sin2_i;
     // Root choice for k_z = k0 n2 cos_t: a propagating transmitted wave
     // (|Re k_z| >= |Im k_z|) must carry power away (Re k_z >= 0); an
@@ -151,10 +161,18 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
     const Cx ci = {cos_i, 0.0};
     const Cx den_s = ci * n1 + cos_t * n2;
     const Cx den_p = ci * n2 + cos_t * n1;
-    c.r_s = cdiv(ci * n1 - cos_t * n2, den_s);
-    c.t_s = cdiv(ci * (n1 * 2.0), den_s);
-    c.r_p = cdiv(ci * n2 - cos_t * n1, den_p);
-    c.t_p = cdiv(ci * (n1 * 2.0), den_p);
+    if (lossy_if) {
+        const Cx is = inv(den_s), ip = inv(den_p);
+        c.r_s = (ci * n1 - cos_t * n2) * is;
+        c.t_s = (ci * (n1 * 2.0)) * is;
+        c.r_p = (ci * n2 - cos_t * n1) * ip;
+        c.t_p = (ci * (n1 * 2.0)) * ip;
+    } else {
+        c.r_s = cdiv(ci * n1 - cos_t * n2, den_s);
+        c.t_s = cdiv(ci * (n1 * 2.0), den_s);
+        c.r_p = cdiv(ci * n2 - cos_t * n1, den_p);
+        c.t_p = cdiv(ci * (n1 * 2.0), den_p);
+    }
     return c;
 }
 
