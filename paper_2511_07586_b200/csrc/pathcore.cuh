@@ -733,6 +733,26 @@ __device__ __forceinline__ void project_pec(const RxDev& R, const V3& aj0, const
     amp[1] = {dot(f1, rh), 0.0};  // HH
 }
 
+// one polarisation of project(): (VV, HV) from (j0, m0), (VH, HH) from (j1, m1)
+__device__ __forceinline__ void project_pol(const RxDev& R, const CV3& aj, const CV3& am, Cx& a_v, Cx& a_h) {
+    const V3 ks = ld3(R.k_s);
+    const CV3 f = cross(ks, cross(ks, aj)) + cross(ks, am);
+    a_v = dot(f, ld3(R.rx_v));
+    a_h = dot(f, ld3(R.rx_h));
+}
+__device__ __forceinline__ void project_pol(const RxDev& R, const V3& aj, const V3& am, Cx& a_v, Cx& a_h) {
+    const V3 ks = ld3(R.k_s);
+    const V3 f = cross(ks, cross(ks, aj)) + cross(ks, am);
+    a_v = {dot(f, ld3(R.rx_v)), 0.0};
+    a_h = {dot(f, ld3(R.rx_h)), 0.0};
+}
+__device__ __forceinline__ void project_pec_pol(const RxDev& R, const V3& aj, Cx& a_v, Cx& a_h) {
+    const V3 ks = ld3(R.k_s);
+    const V3 f = cross(ks, cross(ks, aj));
+    a_v = {dot(f, ld3(R.rx_v)), 0.0};
+    a_h = {dot(f, ld3(R.rx_h)), 0.0};
+}
+
 __device__ __forceinline__ void store_cv(double* p, const CV3& v) {
     p[0] = v.x.re; p[1] = v.x.im; p[2] = v.y.re; p[3] = v.y.im; p[4] = v.z.re; p[5] = v.z.im;
 }

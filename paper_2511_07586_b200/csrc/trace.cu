@@ -437,41 +437,33 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                             //   sc 2: j = n_o x ((d_t x e_t) n2),          m = e_t x n_o, n_o = -n
                             // each the reference's expression operation for operation.
                             const bool ex = sc == 2;
-                            EF f0 = ef_zero<EF>(), f1 = ef_zero<EF>();  // e_r (sc 1) / e_t (sc 2)
-                            if (sc != 0) {
-                                if constexpr (kDet) {
-                                    f0 = ex ? et0 : er0;
-                                    f1 = ex ? et1 : er1;
-                                } else {
-                                    f0 = branch_field(s.e0, ex ? 1 : 0, co, b);
-                                    f1 = branch_field(s.e1, ex ? 1 : 0, co, b);
-                                }
-                            }
                             const V3 nrm = ex ? -h.normal : h.normal;
                             const V3 dj = ex ? b.dir_t : s.dir;
                             const NT nj = ex ? h.n_transmit : s.medium_n;
-                            EF x0 = cross(dj, ex ? f0 : s.e0), x1 = cross(dj, ex ? f1 : s.e1);
-                            if (sc == 1) {
-                                x0 = x0 + cross(b.dir_r, f0);
-                                x1 = x1 + cross(b.dir_r, f1);
-                            }
-                            EF j0 = cross(nrm, x0 * nj), j1 = cross(nrm, x1 * nj);
-                            EF m0 = ef_zero<EF>(), m1 = ef_zero<EF>();
-                            if (sc == 0) {
-                                j0 = j0 * 2.0;
-                                j1 = j1 * 2.0;
-                            } else {
-                                m0 = cross(ex ? f0 : s.e0 + f0, nrm);
-                                m1 = cross(ex ? f1 : s.e1 + f1, nrm);
-                            }
                             // make_contribution (farfield.cpp:70-85)
                             const double cos_n = fabs(dot(s.dir, h.normal));
                             const double scale = s.weight * I.area_weight / (s.prob * cos_n);
-                            j0 = j0 * scale;
-                            m0 = m0 * scale;
-                            j1 = j1 * scale;
-                            m1 = m1 * scale;
-                            if (kMode == kModeFan) {
+                            // one polarisation's currents (e: the incident
+                            // field; e_r / e_t for sc 1 / 2), scaled
+                            auto currents = [&](const EF& e, int pol, EF& j, EF& m) {
+                                EF f = ef_zero<EF>();  // e_r (sc 1) / e_t (sc 2)
+                                if (sc != 0) {
+                                    if constexpr (kDet) f = ex ? (pol ? et1 : et0) : (pol ? er1 : er0);
+                                    else f = branch_field(e, ex ? 1 : 0, co, b);
+                                }
+                                EF x = cross(dj, ex ? f : e);
+                                if (sc == 1) x = x + cross(b.dir_r, f);
+                                j = cross(nrm, x * nj);
+                                m = ef_zero<EF>();
+                                if (sc == 0) j = j * 2.0;
+                                else m = cross(ex ? f : e + f, nrm);
+                                j = j * scale;
+                                m = m * scale;
+                            };
+                            EF j0, m0, j1, m1;
+                            if constexpr (kMode == kModeFan) {
+                                currents(s.e0, 0, j0, m0);
+                                currents(s.e1, 1, j1, m1);
                                 fj0 = j0;
                                 fm0 = m0;
                                 fj1 = j1;
@@ -479,13 +471,27 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                                 fphi = s.phi;
                                 fpt = point;
                             } else {
-                                if constexpr (L::pec) project_pec(R, j0, j1, amp);  // m = 0 on PEC hits
-                                else project(R, j0, m0, j1, m1, amp);
+                                // polarisation by polarisation: half the live
+                                // complex vectors of forming all four
+                                // currents first (the lossy kernel spilled
+                                // them); every value is the same expression
+                                currents(s.e0, 0, j0, m0);
+                                if constexpr (L::pec) project_pec_pol(R, j0, amp[0], amp[3]);  // m = 0 on PEC hits
+                                else project_pol(R, j0, m0, amp[0], amp[3]);
+                                if (scratch) {
+                                    store_cv(&scratch->a_j[0][0][0], j0);
+                                    store_cv(&scratch->a_m[0][0][0], m0);
+                                }
+                                currents(s.e1, 1, j1, m1);
+                                if constexpr (L::pec) project_pec_pol(R, j1, amp[2], amp[1]);
+                                else project_pol(R, j1, m1, amp[2], amp[1]);
                                 s_path = s.phi - dot(ld3(R.k_s), point);
                             }
                             if (scratch) {
-                                store_cv(&scratch->a_j[0][0][0], j0);
-                                store_cv(&scratch->a_m[0][0][0], m0);
+                                if constexpr (kMode == kModeFan) {
+                                    store_cv(&scratch->a_j[0][0][0], j0);
+                                    store_cv(&scratch->a_m[0][0][0], m0);
+                                }
                                 store_cv(&scratch->a_j[1][0][0], j1);
                                 store_cv(&scratch->a_m[1][0][0], m1);
                                 scratch->phi_total = re_of(s.phi);

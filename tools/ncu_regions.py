@@ -154,11 +154,13 @@ if len(sys.argv) > 5 and sys.argv[5] == "lines":  # samples / instructions / cod
     per = {}
     for a, s, i in data:
         tl = ctx_line.get(a - base, (None, None, 0))[2]
-        x = per.setdefault(tl, [0, 0, 0])
+        x = per.setdefault(tl, [0, 0, 0, 0])
         x[0] += s
         x[1] += i
         x[2] += 1
-    print("trace.cu line: samples% inst% sass")
-    for tl, (s, i, n) in sorted(per.items(), key=lambda kv: -kv[1][0])[:40]:
+        x[3] += extra_by_addr.get(a, (0, 0))[1]
+    key = 3 if len(sys.argv) > 6 and sys.argv[6] == "local" else 0
+    print("trace.cu line: samples% inst% sass local-sectors")
+    for tl, (s, i, n, lc) in sorted(per.items(), key=lambda kv: -kv[1][key])[:40]:
         txt = src[tl - 1].strip()[:70] if 0 < tl <= len(src) else ""
-        print(f"{tl:5d} {100 * s / ts:5.1f} {100 * i / ti:5.1f} {n:5d}  {txt}")
+        print(f"{tl:5d} {100 * s / ts:5.1f} {100 * i / ti:5.1f} {n:5d} {lc:10.3g}  {txt}")
