@@ -789,7 +789,10 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
     // complex multiplies -- c5 +3.5%, the table doubles the shared memory.)
     // (Measured and rejected as well: W^2 .. W^(FPL-1) staged per record so
     // a lane forms its phasors by independent products instead of the
-    // recurrence chain -- c5 +2%.)
+    // recurrence chain -- c5 +2%.  Round 2: each lane's first phasor as a
+    // warp prefix product Z0 W1^lane (5 shuffle + multiply steps) instead
+    // of its sincos -- +7%; the next record's sincos software-pipelined
+    // against this record's sums -- +4.6%.)
     constexpr int kSt = 8;
     __shared__ double2 st[4][32][kSt];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
