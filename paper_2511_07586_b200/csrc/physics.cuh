@@ -26,6 +26,7 @@ enum : uint32_t {
 struct Coeffs {
     Cx r_s, r_p, t_s, t_p, cos_t;
     bool tir;
+    bool lossy = false;  // an interface with a lossy side (fresnel_c): no reference counterpart
 };
 
 struct Basis {
@@ -81,6 +82,18 @@ __device__ __forceinline__ Cx csqrt(Cx z) {
     const double m = hypot(z.re, z.im);
     const double a = sqrt(0.5 * (m + fabs(z.re)));
     const double b = 0.5 * z.im / a;
+    return z.re >= 0.0 ? Cx{a, b} : Cx{fabs(b), copysign(a, z.im)};
+}
+
+// the principal root on a lossy interface (no reference counterpart): |z|
+// as sqrt(re^2 + im^2) instead of hypot, one reciprocal square root instead
+// of sqrt + divide (|z| ~ 1e-6 .. 1e6 here, far from over/underflow)
+__device__ __forceinline__ Cx csqrt_lossy(Cx z) {
+    if (z.im == 0.0) return csqrt(z);
+    const double m = sqrt(z.re * z.re + z.im * z.im);
+    const double t = 0.5 * (m + fabs(z.re));
+    const double r = rsqrt(t);
+    const double a = t * r, b = 0.5 * z.im * r;
     return z.re >= 0.0 ? Cx{a, b} : Cx{fabs(b), copysign(a, z.im)};
 }
 
@@ -141,6 +154,7 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
     // the three of the Smith division, a few ulps from it for |n| ~ 1..1e3);
     // real indices keep cdiv, the reference's __divdc3, bit for bit.
     const bool lossy_if = n1.im != 0.0 || n2.im != 0.0;
+    c.lossy = lossy_if;
     auto inv = [](Cx d) {
         const double s = 1.0 / (d.re * d.re + d.im * d.im);
         return Cx{d.re * s, -(d.im * s)};
@@ -152,7 +166,7 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
     // evanescent one must decay away from the interface (Im k_z <= 0).  For
     // real indices this gives the reference's branches exactly: the real
     // root below the critical angle and (0, -sqrt(s2 - 1)) under TIR.
-    Cx cos_t = csqrt(Cx{1.0 - s2.re, -s2.im});
+    Cx cos_t = lossy_if ? csqrt_lossy(Cx{1.0 - s2.re, -s2.im}) : csqrt(Cx{1.0 - s2.re, -s2.im});
     const Cx kz = n2 * cos_t;
     const bool flip = fabs(kz.re) >= fabs(kz.im) ? kz.re < 0.0 : kz.im > 0.0;
     if (flip) cos_t = {-cos_t.re, -cos_t.im};

@@ -558,7 +558,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                             if (two) {
                                 double p_reflect = 0.5;
                                 if (P.fresnel_strategy) {
-                                    const double r_bar = 0.5 * (cabs(co.r_s) + cabs(co.r_p));
+                                    const double r_bar = co.lossy ? 0.5 * (sqrt(cnorm2(co.r_s)) + sqrt(cnorm2(co.r_p)))
+                                                          : 0.5 * (cabs(co.r_s) + cabs(co.r_p));
                                     const double lo_c = (r_bar < P.p_min) ? P.p_min : r_bar;
                                     const double hi_c = 1.0 - P.p_min;
                                     p_reflect = (hi_c < lo_c) ? hi_c : lo_c;
