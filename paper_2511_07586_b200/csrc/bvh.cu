@@ -61,8 +61,14 @@ struct Box {
 // hit.  Criterion: box surface area > kEscRatio x twice the triangle's area;
 // k = ceil(ratio / kEscTarget) <= kEscMaxPieces.  Well-shaped meshes (the
 // icospheres, the dihedral plates) have ratios <= ~5 and are not split.
-constexpr double kEscRatio = 16.0;
-constexpr double kEscTarget = 4.0;
+#ifndef MCSBR_ESC_RATIO
+#define MCSBR_ESC_RATIO 16.0
+#endif
+#ifndef MCSBR_ESC_TARGET
+#define MCSBR_ESC_TARGET 4.0
+#endif
+constexpr double kEscRatio = MCSBR_ESC_RATIO;
+constexpr double kEscTarget = MCSBR_ESC_TARGET;
 constexpr uint32_t kEscMaxPieces = 64;
 
 struct EscInfo {
