@@ -340,6 +340,16 @@ __global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restri
 }
 
 // sorted leaf boxes: lo_s[k] = lo[order[k]]
+// centroids of the primitives in the given order (the SAH build's cen array)
+__global__ void centroid_kernel(const float4* __restrict__ lo, const float4* __restrict__ hi,
+                                const uint32_t* __restrict__ order, int n, float4* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = order[i];
+    const float4 l = lo[p], h = hi[p];
+    out[i] = make_float4(0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z), 0.f);
+}
+
 __global__ void gather_boxes(const float4* __restrict__ lo, const float4* __restrict__ hi,
                              const uint32_t* __restrict__ ord, int n, float4* __restrict__ lo_s,
                              float4* __restrict__ hi_s) {
@@ -499,6 +509,11 @@ __device__ __forceinline__ float half_area(float lx, float ly, float lz, float h
 // Node ids come from the top of the id space (`down` counts down) and are
 // marked 2 in `ready`, which tells the persistent loop that no published
 // task remains above them.
+#ifdef MCSBR_SAH_TIMELINE
+// critical-path diagnostics (A/B builds only): (count, start ns, end ns) of the large tasks
+__device__ unsigned long long g_sah_tl[256][3];
+__device__ unsigned int g_sah_tl_n;
+#endif
 #ifdef MCSBR_SAH_PROF
 // build profile (A/B builds only): per phase, clock cycles summed over tasks
 // by each block's thread 0; [0] = waiting for a task, [8] = tasks, [9] = sum of counts
@@ -670,7 +685,8 @@ __device__ __noinline__ void warp_subtree(int first, int count, int root, const 
 
 __device__ __forceinline__ void sah_split(
     const SahTask t, const float4* __restrict__ blo, const float4* __restrict__ bhi,
-    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
+    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, float4* __restrict__ cen, float4* __restrict__ cen2,
+    int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
     int* __restrict__ ready, int* __restrict__ down) {
     SAHP0();
@@ -687,20 +703,20 @@ __device__ __forceinline__ void sah_split(
     const int end = t.first + t.count;
     const uint32_t* in = t.flip ? idx2 : idx;
     uint32_t* out = t.flip ? idx : idx2;
-    auto centroid = [&](uint32_t p, int a) {
-        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
-        const float lv = a == 0 ? l.x : (a == 1 ? l.y : l.z), hv = a == 0 ? h.x : (a == 1 ? h.y : h.z);
-        return 0.5f * (lv + hv);
-    };
+    // the primitives' centroids travel with their ids (cen pairs with idx,
+    // cen2 with idx2): the partition reads them in order instead of
+    // gathering two boxes per primitive (the top-level partitions, one block
+    // per node, are the build's critical path: c5's root took 3.6 ms)
+    const float4* cin = t.flip ? cen2 : cen;
+    float4* cout = t.flip ? cen : cen2;
     // large nodes (the top levels, one block each) choose their split from a
     // strided sample of ~16 k primitives; the partition below counts exactly
     const int stride = t.count > kSahSampleFrom ? t.count / kSahSample : 1;
     // 1. centroid bounds
     float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
-        const uint32_t p = in[i];
-        const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
-        const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
+        const float4 cc = cin[i];
+        const float c[3] = {cc.x, cc.y, cc.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             mn[a] = fminf(mn[a], c[a]);
@@ -740,7 +756,8 @@ __device__ __forceinline__ void sah_split(
     for (int i = t.first + tid * stride; i < end; i += kSahThreads * stride) {
         const uint32_t p = in[i];
         const float4 l = __ldg(blo + p), h = __ldg(bhi + p);
-        const float c[3] = {0.5f * (l.x + h.x), 0.5f * (l.y + h.y), 0.5f * (l.z + h.z)};
+        const float4 cc = cin[i];
+        const float c[3] = {cc.x, cc.y, cc.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (s_scale[a] == 0.0f) continue;
@@ -820,17 +837,22 @@ __device__ __forceinline__ void sah_split(
     // kPU sub-chunks of 256 per iteration: their loads issued together and
     // one barrier pair per iteration (a top-level node's partition is the
     // build's critical path)
-    constexpr int kPU = 4;
+#ifndef MCSBR_SAH_PU
+#define MCSBR_SAH_PU 4
+#endif
+    constexpr int kPU = MCSBR_SAH_PU;
     __shared__ int s_wl[kPU][kSahThreads / 32];
     int left_base = 0, right_base = 0;
     for (int base = t.first; base < end; base += kPU * kSahThreads) {
         uint32_t p[kPU];
+        float4 cp[kPU];
         bool valid[kPU], left[kPU];
 #pragma unroll
         for (int j = 0; j < kPU; ++j) {
             const int i = base + j * kSahThreads + tid;
             valid[j] = i < end;
             p[j] = valid[j] ? in[i] : 0u;
+            cp[j] = valid[j] ? cin[i] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int j = 0; j < kPU; ++j) {
@@ -838,7 +860,8 @@ __device__ __forceinline__ void sah_split(
             left[j] = false;
             if (valid[j]) {
                 if (axis >= 0) {
-                    const int b = min(kSahBins - 1, max(0, static_cast<int>((centroid(p[j], axis) - cmin) * scale)));
+                    const float ca = axis == 0 ? cp[j].x : (axis == 1 ? cp[j].y : cp[j].z);
+                    const int b = min(kSahBins - 1, max(0, static_cast<int>((ca - cmin) * scale)));
                     left[j] = b < split;
                 } else {
                     left[j] = (i - t.first) < nl;
@@ -871,6 +894,7 @@ __device__ __forceinline__ void sah_split(
                 const int pv = wv + __popc(v[j] & below);
                 const int pos = left[j] ? t.first + left_base + pl : end - 1 - (right_base + (pv - pl));
                 out[pos] = p[j];
+                cout[pos] = cp[j];
             }
             left_base += tl;
             right_base += tv - tl;
@@ -926,7 +950,8 @@ __device__ __forceinline__ void sah_split(
 // of one launch plus a host round trip per tree level.
 __global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
     int n_inner, int* __restrict__ head, const float4* __restrict__ blo, const float4* __restrict__ bhi,
-    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, int2* __restrict__ child, int2* __restrict__ range,
+    uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, float4* __restrict__ cen, float4* __restrict__ cen2,
+    int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
     int* __restrict__ ready, int* __restrict__ down) {
     __shared__ int s_id;
@@ -961,8 +986,25 @@ __global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
         }
         __syncthreads();
         if (s_id >= n_inner) break;
-        sah_split(s_task, blo, bhi, idx, idx2, child, range, par_i, par_l, node_counter, tasks, ready, down);
+#ifdef MCSBR_SAH_TIMELINE
+        unsigned long long tl0 = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
+#endif
+        sah_split(s_task, blo, bhi, idx, idx2, cen, cen2, child, range, par_i, par_l, node_counter, tasks, ready,
+                  down);
         __syncthreads();
+#ifdef MCSBR_SAH_TIMELINE
+        if (threadIdx.x == 0 && s_task.count >= 16384) {
+            unsigned long long tl1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
+            const unsigned k = atomicAdd(&g_sah_tl_n, 1u);
+            if (k < 256) {
+                g_sah_tl[k][0] = static_cast<unsigned long long>(s_task.count);
+                g_sah_tl[k][1] = tl0;
+                g_sah_tl[k][2] = tl1;
+            }
+        }
+#endif
     }
 }
 
@@ -1049,6 +1091,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     unsigned int* dmax = nullptr;
     unsigned int *is4 = nullptr, *idx4 = nullptr;
     uint32_t* sidx = nullptr;         // SAH: the final triangle order
+    float4 *cen = nullptr, *cen2 = nullptr;  // SAH: centroids travelling with the ids
     SahTask* tasks = nullptr;
     int* node_counter = nullptr;
     const uint32_t* order = nullptr;  // final leaf order (SAH or Morton)
@@ -1118,6 +1161,8 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
         bool sah = !(bvh_env && std::strcmp(bvh_env, "lbvh") == 0);
         if (sah) {
             BVH_CHECK(dev_malloc(&sidx, sizeof(uint32_t) * n));
+            BVH_CHECK(dev_malloc(&cen, sizeof(float4) * n));
+            BVH_CHECK(dev_malloc(&cen2, sizeof(float4) * n));
             BVH_CHECK(dev_malloc(&tasks, sizeof(SahTask) * inner));
             BVH_CHECK(dev_malloc(&node_counter, sizeof(int) * (inner + 3)));  // counter, head, ready[inner], down
             BVH_CHECK(cudaMemcpyAsync(sidx, ids_s, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
@@ -1133,13 +1178,31 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                 BVH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
                 BVH_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sah_build_kernel, kSahThreads, 0));
                 const int grid = std::max(1, std::min(inner, sms * std::max(per_sm, 1)));  // co-resident
+                centroid_kernel<<<G, B, 0, stream>>>(blo, bhi, sidx, n, cen);
+                BVH_CHECK(cudaGetLastError());
                 sah_build_kernel<<<grid, kSahThreads, 0, stream>>>(inner, node_counter + 1, blo, bhi, sidx, ids,
-                                                                   child, range, par_i, par_l, node_counter,
+                                                                   cen, cen2, child, range, par_i, par_l, node_counter,
                                                                    tasks, node_counter + 2, node_counter + inner + 2);
                 BVH_CHECK(cudaGetLastError());
             }
             depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
             BVH_CHECK(cudaGetLastError());
+#ifdef MCSBR_SAH_TIMELINE
+            {
+                unsigned long long tl[256][3];
+                unsigned int tn = 0;
+                BVH_CHECK(cudaMemcpyFromSymbolAsync(&tn, g_sah_tl_n, sizeof(tn), 0, cudaMemcpyDeviceToHost, stream));
+                BVH_CHECK(cudaMemcpyFromSymbolAsync(tl, g_sah_tl, sizeof(tl), 0, cudaMemcpyDeviceToHost, stream));
+                BVH_CHECK(cudaStreamSynchronize(stream));
+                unsigned long long t0 = ~0ull;
+                for (unsigned k = 0; k < std::min(tn, 256u); ++k) t0 = std::min(t0, tl[k][1]);
+                for (unsigned k = 0; k < std::min(tn, 256u); ++k)
+                    std::fprintf(stderr, "sah task %7llu prims: %8.3f .. %8.3f ms\n", tl[k][0], (tl[k][1] - t0) * 1e-6,
+                                 (tl[k][2] - t0) * 1e-6);
+                const unsigned z = 0;
+                BVH_CHECK(cudaMemcpyToSymbolAsync(g_sah_tl_n, &z, sizeof(z), 0, cudaMemcpyHostToDevice, stream));
+            }
+#endif
 #ifdef MCSBR_SAH_PROF
             {
                 unsigned long long pr[10];
@@ -1235,6 +1298,8 @@ done:
     dev_free(tmp, synced);
     dev_free(scan_tmp, synced);
     dev_free(sidx, synced);
+    dev_free(cen, synced);
+    dev_free(cen2, synced);
     dev_free(tasks, synced);
     dev_free(node_counter, synced);
     if (e0) cudaEventDestroy(e0);
