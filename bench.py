@@ -472,6 +472,23 @@ def main():
             ncu = pk.get("digest")
         except Exception:
             pass
+    # the cache-level picture of the same kernel from the committed ncu
+    # capture (one launch of the bench sweep): L1 / L2 bytes per launch, the
+    # bandwidth they imply over that launch, and their share of the unit's
+    # peak throughput as ncu reports it; issue-slot activity
+    cache_roofs = None
+    if ncu and ncu.get("duration_ms"):
+        dur = ncu["duration_ms"] / 1e3
+        cache_roofs = {
+            "l1_bytes_per_launch": ncu.get("l1_bytes_per_launch"),
+            "l1_GBps": None if ncu.get("l1_bytes_per_launch") is None else ncu["l1_bytes_per_launch"] / dur / 1e9,
+            "l1_throughput_pct_of_peak": ncu.get("l1_throughput_pct"),
+            "l2_bytes_per_launch": ncu.get("l2_bytes_per_launch"),
+            "l2_GBps": None if ncu.get("l2_bytes_per_launch") is None else ncu["l2_bytes_per_launch"] / dur / 1e9,
+            "l2_throughput_pct_of_peak": ncu.get("l2_throughput_pct"),
+            "issue_active_pct": ncu.get("issue_active_pct"),
+            "source": ncu.get("source"),
+        }
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     nf = len(W.freqs)
     contribs = int(st.contributions)
@@ -559,7 +576,8 @@ def main():
                                  "every node and triangle byte came from DRAM) x the queries the kernel traces "
                                  "(segments + occlusion queries, minus launch rays the coverage bitmap proves "
                                  "to miss), / the path kernel's own CUDA-event time over the timed steps. "
-                                 "DRAM is not what binds this kernel (see ncu): it is latency / issue bound."},
+                                 "DRAM is not what binds this kernel (see ncu): it is latency / issue bound.",
+                         "cache_roofs": cache_roofs},
             "ncu": ncu,
             "accumulation_roofline": acc,
             "cpu_baseline": cpu,

@@ -76,11 +76,16 @@ want = {
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_inst_pct",
     "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum": "local_ld_sectors",
     "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum": "local_st_sectors",
+    "lts__t_sectors.sum": "l2_sectors",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed": "l1_throughput_pct",
 }
 out = {"source": os.path.basename(rep), "command": command}
 for i, key in enumerate(h):
-    if key in want:
-        out[want[key]] = {"value": v[i], "unit": u[i]}
+    base = key.split(".", 2)[-1] if key.startswith(("SM_A.", "SM_B.", "LTS.", "DRAM.")) else key
+    if key in want or base in want:
+        out[want.get(key, want.get(base))] = {"value": v[i], "unit": u[i]}
+    elif base == "l1tex__t_sectors.sum":
+        out["l1_sectors"] = {"value": v[i], "unit": u[i]}
 stalls = {k.split("stalled_")[1]: float(x.replace(",", "")) for k, x in zip(h, v)
           if k.startswith("smsp__pcsamp_warps_issue_stalled_") and "not_issued" not in k and x}
 tot_s = sum(stalls.values()) or 1.0
@@ -113,6 +118,9 @@ if len(sys.argv) > 7:  # the bench workload's path-kernel evidence: profiles/pat
               "duration_ms": num("duration"), "dram_bytes_per_launch": dram,
               "l2_hit_pct": num("l2_hit_pct"), "l1_hit_pct": num("l1_hit_pct"),
               "l2_throughput_pct": num("l2_throughput_pct"),
+              "l1_throughput_pct": num("l1_throughput_pct"),
+              "l1_bytes_per_launch": None if num("l1_sectors") is None else 32 * num("l1_sectors"),
+              "l2_bytes_per_launch": None if num("l2_sectors") is None else 32 * num("l2_sectors"),
               "issue_active_pct": num("smsp_issue_active_pct"), "warps_active_per_sm": num("warps_active_per_sm"),
               "fp64_pipe_pct": num("fp64_pipe_pct"), "fp32_fma_pipe_pct": num("fma_pipe_pct"),
               "sfu_xu_inst_pct": num("sfu_xu_inst_pct"), "simt_threads_per_warp": num("simt_efficiency_threads"),
