@@ -44,6 +44,22 @@ __device__ __forceinline__ Coeffs coeffs_pec() {  // em_math.hpp:127-133
     return c;
 }
 
+// __divdc3 of two complex numbers with zero imaginary parts is
+// (num.re / den.re, +-0): ratio = 0, denom = c exactly, x = (a + 0) / c, and
+// its range scalings multiply numerator and denominator by the same power of
+// two (|c| in [2^-52, 2^1022] skips them anyway).  Real-index Fresnel
+// coefficients below the critical angle are exactly that case, so they take
+// one IEEE division inline instead of the out-of-line Smith division (which
+// was 10% of the lossless dielectric kernel's samples); the sign of a zero
+// imaginary part may differ, which no later operation can turn into a
+// non-zero difference.  Anything else goes to cdiv.
+__device__ __forceinline__ Cx cdiv_r(Cx num, Cx den) {
+    if (num.im == 0.0 && den.im == 0.0 && fabs(den.re) >= 2.220446049250313e-16 &&
+        fabs(den.re) < 8.98846567431158e307)
+        return {num.re / den.re, 0.0};
+    return cdiv(num, den);
+}
+
 __device__ inline Coeffs fresnel(double n1, double n2, double cos_i, uint32_t& fault) {
     Coeffs c;
     c.tir = false;
@@ -66,10 +82,10 @@ __device__ inline Coeffs fresnel(double n1, double n2, double cos_i, uint32_t& f
     const Cx ci = {cos_i, 0.0};
     const Cx den_s = ci * n1 + cos_t * n2;
     const Cx den_p = ci * n2 + cos_t * n1;
-    c.r_s = cdiv(ci * n1 - cos_t * n2, den_s);
-    c.t_s = cdiv(ci * (2.0 * n1), den_s);
-    c.r_p = cdiv(ci * n2 - cos_t * n1, den_p);
-    c.t_p = cdiv(ci * (2.0 * n1), den_p);
+    c.r_s = cdiv_r(ci * n1 - cos_t * n2, den_s);
+    c.t_s = cdiv_r(ci * (2.0 * n1), den_s);
+    c.r_p = cdiv_r(ci * n2 - cos_t * n1, den_p);
+    c.t_p = cdiv_r(ci * (2.0 * n1), den_p);
     return c;
 }
 
@@ -159,7 +175,7 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
         const double s = 1.0 / (d.re * d.re + d.im * d.im);
         return Cx{d.re * s, -(d.im * s)};
     };
-    const Cx q = lossy_if ? n1 * inv(n2) : cdiv(n1, n2);
+    const Cx q = lossy_if ? n1 * inv(n2) : cdiv_r(n1, n2);
     const Cx s2 = (q * q) * sin2_i;
     // Root choice for k_z = k0 n2 cos_t: a propagating transmitted wave
     // (|Re k_z| >= |Im k_z|) must carry power away (Re k_z >= 0); an
@@ -182,10 +198,10 @@ __device__ inline Coeffs fresnel_c(Cx n1, Cx n2, double cos_i, bool tir, uint32_
         c.r_p = (ci * n2 - cos_t * n1) * ip;
         c.t_p = (ci * (n1 * 2.0)) * ip;
     } else {
-        c.r_s = cdiv(ci * n1 - cos_t * n2, den_s);
-        c.t_s = cdiv(ci * (n1 * 2.0), den_s);
-        c.r_p = cdiv(ci * n2 - cos_t * n1, den_p);
-        c.t_p = cdiv(ci * (n1 * 2.0), den_p);
+        c.r_s = cdiv_r(ci * n1 - cos_t * n2, den_s);
+        c.t_s = cdiv_r(ci * (n1 * 2.0), den_s);
+        c.r_p = cdiv_r(ci * n2 - cos_t * n1, den_p);
+        c.t_p = cdiv_r(ci * (n1 * 2.0), den_p);
     }
     return c;
 }
