@@ -387,6 +387,7 @@ namespace {
 
 // scenes up to this many triangles get the long scheduling chunks (run_job)
 constexpr uint32_t kSmallSceneTris = 131072;
+constexpr uint32_t kLargeSceneTris = 524288;  // above: 512-entry chunk cap (c5), below 256 (c4)
 
 // launch_rect's axes (geometry.cpp:246-253): seed axis x, or y if |k.x| > 0.9
 void plan_axes(const double k_inc[3], V* k, V* u, V* v) {
@@ -845,7 +846,11 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // window, and fewer, longer chunks there save the per-chunk scheduling
     // and incidence changes (c2 -2.7% at 1024, -3.3% at 2048; c4 +4% at 512).
     // (A/B knobs sanitised: chunk sizes non-zero multiples of 32, min <= max)
-    p.chunk_max = std::max(32u, env_u32("MCSBR_CHUNK_MAX", s->nt <= kSmallSceneTris ? 2048u : 256u) / 32u * 32u);
+    // Measured (r02, same box): c5 (1 M triangles) 256 -> 512: path kernel
+    // -2.2% (lossy) / -2.3% (lossless twin), accumulation unchanged; 1024:
+    // +0.7%; c4 (200 k) 256 -> 512: +8%.
+    const uint32_t cap_default = s->nt <= kSmallSceneTris ? 2048u : (s->nt <= kLargeSceneTris ? 256u : 512u);
+    p.chunk_max = std::max(32u, env_u32("MCSBR_CHUNK_MAX", cap_default) / 32u * 32u);
     p.chunk_min = std::min(p.chunk_max, std::max(32u, env_u32("MCSBR_CHUNK_MIN", 32) / 32u * 32u));
     p.gss_div = env_u32("MCSBR_GSS", 16);
     // band height of the launch-entry dispatch order (0 = linear; a power of two)
