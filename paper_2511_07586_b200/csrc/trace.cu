@@ -871,28 +871,39 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
                 Cx am[4];
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) am[ch] = cx2(t[ch]);
+                auto sweep = [&](auto real_tag) {
+                    constexpr bool kReal = decltype(real_tag)::value;
 #pragma unroll
-                for (int m = 0; m < FPL; ++m) {
-                    const uint32_t f = f0 + 32u * m;
-                    if (kFull || f < f_end) {
+                    for (int m = 0; m < FPL; ++m) {
+                        const uint32_t f = f0 + 32u * m;
+                        if (kFull || f < f_end) {
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) {
-                            if (kRealAmp) {  // PEC scenes: the amplitudes are real
-                                acc[m][2 * ch] = __fma_rn(am[ch].re, z.re, acc[m][2 * ch]);
-                                acc[m][2 * ch + 1] = __fma_rn(am[ch].re, z.im, acc[m][2 * ch + 1]);
-                            } else {
-                                acc[m][2 * ch] =
-                                    __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, acc[m][2 * ch]));
-                                acc[m][2 * ch + 1] =
-                                    __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
+                            for (int ch = 0; ch < 4; ++ch) {
+                                if (kReal) {  // real amplitudes: half the products
+                                    acc[m][2 * ch] = __fma_rn(am[ch].re, z.re, acc[m][2 * ch]);
+                                    acc[m][2 * ch + 1] = __fma_rn(am[ch].re, z.im, acc[m][2 * ch + 1]);
+                                } else {
+                                    acc[m][2 * ch] =
+                                        __fma_rn(am[ch].re, z.re, __fma_rn(-am[ch].im, z.im, acc[m][2 * ch]));
+                                    acc[m][2 * ch + 1] =
+                                        __fma_rn(am[ch].re, z.im, __fma_rn(am[ch].im, z.re, acc[m][2 * ch + 1]));
+                                }
+                            }
+                            if (m + 1 < FPL && (kFull || f + 32u < f_end)) {
+                                if (kUniform) z = cmul(z, w);
+                                else z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
                             }
                         }
-                        if (m + 1 < FPL && (kFull || f + 32u < f_end)) {
-                            if (kUniform) z = cmul(z, w);
-                            else z = phasor(P.k0[f + 32u], Cx{t4.x, t4.y});
-                        }
                     }
-                }
+                };
+                // PEC scenes: every amplitude is real; otherwise a record whose
+                // four amplitudes are real (a path that met only PEC surfaces
+                // and lossless interfaces) takes the real sweep as well --
+                // warp-uniform, the warp works on one record at a time
+                if (kRealAmp || (am[0].im == 0.0 && am[1].im == 0.0 && am[2].im == 0.0 && am[3].im == 0.0))
+                    sweep(std::true_type{});
+                else
+                    sweep(std::false_type{});
             }
             __syncwarp();
         }
