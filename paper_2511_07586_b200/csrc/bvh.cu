@@ -24,6 +24,7 @@
 // (Scene::intersect_brute_force, geometry.cpp:218-240) for ANY tree shape.
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1146,8 +1147,17 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     tmp_bytes = radix_sort_temp_bytes(n);
     BVH_CHECK(dev_malloc(&tmp, tmp_bytes));
     {
+#ifdef MCSBR_BVH_PHASES
+        cudaStreamSynchronize(stream);
+        const auto ph0 = std::chrono::steady_clock::now();
+#endif
         bool in_alt = false;
         BVH_CHECK(radix_sort_pairs(keys, keys_s, ids, ids_s, n, 64, tmp, stream, &in_alt));
+#ifdef MCSBR_BVH_PHASES
+        cudaStreamSynchronize(stream);
+        std::fprintf(stderr, "[bvh] sort %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ph0).count());
+#endif
         if (!in_alt) {
             std::swap(keys, keys_s);
             std::swap(ids, ids_s);
