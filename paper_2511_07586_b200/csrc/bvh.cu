@@ -684,12 +684,235 @@ __device__ __noinline__ void warp_subtree(int first, int count, int root, const 
     if (lane < count) idx[first + lane] = p;
 }
 
+// Cooperative partition of the large nodes (the build's critical path is
+// the chain of top-level partitions, one block per node: c5's root of 1.04 M
+// references took 1.6 ms, its 838 k child 1.4 ms).  A block that takes a
+// node of at least kCoopMin references still chooses the split itself (from
+// the sample), then publishes the partition as a job of chunks in a slot of
+// `jobs`: blocks that are waiting for their next task grab chunks meanwhile.
+// Phase 1 counts each chunk's left references; the owner turns the counts
+// into per-chunk prefixes; phase 2 scatters every chunk to its final place.
+// The permutation is exactly the single-block partition's (left side in
+// order from `first`, right side in order from `end - 1` down), so the tree
+// does not change.  The owner works on its own job too, so progress never
+// depends on helpers.
+constexpr int kCoopSlots = 16;
+constexpr int kCoopMaxChunks = 1024;
+#ifndef MCSBR_SAH_COOP_MIN
+#define MCSBR_SAH_COOP_MIN 65536
+#endif
+constexpr int kCoopMin = MCSBR_SAH_COOP_MIN;
+constexpr int kCoopIdle = 0x3fffffff;  // next1 / next2 of a slot with no open phase
+
+struct CoopJob {
+    int first, end, flip, axis, split, nl_pos, chunk, nchunks;
+    float cmin, scale;
+    int next1, done1, next2, done2, owner, pad;
+};
+
+struct CoopArgs {
+    CoopJob* jobs;
+    int* counts;  // [kCoopSlots][kCoopMaxChunks] left references per chunk, then exclusive prefixes
+};
+
+// Block-wide partition of the span [lo, hi) of a node [first, end): a left
+// reference goes to first + lb + (its rank among the span's left ones), a
+// right one to end - 1 - (rb + its rank among the right ones).  write =
+// false only counts.  Returns the span's left count (every thread).
+__device__ int partition_span(int lo, int hi, int first, int end, int axis, int split, float cmin, float scale,
+                              int nl_pos, const uint32_t* in, uint32_t* out, const float4* cin, float4* cout,
+                              int lb, int rb, bool write) {
+#ifndef MCSBR_SAH_PU
+#define MCSBR_SAH_PU 4
+#endif
+    constexpr int kPU = MCSBR_SAH_PU;
+    __shared__ int s_wl[kPU][kSahThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int left_base = 0, right_base = 0;
+    for (int base = lo; base < hi; base += kPU * kSahThreads) {
+        uint32_t p[kPU];
+        float4 cp[kPU];
+        bool valid[kPU], left[kPU];
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            const int i = base + j * kSahThreads + tid;
+            valid[j] = i < hi;
+            p[j] = valid[j] && write ? __ldcg(in + i) : 0u;
+            cp[j] = valid[j] ? __ldcg(cin + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            const int i = base + j * kSahThreads + tid;
+            left[j] = false;
+            if (valid[j]) {
+                if (axis >= 0) {
+                    const float ca = axis == 0 ? cp[j].x : (axis == 1 ? cp[j].y : cp[j].z);
+                    const int b = min(kSahBins - 1, max(0, static_cast<int>((ca - cmin) * scale)));
+                    left[j] = b < split;
+                } else {
+                    left[j] = (i - first) < nl_pos;
+                }
+            }
+        }
+        unsigned m[kPU], v[kPU];
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            m[j] = __ballot_sync(0xffffffffu, valid[j] && left[j]);
+            v[j] = __ballot_sync(0xffffffffu, valid[j]);
+            if (lane == 0) s_wl[j][wid] = __popc(m[j]) | (__popc(v[j]) << 16);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kPU; ++j) {
+            int wl = 0, wv = 0, tl = 0, tv = 0;
+            for (int w = 0; w < kSahThreads / 32; ++w) {
+                const int x = s_wl[j][w];
+                if (w < wid) {
+                    wl += x & 0xffff;
+                    wv += x >> 16;
+                }
+                tl += x & 0xffff;
+                tv += x >> 16;
+            }
+            if (write && valid[j]) {
+                const unsigned below = (1u << lane) - 1u;
+                const int pl = wl + __popc(m[j] & below);
+                const int pv = wv + __popc(v[j] & below);
+                const int pos = left[j] ? first + lb + left_base + pl : end - 1 - (rb + right_base + (pv - pl));
+                out[pos] = p[j];
+                cout[pos] = cp[j];
+            }
+            left_base += tl;
+            right_base += tv - tl;
+        }
+        __syncthreads();
+    }
+    return left_base;
+}
+
+// one chunk of slot `slot`'s open phase (block-wide), then its done count
+__device__ void coop_chunk(const CoopArgs& ca, int slot, int phase, int c, uint32_t* idx, uint32_t* idx2,
+                           float4* cen, float4* cen2) {
+    const volatile CoopJob* J = ca.jobs + slot;
+    const int first = J->first, end = J->end, flip = J->flip, chunk = J->chunk;
+    const int lo = first + c * chunk, hi = min(end, lo + chunk);
+    const uint32_t* in = flip ? idx2 : idx;
+    uint32_t* out = flip ? idx : idx2;
+    const float4* cin = flip ? cen2 : cen;
+    float4* cout = flip ? cen : cen2;
+    int* cnt = ca.counts + slot * kCoopMaxChunks;
+    if (phase == 1) {
+        const int l = partition_span(lo, hi, first, end, J->axis, J->split, J->cmin, J->scale, J->nl_pos, in, out,
+                                     cin, cout, 0, 0, false);
+        if (threadIdx.x == 0) cnt[c] = l;
+    } else {
+        const int lb = __ldcg(cnt + c);
+        partition_span(lo, hi, first, end, J->axis, J->split, J->cmin, J->scale, J->nl_pos, in, out, cin, cout, lb,
+                       (lo - first) - lb, true);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(phase == 1 ? &ca.jobs[slot].done1 : &ca.jobs[slot].done2, 1);
+}
+
+// thread 0: grab a chunk of any open cooperative phase
+__device__ __forceinline__ bool coop_grab(const CoopArgs& ca, int* slot, int* phase, int* c) {
+    for (int s = 0; s < kCoopSlots; ++s) {
+        volatile CoopJob* J = ca.jobs + s;
+        if (J->owner < 0) continue;
+        for (int ph = 1; ph <= 2; ++ph) {
+            int* nx = ph == 1 ? &ca.jobs[s].next1 : &ca.jobs[s].next2;
+            if (*reinterpret_cast<volatile int*>(nx) < J->nchunks) {
+                const int k = atomicAdd(nx, 1);
+                __threadfence();
+                if (k < J->nchunks) {
+                    *slot = s;
+                    *phase = ph;
+                    *c = k;
+                    return true;
+                }
+            }
+        }
+    }
+    return false;
+}
+
+// the owner's side of a cooperative partition; returns the left count
+__device__ int coop_partition(const CoopArgs& ca, int node, int first, int end, int flip, int axis, int split,
+                              float cmin, float scale, int nl_pos, uint32_t* idx, uint32_t* idx2, float4* cen,
+                              float4* cen2) {
+    __shared__ int s_slot, s_c, s_total;
+    const int count = end - first;
+    if (threadIdx.x == 0) {
+        int slot = 0;
+        while (atomicCAS(&ca.jobs[slot].owner, -1, node) != -1) slot = (slot + 1) % kCoopSlots;
+        CoopJob* J = ca.jobs + slot;
+        int chunk = (count + kCoopMaxChunks - 1) / kCoopMaxChunks;
+        chunk = max(4096, (chunk + 1023) / 1024 * 1024);
+        J->first = first;
+        J->end = end;
+        J->flip = flip;
+        J->axis = axis;
+        J->split = split;
+        J->nl_pos = nl_pos;
+        J->chunk = chunk;
+        J->nchunks = (count + chunk - 1) / chunk;
+        J->cmin = cmin;
+        J->scale = scale;
+        J->done1 = 0;
+        J->done2 = 0;
+        J->next2 = kCoopIdle;
+        __threadfence();
+        atomicExch(&J->next1, 0);  // phase 1 open
+        s_slot = slot;
+    }
+    __syncthreads();
+    const int slot = s_slot;
+    CoopJob* J = ca.jobs + slot;
+    const int nchunks = *reinterpret_cast<volatile int*>(&J->nchunks);
+    for (int phase = 1; phase <= 2; ++phase) {
+        int* nx = phase == 1 ? &J->next1 : &J->next2;
+        int* dn = phase == 1 ? &J->done1 : &J->done2;
+        for (;;) {  // work on the own job's chunks
+            if (threadIdx.x == 0) s_c = atomicAdd(nx, 1);
+            __syncthreads();
+            const int c = s_c;
+            __syncthreads();
+            if (c >= nchunks) break;
+            coop_chunk(ca, slot, phase, c, idx, idx2, cen, cen2);
+        }
+        if (threadIdx.x == 0) {
+            while (*reinterpret_cast<volatile int*>(dn) < nchunks) __nanosleep(32);
+            __threadfence();
+            if (phase == 1) {  // chunk counts -> exclusive prefixes (in place), total
+                int* cnt = ca.counts + slot * kCoopMaxChunks;
+                int run = 0;
+                for (int k = 0; k < nchunks; ++k) {
+                    const int v = __ldcg(cnt + k);
+                    cnt[k] = run;
+                    run += v;
+                }
+                s_total = run;
+                __threadfence();
+                atomicExch(&J->next2, 0);  // phase 2 open
+            } else {
+                atomicExch(&J->next1, kCoopIdle);
+                atomicExch(&J->next2, kCoopIdle);
+                __threadfence();
+                atomicExch(&J->owner, -1);
+            }
+        }
+        __syncthreads();
+    }
+    return s_total;
+}
+
 __device__ __forceinline__ void sah_split(
     const SahTask t, const float4* __restrict__ blo, const float4* __restrict__ bhi,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, float4* __restrict__ cen, float4* __restrict__ cen2,
     int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
-    int* __restrict__ ready, int* __restrict__ down) {
+    int* __restrict__ ready, int* __restrict__ down, const CoopArgs ca) {
     SAHP0();
     __shared__ int s_cnt[3][kSahBins];
     __shared__ int s_box[3][kSahBins][6];
@@ -835,73 +1058,16 @@ __device__ __forceinline__ void sah_split(
     // 4. partition of [first, end) from `in` into `out`: the left side from
     // `first` up in order, the right side from `end - 1` down, so one pass
     // needs no left count (a sampled split's exact count falls out of it)
-    // kPU sub-chunks of 256 per iteration: their loads issued together and
-    // one barrier pair per iteration (a top-level node's partition is the
-    // build's critical path)
-#ifndef MCSBR_SAH_PU
-#define MCSBR_SAH_PU 4
-#endif
-    constexpr int kPU = MCSBR_SAH_PU;
-    __shared__ int s_wl[kPU][kSahThreads / 32];
-    int left_base = 0, right_base = 0;
-    for (int base = t.first; base < end; base += kPU * kSahThreads) {
-        uint32_t p[kPU];
-        float4 cp[kPU];
-        bool valid[kPU], left[kPU];
-#pragma unroll
-        for (int j = 0; j < kPU; ++j) {
-            const int i = base + j * kSahThreads + tid;
-            valid[j] = i < end;
-            p[j] = valid[j] ? in[i] : 0u;
-            cp[j] = valid[j] ? cin[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < kPU; ++j) {
-            const int i = base + j * kSahThreads + tid;
-            left[j] = false;
-            if (valid[j]) {
-                if (axis >= 0) {
-                    const float ca = axis == 0 ? cp[j].x : (axis == 1 ? cp[j].y : cp[j].z);
-                    const int b = min(kSahBins - 1, max(0, static_cast<int>((ca - cmin) * scale)));
-                    left[j] = b < split;
-                } else {
-                    left[j] = (i - t.first) < nl;
-                }
-            }
-        }
-        unsigned m[kPU], v[kPU];
-#pragma unroll
-        for (int j = 0; j < kPU; ++j) {
-            m[j] = __ballot_sync(0xffffffffu, valid[j] && left[j]);
-            v[j] = __ballot_sync(0xffffffffu, valid[j]);
-            if (lane == 0) s_wl[j][wid] = __popc(m[j]) | (__popc(v[j]) << 16);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kPU; ++j) {
-            int wl = 0, wv = 0, tl = 0, tv = 0;
-            for (int w = 0; w < kSahThreads / 32; ++w) {
-                const int x = s_wl[j][w];
-                if (w < wid) {
-                    wl += x & 0xffff;
-                    wv += x >> 16;
-                }
-                tl += x & 0xffff;
-                tv += x >> 16;
-            }
-            if (valid[j]) {
-                const unsigned below = (1u << lane) - 1u;
-                const int pl = wl + __popc(m[j] & below);
-                const int pv = wv + __popc(v[j] & below);
-                const int pos = left[j] ? t.first + left_base + pl : end - 1 - (right_base + (pv - pl));
-                out[pos] = p[j];
-                cout[pos] = cp[j];
-            }
-            left_base += tl;
-            right_base += tv - tl;
-        }
-        __syncthreads();
-    }
+    // (kPU sub-chunks of 256 per iteration in partition_span: their loads
+    // issued together, one barrier pair per iteration); large nodes
+    // cooperatively with the waiting blocks
+    int left_base;
+    if (t.count >= kCoopMin && ca.jobs)
+        left_base = coop_partition(ca, t.node, t.first, end, t.flip, axis, split, cmin, scale, nl, idx, idx2, cen,
+                                   cen2);
+    else
+        left_base = partition_span(t.first, end, t.first, end, axis, split, cmin, scale, nl, in, out, cin, cout, 0, 0,
+                                   true);
     nl = left_base;
     if (nl == 0 || nl == t.count) nl = t.count / 2;  // a sampled split that separates nothing: by position
     SAHP(5);
@@ -954,45 +1120,60 @@ __global__ void __launch_bounds__(kSahThreads, 4) sah_build_kernel(
     uint32_t* __restrict__ idx, uint32_t* __restrict__ idx2, float4* __restrict__ cen, float4* __restrict__ cen2,
     int2* __restrict__ child, int2* __restrict__ range,
     int* __restrict__ par_i, int* __restrict__ par_l, int* __restrict__ node_counter, SahTask* __restrict__ tasks,
-    int* __restrict__ ready, int* __restrict__ down) {
+    int* __restrict__ ready, int* __restrict__ down, const CoopArgs ca) {
     __shared__ int s_id;
     __shared__ SahTask s_task;
+    __shared__ int s_help[3];  // slot, phase, chunk of a cooperative partition to help with (slot -1: none)
     for (;;) {
-        if (threadIdx.x == 0) {
-#ifdef MCSBR_SAH_PROF
-            const long long w0 = clock64();
-#endif
-            int i = atomicAdd(head, 1);
-            if (i < n_inner) {
-                int r;
-                while ((r = atomicAdd(ready + i, 0)) == 0) __nanosleep(64);
-                if (r == 2) {
-                    i = n_inner;  // a warp-built node: every id from here up is one
-                } else {
-                    __threadfence();
-                    s_task.first = __ldcg(&tasks[i].first);
-                    s_task.count = __ldcg(&tasks[i].count);
-                    s_task.node = __ldcg(&tasks[i].node);
-                    s_task.flip = __ldcg(&tasks[i].flip);
-                }
-            }
-            s_id = i;
-#ifdef MCSBR_SAH_PROF
-            atomicAdd(&g_sah_prof[0], static_cast<unsigned long long>(clock64() - w0));
-            if (i < n_inner) {
-                atomicAdd(&g_sah_prof[8], 1ull);
-                atomicAdd(&g_sah_prof[9], static_cast<unsigned long long>(s_task.count));
-            }
-#endif
-        }
+        if (threadIdx.x == 0) s_id = atomicAdd(head, 1);
         __syncthreads();
+        const int i0 = s_id;
+        __syncthreads();
+        if (i0 >= n_inner) break;
+        // wait for task i0; meanwhile help the open cooperative partitions
+        for (;;) {
+            if (threadIdx.x == 0) {
+#ifdef MCSBR_SAH_PROF
+                const long long w0 = clock64();
+#endif
+                s_help[0] = -1;
+                for (;;) {
+                    const int r = atomicAdd(ready + i0, 0);
+                    if (r != 0) {
+                        if (r == 2) {
+                            s_id = n_inner;  // a warp-built node: every id from here up is one
+                        } else {
+                            __threadfence();
+                            s_task.first = __ldcg(&tasks[i0].first);
+                            s_task.count = __ldcg(&tasks[i0].count);
+                            s_task.node = __ldcg(&tasks[i0].node);
+                            s_task.flip = __ldcg(&tasks[i0].flip);
+                        }
+                        break;
+                    }
+                    if (ca.jobs && coop_grab(ca, &s_help[0], &s_help[1], &s_help[2])) break;
+                    __nanosleep(64);
+                }
+#ifdef MCSBR_SAH_PROF
+                atomicAdd(&g_sah_prof[0], static_cast<unsigned long long>(clock64() - w0));
+                if (s_help[0] < 0 && s_id < n_inner) {
+                    atomicAdd(&g_sah_prof[8], 1ull);
+                    atomicAdd(&g_sah_prof[9], static_cast<unsigned long long>(s_task.count));
+                }
+#endif
+            }
+            __syncthreads();
+            if (s_help[0] < 0) break;
+            coop_chunk(ca, s_help[0], s_help[1], s_help[2], idx, idx2, cen, cen2);
+            __syncthreads();
+        }
         if (s_id >= n_inner) break;
 #ifdef MCSBR_SAH_TIMELINE
         unsigned long long tl0 = 0;
         if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
 #endif
         sah_split(s_task, blo, bhi, idx, idx2, cen, cen2, child, range, par_i, par_l, node_counter, tasks, ready,
-                  down);
+                  down, ca);
         __syncthreads();
 #ifdef MCSBR_SAH_TIMELINE
         if (threadIdx.x == 0 && s_task.count >= 16384) {
@@ -1093,6 +1274,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     unsigned int *is4 = nullptr, *idx4 = nullptr;
     uint32_t* sidx = nullptr;         // SAH: the final triangle order
     float4 *cen = nullptr, *cen2 = nullptr;  // SAH: centroids travelling with the ids
+    void *coop_jobs = nullptr, *coop_counts = nullptr;  // SAH: cooperative partition slots
     SahTask* tasks = nullptr;
     int* node_counter = nullptr;
     const uint32_t* order = nullptr;  // final leaf order (SAH or Morton)
@@ -1190,9 +1372,23 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                 const int grid = std::max(1, std::min(inner, sms * std::max(per_sm, 1)));  // co-resident
                 centroid_kernel<<<G, B, 0, stream>>>(blo, bhi, sidx, n, cen);
                 BVH_CHECK(cudaGetLastError());
+                CoopArgs ca{nullptr, nullptr};
+                if (n >= kCoopMin) {  // cooperative partitions of the large nodes
+                    BVH_CHECK(dev_malloc(&coop_jobs, sizeof(CoopJob) * kCoopSlots));
+                    BVH_CHECK(dev_malloc(&coop_counts, sizeof(int) * kCoopSlots * kCoopMaxChunks));
+                    CoopJob init[kCoopSlots];
+                    std::memset(init, 0, sizeof(init));
+                    for (CoopJob& j : init) {
+                        j.owner = -1;
+                        j.next1 = j.next2 = kCoopIdle;
+                    }
+                    BVH_CHECK(cudaMemcpyAsync(coop_jobs, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+                    ca = CoopArgs{static_cast<CoopJob*>(coop_jobs), static_cast<int*>(coop_counts)};
+                }
                 sah_build_kernel<<<grid, kSahThreads, 0, stream>>>(inner, node_counter + 1, blo, bhi, sidx, ids,
                                                                    cen, cen2, child, range, par_i, par_l, node_counter,
-                                                                   tasks, node_counter + 2, node_counter + inner + 2);
+                                                                   tasks, node_counter + 2, node_counter + inner + 2,
+                                                                   ca);
                 BVH_CHECK(cudaGetLastError());
             }
             depth_kernel<<<G, B, 0, stream>>>(n, par_i, par_l, dmax);
@@ -1310,6 +1506,8 @@ done:
     dev_free(sidx, synced);
     dev_free(cen, synced);
     dev_free(cen2, synced);
+    dev_free(coop_jobs, synced);
+    dev_free(coop_counts, synced);
     dev_free(tasks, synced);
     dev_free(node_counter, synced);
     if (e0) cudaEventDestroy(e0);

@@ -5,8 +5,10 @@
 // buffers.  Per pass:
 //   1. digit_hist_kernel   one block per 4096-element tile counts its digits
 //                          (shared-memory atomics) -> hist[digit][tile];
-//   2. scan over hist      (digit-major, so the exclusive prefix of
-//                          hist[d][t] is where tile t's digit-d elements go);
+//   2. digit_scan_kernel   (digit-major, so the exclusive prefix of
+//                          hist[d][t] is where tile t's digit-d elements go):
+//                          one warp per digit, its base from the digit totals
+//                          the histogram kernel accumulated;
 //   3. digit_scatter_kernel the tile again, each warp owning 512 consecutive
 //                          elements in 16 rounds of 32: __match_any_sync
 //                          groups a round's lanes by digit, per-warp digit
@@ -39,7 +41,8 @@ constexpr int kRadix = 256;
 
 __global__ void __launch_bounds__(kThreads) digit_hist_kernel(const uint64_t* __restrict__ keys, uint32_t n,
                                                               int shift, uint32_t n_tiles,
-                                                              uint32_t* __restrict__ hist) {
+                                                              uint32_t* __restrict__ hist,
+                                                              uint32_t* __restrict__ totals) {
     __shared__ uint32_t h[kRadix];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -50,7 +53,42 @@ __global__ void __launch_bounds__(kThreads) digit_hist_kernel(const uint64_t* __
         if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
     }
     __syncthreads();
-    hist[static_cast<uint64_t>(threadIdx.x) * n_tiles + blockIdx.x] = h[threadIdx.x];
+    const uint32_t c = h[threadIdx.x];
+    hist[static_cast<uint64_t>(threadIdx.x) * n_tiles + blockIdx.x] = c;
+    if (c) atomicAdd(totals + threadIdx.x, c);
+}
+
+// digit offsets for the scatter: one warp per digit d.  The digit's base is
+// the sum of the totals of the digits below it; its row hist[d][0..T) is
+// scanned 32 tiles at a time.  (A single block scanning all 256 x T entries
+// took ~10x longer: it was ~70% of a 1 M-element sort.)
+__global__ void __launch_bounds__(256) digit_scan_kernel(const uint32_t* __restrict__ hist,
+                                                         const uint32_t* __restrict__ totals, uint32_t n_tiles,
+                                                         uint32_t* __restrict__ offs) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t d = blockIdx.x * 8 + (threadIdx.x >> 5);
+    uint32_t base = 0;
+#pragma unroll
+    for (int k = 0; k < kRadix / 32; ++k) {
+        const uint32_t dd = static_cast<uint32_t>(lane) * (kRadix / 32) + k;
+        if (dd < d) base += totals[dd];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+    const uint32_t* row = hist + static_cast<uint64_t>(d) * n_tiles;
+    uint32_t* orow = offs + static_cast<uint64_t>(d) * n_tiles;
+    for (uint32_t t0 = 0; t0 < n_tiles; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        const uint32_t v = t < n_tiles ? row[t] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (t < n_tiles) orow[t] = base + x - v;
+        base += __shfl_sync(0xffffffffu, x, 31);
+    }
 }
 
 // exclusive scan of n values in ONE block of 1024 threads (each thread a
@@ -208,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) tile_scan_kernel(const uint32_t* __r
 
 size_t radix_sort_temp_bytes(uint32_t n) {
     const uint64_t tiles = (static_cast<uint64_t>(n) + kTile - 1) / kTile;
-    return sizeof(uint32_t) * 2 * kRadix * std::max<uint64_t>(tiles, 1);
+    return sizeof(uint32_t) * (2 * kRadix * std::max<uint64_t>(tiles, 1) + 8 * kRadix);  // + per-pass totals
 }
 
 cudaError_t radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint32_t n,
@@ -218,11 +256,17 @@ cudaError_t radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals,
     const uint32_t tiles = static_cast<uint32_t>((static_cast<uint64_t>(n) + kTile - 1) / kTile);
     uint32_t* hist = static_cast<uint32_t*>(temp);
     uint32_t* offs = hist + static_cast<uint64_t>(kRadix) * tiles;
+    uint32_t* totals = offs + static_cast<uint64_t>(kRadix) * tiles;  // [8 passes][256]
+    const int passes = (key_bits + 7) / 8;
+    if (passes > 8) return cudaErrorInvalidValue;
+    cudaError_t z = cudaMemsetAsync(totals, 0, sizeof(uint32_t) * kRadix * passes, stream);
+    if (z != cudaSuccess) return z;
     uint64_t *kin = keys, *kout = keys_alt;
     uint32_t *vin = vals, *vout = vals_alt;
     for (int shift = 0; shift < key_bits; shift += 8) {
-        digit_hist_kernel<<<tiles, kThreads, 0, stream>>>(kin, n, shift, tiles, hist);
-        scan_one_block_kernel<<<1, 1024, 0, stream>>>(hist, offs, kRadix * tiles);
+        uint32_t* tot = totals + kRadix * (shift / 8);
+        digit_hist_kernel<<<tiles, kThreads, 0, stream>>>(kin, n, shift, tiles, hist, tot);
+        digit_scan_kernel<<<kRadix / 8, 256, 0, stream>>>(hist, tot, tiles, offs);
         digit_scatter_kernel<<<tiles, kThreads, 0, stream>>>(kin, vin, n, shift, tiles, offs, kout, vout);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
