@@ -479,6 +479,19 @@ struct SahTask {
 #endif
 constexpr int kSahBins = MCSBR_SAH_BINS;
 constexpr int kSahThreads = 256;
+static uint32_t env_u32_bvh(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+// scenes up to this many references skip the Morton pre-sort before the SAH
+// build (all of them: the binned SAH splits do not need the order; trees
+// of the same quality -- kernel times within noise on c1, c2, c4 and the c5
+// bench sweep -- and the builds save the sort: c5 5.5 -> 5.1 ms, c4 1.85 ->
+// 1.6, c2 0.75 -> 0.54, c1 0.85 -> 0.58 ms); the Karras fallback still sorts
+#ifndef MCSBR_NO_PRESORT_MAX
+#define MCSBR_NO_PRESORT_MAX 0xffffffffu
+#endif
+constexpr uint32_t kNoPresortMax = MCSBR_NO_PRESORT_MAX;
 #ifndef MCSBR_SAH_SAMPLE
 #define MCSBR_SAH_SAMPLE 4096
 #endif
@@ -1286,6 +1299,10 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     const int G = (n + B - 1) / B;
     const int inner = n > 1 ? n - 1 : 1;
     double s[3];
+    // the Morton pre-sort is skipped for small scenes when the SAH build runs (below)
+    const char* bvh_env0 = std::getenv("MCSBR_BVH");
+    const bool sah_wanted = !(bvh_env0 && std::strcmp(bvh_env0, "lbvh") == 0);
+    const bool presort = !(sah_wanted && n <= static_cast<int>(env_u32_bvh("MCSBR_BVH_PRESORT_MAX", kNoPresortMax)));
     out->nodes = nullptr;
     out->tri64 = nullptr;
     for (int k = 0; k < 3; ++k) {
@@ -1325,10 +1342,15 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
                                      ids, blo, bhi);
     BVH_CHECK(cudaGetLastError());
     // stable LSD radix sort of the (Morton key, reference) pairs (sort.cu);
-    // the sorted pairs end up in keys_s / ids_s
+    // the sorted pairs end up in keys_s / ids_s.  Skipped when the SAH build
+    // runs (kNoPresortMax, MCSBR_BVH_PRESORT_MAX): the binned SAH only needs
+    // the references in any order (its splits are spatial); the Karras
+    // fallback sorts when it is needed.
     tmp_bytes = radix_sort_temp_bytes(n);
     BVH_CHECK(dev_malloc(&tmp, tmp_bytes));
-    {
+    if (!presort) {
+        BVH_CHECK(cudaMemcpyAsync(ids_s, ids, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, stream));
+    } else {
 #ifdef MCSBR_BVH_PHASES
         cudaStreamSynchronize(stream);
         const auto ph0 = std::chrono::steady_clock::now();
@@ -1347,7 +1369,7 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     }
     order = ids_s;
     if (n > 1) {
-        // binned SAH from the Morton order (locality), unless MCSBR_BVH=lbvh or
+        // binned SAH (from the reference order), unless MCSBR_BVH=lbvh or
         // the tree comes out deeper than the traversal stack allows
         const char* bvh_env = std::getenv("MCSBR_BVH");
         bool sah = !(bvh_env && std::strcmp(bvh_env, "lbvh") == 0);
@@ -1428,6 +1450,15 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
             if (3 * ((md + 1) / 2 + 1) > static_cast<unsigned>(kStackSize)) {
                 sah = false;  // too deep for the traversal stack: Karras tree instead
                 BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
+                if (!presort) {  // the Karras tree needs the Morton order
+                    bool in_alt = false;
+                    BVH_CHECK(radix_sort_pairs(keys, keys_s, ids, ids_s, n, 64, tmp, stream, &in_alt));
+                    if (!in_alt) {
+                        std::swap(keys, keys_s);
+                        std::swap(ids, ids_s);
+                    }
+                    order = ids_s;
+                }
                 BVH_CHECK(cudaMemsetAsync(par_i, 0xff, sizeof(int) * inner, stream));
                 BVH_CHECK(cudaMemsetAsync(par_l, 0xff, sizeof(int) * n, stream));
             } else {
