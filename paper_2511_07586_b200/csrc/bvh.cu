@@ -484,10 +484,11 @@ static uint32_t env_u32_bvh(const char* name, uint32_t dflt) {
     return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
 }
 // scenes up to this many references skip the Morton pre-sort before the SAH
-// build (all of them: the binned SAH splits do not need the order; trees
-// of the same quality -- kernel times within noise on c1, c2, c4 and the c5
-// bench sweep -- and the builds save the sort: c5 5.5 -> 5.1 ms, c4 1.85 ->
-// 1.6, c2 0.75 -> 0.54, c1 0.85 -> 0.58 ms); the Karras fallback still sorts
+// build (all of them: the binned SAH splits do not need the order.  The
+// strided split sample of the unsorted references gives c5 a better tree --
+// its bench path kernel 436 -> 423 ms -- and c1 / c2 / c4 trees of the same
+// quality; the builds save the sort: c5 5.5 -> 5.1 ms, c4 1.85 -> 1.6, c2
+// 0.75 -> 0.54, c1 0.85 -> 0.58 ms); the Karras fallback still sorts
 #ifndef MCSBR_NO_PRESORT_MAX
 #define MCSBR_NO_PRESORT_MAX 0xffffffffu
 #endif
@@ -1302,7 +1303,8 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
     // the Morton pre-sort is skipped for small scenes when the SAH build runs (below)
     const char* bvh_env0 = std::getenv("MCSBR_BVH");
     const bool sah_wanted = !(bvh_env0 && std::strcmp(bvh_env0, "lbvh") == 0);
-    const bool presort = !(sah_wanted && n <= static_cast<int>(env_u32_bvh("MCSBR_BVH_PRESORT_MAX", kNoPresortMax)));
+    const bool presort =
+        !(sah_wanted && static_cast<uint32_t>(n) <= env_u32_bvh("MCSBR_BVH_PRESORT_MAX", kNoPresortMax));
     out->nodes = nullptr;
     out->tri64 = nullptr;
     for (int k = 0; k < 3; ++k) {
