@@ -713,7 +713,7 @@ __device__ __noinline__ void warp_subtree(int first, int count, int root, const 
 constexpr int kCoopSlots = 16;
 constexpr int kCoopMaxChunks = 1024;
 #ifndef MCSBR_SAH_COOP_MIN
-#define MCSBR_SAH_COOP_MIN 65536
+#define MCSBR_SAH_COOP_MIN 16384
 #endif
 constexpr int kCoopMin = MCSBR_SAH_COOP_MIN;
 constexpr int kCoopIdle = 0x3fffffff;  // next1 / next2 of a slot with no open phase
