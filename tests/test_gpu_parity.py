@@ -128,6 +128,37 @@ def test_intersect_equals_brute_force(scene_name, params):
     assert np.array_equal(ids_any != 0xFFFFFFFF, ids_cl != 0xFFFFFFFF)
 
 
+@pytest.mark.parametrize("which", ["sphere_l6", "airframe_200k"])
+def test_intersect_equals_brute_force_large_scenes(which):
+    """The large-scene BVH builds (cooperative top-level partitions of nodes
+    of >= 16 k references, early split clipping of the airframe's slivers,
+    no Morton pre-sort): closest hits and any-hit answers == brute force bit
+    for bit on random rays."""
+    from paper_2511_07586_b200.geometry import airframe
+
+    if which == "sphere_l6":
+        sd = M.make_builtin_scene("sphere", {"subdivisions": 6})  # 81,920 triangles
+        n = 20000
+    else:
+        sd, _ = airframe(200_000, seed=4)
+        n = 4000
+    s = M.Scene(sd)
+    rng = np.random.default_rng(7)
+    o, d = _random_rays(rng, n, max(sd.bounding_radius, 1.0) * 2, sd)
+    t_min = np.zeros(len(o))
+    t, ids = s.intersect_batch(o, d, t_min)
+    ps = oracle.port_scene(sd)
+    hb = oracle.intersect("port", ps, o, d, t_min, 1)
+    assert np.array_equal(ids, hb[:, 12].astype(np.uint32))
+    hit = ids != 0xFFFFFFFF
+    assert hit.sum() > n // 10
+    assert np.array_equal(t[hit], hb[hit, 0])
+    eps = np.full(len(o), sd.self_intersection_epsilon())
+    _, ids_any = s.intersect_batch(o, d, eps, any_hit=True)
+    _, ids_cl = s.intersect_batch(o, d, eps)
+    assert np.array_equal(ids_any != 0xFFFFFFFF, ids_cl != 0xFFFFFFFF)
+
+
 def test_intersect_shared_edge_and_closed_form():
     """tests/test_geometry.cpp:106-118 and :145-151 equivalents on the GPU."""
     s = M.Scene(M.make_builtin_scene("pec_cube"))
