@@ -341,6 +341,11 @@ __global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restri
 }
 
 // sorted leaf boxes: lo_s[k] = lo[order[k]]
+__global__ void iota_kernel(uint32_t* __restrict__ out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<uint32_t>(i);
+}
+
 // centroids of the primitives in the given order (the SAH build's cen array)
 __global__ void centroid_kernel(const float4* __restrict__ lo, const float4* __restrict__ hi,
                                 const uint32_t* __restrict__ order, int n, float4* __restrict__ out) {
@@ -1449,10 +1454,14 @@ cudaError_t build_bvh(const double* d_vertices, const uint4* d_tri_idx, uint32_t
             unsigned int md = 0;
             BVH_CHECK(cudaMemcpyAsync(&md, dmax, sizeof(md), cudaMemcpyDeviceToHost, stream));
             BVH_CHECK(cudaStreamSynchronize(stream));
-            if (3 * ((md + 1) / 2 + 1) > static_cast<unsigned>(kStackSize)) {
+            if (3 * ((md + 1) / 2 + 1) > static_cast<unsigned>(kStackSize) ||
+                env_u32_bvh("MCSBR_BVH_FORCE_FALLBACK", 0) != 0) {  // (the knob exercises this path in tests)
                 sah = false;  // too deep for the traversal stack: Karras tree instead
                 BVH_CHECK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), stream));
                 if (!presort) {  // the Karras tree needs the Morton order
+                    // (the SAH build used `ids` as its partition scratch: restore 0..n-1)
+                    iota_kernel<<<G, B, 0, stream>>>(ids, n);
+                    BVH_CHECK(cudaGetLastError());
                     bool in_alt = false;
                     BVH_CHECK(radix_sort_pairs(keys, keys_s, ids, ids_s, n, 64, tmp, stream, &in_alt));
                     if (!in_alt) {

@@ -128,17 +128,20 @@ def test_intersect_equals_brute_force(scene_name, params):
     assert np.array_equal(ids_any != 0xFFFFFFFF, ids_cl != 0xFFFFFFFF)
 
 
-@pytest.mark.parametrize("which", ["sphere_l6", "airframe_200k"])
-def test_intersect_equals_brute_force_large_scenes(which):
+@pytest.mark.parametrize("which", ["sphere_l6", "airframe_200k", "sphere_l6_karras_fallback"])
+def test_intersect_equals_brute_force_large_scenes(which, monkeypatch):
     """The large-scene BVH builds (cooperative top-level partitions of nodes
     of >= 16 k references, early split clipping of the airframe's slivers,
-    no Morton pre-sort): closest hits and any-hit answers == brute force bit
-    for bit on random rays."""
+    no Morton pre-sort, and the depth fallback to the Karras tree after an
+    SAH build): closest hits and any-hit answers == brute force bit for bit
+    on random rays."""
     from paper_2511_07586_b200.geometry import airframe
 
-    if which == "sphere_l6":
+    if which.startswith("sphere_l6"):
         sd = M.make_builtin_scene("sphere", {"subdivisions": 6})  # 81,920 triangles
         n = 20000
+        if which.endswith("fallback"):  # the SAH build's depth fallback to the Karras tree (sorts late)
+            monkeypatch.setenv("MCSBR_BVH_FORCE_FALLBACK", "1")
     else:
         sd, _ = airframe(200_000, seed=4)
         n = 4000
