@@ -294,32 +294,6 @@ __global__ void refit_kernel(int n, const int2* __restrict__ child, const int* _
     }
 }
 
-__device__ __forceinline__ int child_ref(int c, const int2* __restrict__ range) {
-    if (c < 0) return ~((~c) << 3 | 1);
-    const int2 r = range[c];
-    const int cnt = r.y - r.x + 1;
-    if (cnt <= kLeafMax) return ~(r.x << 3 | cnt);
-    return c;
-}
-
-__global__ void emit_kernel(int n, const int2* __restrict__ child, const int2* __restrict__ range,
-                            const float4* __restrict__ ilo, const float4* __restrict__ ihi,
-                            const float4* __restrict__ llo, const float4* __restrict__ lhi,
-                            float4* __restrict__ nodes) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    const int2 c = child[i];
-    float4 a0, a1, b0, b1;
-    load_box(c.x, ilo, ihi, llo, lhi, a0, a1);
-    load_box(c.y, ilo, ihi, llo, lhi, b0, b1);
-    float4* o = nodes + 4ll * i;
-    o[0] = make_float4(a0.x, a1.x, a0.y, a1.y);
-    o[1] = make_float4(b0.x, b1.x, b0.y, b1.y);
-    o[2] = make_float4(a0.z, a1.z, b0.z, b1.z);
-    o[3] = make_float4(__int_as_float(child_ref(c.x, range)), __int_as_float(child_ref(c.y, range)),
-                       0.f, 0.f);
-}
-
 __global__ void tri_kernel(const double* __restrict__ vtx, const uint4* __restrict__ tri,
                            const uint32_t* __restrict__ order, const uint32_t* __restrict__ ref_tri, uint32_t n,
                            double2* __restrict__ out) {
@@ -939,7 +913,6 @@ __device__ __forceinline__ void sah_split(
     __shared__ float s_cmin[3], s_scale[3];
     __shared__ float s_cost[3];
     __shared__ int s_split[3], s_nl[3];
-    __shared__ int s_warp_l[kSahThreads / 32];
     __shared__ float s_ra[3][kSahBins];  // sweep: suffix areas / counts per axis
     __shared__ int s_rc[3][kSahBins];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

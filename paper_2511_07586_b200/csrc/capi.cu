@@ -252,7 +252,6 @@ struct V {
     double x, y, z;
 };
 inline V operator+(V a, V b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-inline V operator-(V a, V b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 inline V operator*(V a, double s) { return {a.x * s, a.y * s, a.z * s}; }
 inline double dot(V a, V b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 inline V cross(V a, V b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }

@@ -438,7 +438,10 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                             // each the reference's expression operation for operation.
                             const bool ex = sc == 2;
                             const V3 nrm = ex ? -h.normal : h.normal;
-                            const V3 dj = ex ? b.dir_t : s.dir;
+                            V3 dj = s.dir;  // (PEC kernels: sc == 0, and no basis yet)
+                            if constexpr (!kLateBasis) {
+                                if (ex) dj = b.dir_t;
+                            }
                             const NT nj = ex ? h.n_transmit : s.medium_n;
                             // make_contribution (farfield.cpp:70-85)
                             const double cos_n = fabs(dot(s.dir, h.normal));
