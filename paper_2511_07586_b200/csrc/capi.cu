@@ -519,7 +519,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 
 constexpr uint64_t kPathStateBytes = 192;
-constexpr uint64_t kRecCapMax = uint64_t{1} << 27;  // contribution records (96 B each): 12.9 GB
+constexpr uint64_t kRecCapMax = uint64_t{1} << 28;  // contribution records (96 B each): 25.8 GB
 constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: at most 256 MB per job
 
 // Fold the peak record count of the scene's previous F > 1 job (if its
