@@ -111,6 +111,39 @@ def test_exact_shards_are_byte_identical_to_one_launch(world):
     assert vals.reshape(n, 1, 4, nf).tobytes() == full.tobytes()
 
 
+def test_exact_shards_with_empty_ranks():
+    """Incidences smaller than one stripe (1024 dispatch indices): only rank 0
+    has launch units, the other ranks launch nothing for them; the limbs of
+    all ranks still add up to the single launch's bytes."""
+    import torch
+
+    obj, mm = M.dihedral_grid(0.5, 16)
+    sd = M.load_scene(obj, mm)
+    s = M.Scene(sd)
+    excs = [M.monostatic_excitation(90.0, p) for p in (10.0, 45.0)]
+    incs, rxs = [(e, 1.5) for e in excs], [[e] for e in excs]  # a few hundred entries each
+    freqs = np.linspace(9e9, 11e9, 3)
+    cfg = M.McConfig(reduction=EXACT, samples_per_stratum=1, max_bounce=4, seed=4)
+    full, st_full = M.estimate_batch(s, incs, rxs, freqs, cfg)
+    assert 0 < st_full.rays_launched < 2 * 1024
+    n, nf = len(incs), len(freqs)
+    inc = (A.Incidence * n)(*[e.incidence(spw) for e, spw in incs])
+    rx = (A.Receiver * n)(*[r[0].receiver() for r in rxs])
+    c = cfg.to_c()
+    dev = torch.device("cuda", 0)
+    fr = np.ascontiguousarray(freqs, dtype=np.float64)
+    limbs = torch.zeros(n * nf * 8 * A.MCSBR_EXACT_LIMBS, dtype=torch.int64, device=dev)
+    counters = torch.zeros(A.MCSBR_COUNTER_WORDS, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for rank in range(4):
+        A.check(A.lib().mcsbr_gpu_trace_device(
+            s.handle, inc, n, rx, 1, 1, fr.ctypes.data_as(C.POINTER(C.c_double)), nf, C.byref(c), rank, 4,
+            C.c_void_p(limbs.data_ptr()), C.c_void_p(counters.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    vals, st = D.allreduce_finalize(limbs, counters, freqs, n)
+    assert st.rays_launched == st_full.rays_launched and st.contributions == st_full.contributions
+    assert vals.reshape(n, 1, 4, nf).tobytes() == full.tobytes()
+
+
 def test_exact_matches_oracle():
     _, sd, incs, rxs, freqs, kw = CASES[0]
     exc, spw = incs[1]
