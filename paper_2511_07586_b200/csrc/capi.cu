@@ -925,7 +925,9 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
             CK(kt_mark(0, stream, s->device, true), "cudaEventRecord");
             if (defer) {
                 CK(kt_mark(1, stream, s->device, false), "cudaEventRecord");
-                CK(launch_accumulate(p, s->sms, stream, &g_launches), "accumulate launch");
+                CK(launch_accumulate(p, s->sms, stream, &g_launches,
+                                     static_cast<uint64_t>(static_cast<double>(gr.entries) * s->rec_ratio / 1.25)),
+                   "accumulate launch");
                 CK(kt_mark(1, stream, s->device, true), "cudaEventRecord");
             }
         }

@@ -246,8 +246,8 @@ cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stre
 // exact sums (3 words per value) -> 48-bit limbs ADDED into limbs (4 per value)
 cudaError_t launch_exact_limbs(const unsigned long long* xsums, uint64_t n_values, long long* limbs,
                                cudaStream_t stream);
-cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream,
-                              uint64_t* launches);
+cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches,
+                              uint64_t expected_records = 0);
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,
                              const double* tmin, uint32_t n, int any_hit, double* t_out,
                              uint32_t* id_out, cudaStream_t stream);

@@ -785,6 +785,9 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
 // kUniform: the uniform-grid recurrence (P.uniform_f, compile time);
 // kFull: every lane owns all FPL of its frequencies (nf - f_begin >= 32 FPL),
 // so the per-frequency bounds tests drop out of the inner loop.
+#ifndef MCSBR_ACC_MIN_SPAN
+#define MCSBR_ACC_MIN_SPAN 512
+#endif
 template <int FPL, bool kRealAmp, bool kUniform, bool kFull>
 __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t f_begin) {
     // staged record: [0..3] amplitudes, [4] (ph0, dph) | s, [5] (la0, dla),
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
     const uint64_t n = min(n_all, P.rec_cap);
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 4, gw = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
     uint64_t span = ((n + nw - 1) / nw + 31) & ~31ull;
-    span = span < 512 ? 512 : span;
+    span = span < MCSBR_ACC_MIN_SPAN ? MCSBR_ACC_MIN_SPAN : span;
     const uint32_t f_end = min(P.nf, f_begin + 32u * FPL);
     const uint32_t f0 = f_begin + static_cast<uint32_t>(lane);
     const double f0d = static_cast<double>(f0);
@@ -1061,8 +1064,16 @@ cudaError_t launch_exact_limbs(const unsigned long long* xsums, uint64_t n_value
 
 // deferred accumulation of one path-kernel launch's records (F > 1, or any
 // F under MCSBR_REDUCE_EXACT)
-cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
-    const unsigned blocks = static_cast<unsigned>(device_sms) * 4;
+cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches,
+                              uint64_t expected_records) {
+    // One wave of 4 blocks per SM; launches expected to carry more than ~8 k
+    // records per warp of a wave get up to 4 waves (shorter spans balance
+    // the warps' unequal record costs -- real / complex amplitudes -- at the
+    // tail: c5 accumulation -9.7%), small ones stay at one (more warps means
+    // more sum flushes: c4 +7.5% at 4 waves)
+    const uint64_t per_wave = static_cast<uint64_t>(device_sms) * 16 * 8192;
+    const unsigned waves = static_cast<unsigned>(std::min<uint64_t>(4, std::max<uint64_t>(1, expected_records / per_wave)));
+    const unsigned blocks = static_cast<unsigned>(device_sms) * 4 * waves;
     if (p.xsums) {
         for (uint32_t fb = 0; fb < p.nf; fb += 32) {
             accumulate_exact_kernel<<<blocks, 128, 0, stream>>>(p, fb);
