@@ -854,7 +854,10 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     p.gss_div = env_u32("MCSBR_GSS", 16);
     // band height of the launch-entry dispatch order (0 = linear; a power of two)
     {
-        const uint32_t bh = env_u32("MCSBR_BAND", 4);
+        // 8-row bands above 512 k triangles: c5 path kernel -1.6% (its
+        // accumulation +3.8%: the records come out less ordered), 4 below
+        // (c4 +41% at 8)
+        const uint32_t bh = env_u32("MCSBR_BAND", s->nt > kLargeSceneTris ? 8u : 4u);
         p.band_order = static_cast<int32_t>(bh & (bh - 1) ? 4 : bh);
     }
     p.uniform_f = job.uniform_f;
