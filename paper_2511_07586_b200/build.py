@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmcsbr_gpu.so")
-SOURCES = ["capi.cu", "bvh.cu", "trace.cu", "imaging.cu", "cover.cu", "wavefront.cu", "prep.cu", "sort.cu"]
+SOURCES = ["capi.cu", "bvh.cu", "trace.cu", "imaging.cu", "cover.cu", "wavefront.cu", "prep.cu", "sort.cu", "spread.cu"]
 HEADERS = ["dmath.cuh", "rng.cuh", "physics.cuh", "internal.h", "pathcore.cuh", "fixedpoint.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

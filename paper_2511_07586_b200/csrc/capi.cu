@@ -344,6 +344,11 @@ struct mcsbr_scene {
     DevBuf<unsigned long long> counters;
     DevBuf<unsigned long long> tile;
     DevBuf<double> recs;  // deferred-accumulation contribution records
+    DevBuf<double> nufft_grid;  // spread.cu: per-incidence grids of one launch group
+    DevBuf<double> nufft_hat;   // spread.cu: 1 / Psi(m)
+    uint32_t nufft_hat_nf = 0;  // the nf nufft_hat holds
+    DevBuf<uint32_t> nufft_idx;     // spread.cu: record indices by incidence
+    DevBuf<uint32_t> nufft_bucket;  // spread.cu: per-incidence counts / cursors
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
     DevBuf<float4> leaf32;                 // statistical-mode fp32 leaf triangle records (built on first use)
     DevBuf<double> plan_axes;              // launch planning (prep.cu): axes in,
@@ -746,6 +751,46 @@ int run_wavefront(mcsbr_scene* s, const TraceParams& p, const WfParams& w, cudaS
     return set_err(MCSBR_EDEVICE, "wavefront: iteration limit reached");
 }
 
+// MCSBR_RECSTATS (diagnostic): statistics of one launch's contribution
+// records on stderr -- count, real-amplitude and complex-path fractions, and
+// the distribution of the attenuation per frequency step |kdph * Im s| in
+// units of 2 pi / (2 nf) (a sample of every 16th record)
+static void record_stats(mcsbr_scene* s, const TraceParams& p, cudaStream_t stream) {
+    unsigned long long n = 0;
+    cudaMemcpyAsync(&n, p.rec_count, sizeof(n), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    n = std::min<unsigned long long>(n, p.rec_cap);
+    const uint64_t stride = 16, m = n / stride;
+    std::vector<double> v(12 * m);
+    if (m) cudaMemcpy2DAsync(v.data(), 12 * sizeof(double), s->recs.p, stride * 12 * sizeof(double),
+                             12 * sizeof(double), m, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    uint64_t real_amp = 0, cplx_s = 0, hist[8] = {};
+    double smin = 1e300, smax = -1e300;
+    const double h = 2.0 * 3.141592653589793 / (2.0 * p.nf);
+    for (uint64_t i = 0; i < m; ++i) {
+        const double* r = v.data() + 12 * i;
+        if (r[1] == 0 && r[3] == 0 && r[5] == 0 && r[7] == 0) ++real_amp;
+        smin = std::min(smin, r[8]);
+        smax = std::max(smax, r[8]);
+        if (r[9] != 0) {
+            ++cplx_s;
+            const double eta = std::fabs(p.kdph * r[9]) / h;
+            int b = 0;
+            for (double t = 1e-4; b < 7 && eta > t; t *= 4) ++b;
+            ++hist[b];
+        }
+    }
+    std::fprintf(stderr,
+                 "[recstats] records %llu sample %llu real_amp %.4f complex_s %.4f s [%.4g, %.4g] kdph %.4g "
+                 "eta(<1e-4,4e-4,1.6e-3,6.4e-3,.0256,.1024,.41,>) %llu %llu %llu %llu %llu %llu %llu %llu\n",
+                 n, static_cast<unsigned long long>(m), m ? double(real_amp) / m : 0.0,
+                 m ? double(cplx_s) / m : 0.0, smin, smax, p.kdph, (unsigned long long)hist[0],
+                 (unsigned long long)hist[1], (unsigned long long)hist[2], (unsigned long long)hist[3],
+                 (unsigned long long)hist[4], (unsigned long long)hist[5], (unsigned long long)hist[6],
+                 (unsigned long long)hist[7]);
+}
+
 // Upload a planned job and run the path kernel(s) on s->stream, adding into
 // d_sums / d_counters.  One launch per receiver index (receivers of one
 // incidence share nothing but the geometry).
@@ -783,6 +828,42 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // up to kCoverBudget words in total (later incidences go unculled); the
     // deterministic solver's per-root stack accounting needs every root ray,
     // so its jobs are not culled
+    // uniform frequency grids: accumulation as a non-uniform DFT (spread.cu);
+    // MCSBR_ACC=direct keeps the per-frequency phasor kernel (A/B)
+    NufftPlan nq{};
+    const char* acc_env = std::getenv("MCSBR_ACC");
+    const bool acc_direct = acc_env && std::strcmp(acc_env, "direct") == 0;
+    const bool nufft = defer && !exact && job.uniform_f && nufft_supported(nf) && !acc_direct;
+    if (nufft) {
+        nq.ng = 2 * nf;
+        nq.fc = nf / 2;
+        nq.beta = 2.30 * 16;
+        nq.kc = job.kph0 + static_cast<double>(nq.fc) * job.kdph;
+        nq.u2t = job.kdph * static_cast<double>(nq.ng) / (2.0 * M_PI);
+        const char* em = std::getenv("MCSBR_NUFFT_ETA_MAX");  // tests: force the direct fallback
+        nq.eta_max = em ? std::strtod(em, nullptr) : 0.5;
+        const char* ep = std::getenv("MCSBR_NUFFT_ETA_POLY");  // tests: force the exact continuation
+        nq.eta_poly = std::min(nq.eta_max, ep ? std::strtod(ep, nullptr) : 0.1);
+        uint32_t max_inc = 1;
+        for (const Job::Group& gr : job.groups) max_inc = std::max(max_inc, gr.a1 - gr.a0);
+        CK(s->nufft_grid.reserve(nufft_grid_values(nf) * max_inc), "dev_malloc(nufft grids)");
+        if (s->nufft_hat_nf != nf) {  // pageable source: the call returns once it is staged
+            std::vector<double> hat, coef;
+            nufft_tables(nf, nq.ng, nq.beta, hat, coef);
+            hat.insert(hat.end(), coef.begin(), coef.end());
+            CK(s->nufft_hat.reserve(hat.size()), "dev_malloc(nufft weights)");
+            CK(cudaMemcpyAsync(s->nufft_hat.p, hat.data(), sizeof(double) * hat.size(), cudaMemcpyHostToDevice,
+                               stream), "upload nufft weights");
+            s->nufft_hat_nf = nf;
+        }
+        CK(s->nufft_idx.reserve(rec_cap), "dev_malloc(nufft record order)");
+        CK(s->nufft_bucket.reserve(2ull * (max_inc + 1)), "dev_malloc(nufft buckets)");
+        nq.coef = s->nufft_hat.p + nf;
+        nq.idx = env_u32("MCSBR_NUFFT_SORT", 1) ? s->nufft_idx.p : nullptr;
+        nq.bucket = s->nufft_bucket.p;
+        nq.grid = s->nufft_grid.p;
+        nq.inv_hat = s->nufft_hat.p;
+    }
     std::vector<IncDev> incs = job.inc;
     incs.resize(n_units + job.n_inc);
     const bool det_job = extra && extra->det;
@@ -926,11 +1007,14 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
                 CK(launch_trace(p, s->sms, stream, &g_launches), "path kernel launch");
             }
             CK(kt_mark(0, stream, s->device, true), "cudaEventRecord");
+            if (defer && std::getenv("MCSBR_RECSTATS")) record_stats(s, p, stream);
             if (defer) {
                 CK(kt_mark(1, stream, s->device, false), "cudaEventRecord");
-                CK(launch_accumulate(p, s->sms, stream, &g_launches,
-                                     static_cast<uint64_t>(static_cast<double>(gr.entries) * s->rec_ratio / 1.25)),
-                   "accumulate launch");
+                const uint64_t expected = static_cast<uint64_t>(static_cast<double>(gr.entries) * s->rec_ratio / 1.25);
+                if (nufft)
+                    CK(launch_spread(p, nq, gr.a1 - gr.a0, s->sms, stream, &g_launches, expected), "spread launch");
+                else
+                    CK(launch_accumulate(p, s->sms, stream, &g_launches, expected), "accumulate launch");
                 CK(kt_mark(1, stream, s->device, true), "cudaEventRecord");
             }
         }
@@ -1355,6 +1439,10 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->counters.release(true);
     s->tile.release(true);
     s->recs.release(true);
+    s->nufft_grid.release(true);
+    s->nufft_hat.release(true);
+    s->nufft_idx.release(true);
+    s->nufft_bucket.release(true);
     s->cover.release(true);
     s->leaf32.release(true);
     s->plan_axes.release(true);

@@ -22,6 +22,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -251,6 +252,30 @@ cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t
 cudaError_t launch_intersect(const SceneView& s, const double* o, const double* d,
                              const double* tmin, uint32_t n, int any_hit, double* t_out,
                              uint32_t* id_out, cudaStream_t stream);
+// spread.cu: deferred accumulation on uniform frequency grids as a type-1
+// non-uniform DFT (records spread onto a 2F-point grid, then one small DFT
+// per incidence)
+struct NufftPlan {
+    uint32_t ng;             // grid points (2 nf)
+    uint32_t fc;             // centre frequency index (nf / 2)
+    double beta;             // kernel shape
+    double kc;               // kph0 + fc * kdph
+    double u2t;              // kdph * ng / (2 pi): grid cells per unit path length
+    double eta_poly;         // |Im t| up to which the kernel polynomial is continued (0.1 cells)
+    double eta_max;          // |Im t| above which a record is added directly (0.5 cells)
+    double* grid;            // [n_inc][8][ng] (group incidences)
+    const double* inv_hat;   // [nf] 1 / Psi(f - fc)
+    const double* coef;      // [16][kNufftPolyN] psi per window point, monomials in 2 delta - 1
+    uint32_t* idx;           // [rec_cap] record indices ordered by incidence (or nullptr)
+    uint32_t* bucket;        // [2 (n_inc + 1)] per-incidence counts, then cursors
+};
+constexpr int kNufftPolyN = 14;
+constexpr uint32_t kNufftSortMaxInc = 4096;  // larger groups spread in record order
+bool nufft_supported(uint32_t nf);
+size_t nufft_grid_values(uint32_t nf);  // doubles per incidence
+void nufft_tables(uint32_t nf, uint32_t ng, double beta, std::vector<double>& inv_hat, std::vector<double>& coef);
+cudaError_t launch_spread(const TraceParams& p, const NufftPlan& q, uint32_t n_inc, int device_sms,
+                          cudaStream_t stream, uint64_t* launches, uint64_t expected_records);
 // general-F / receiver mode selection helpers
 bool trace_uses_register_accumulator(const TraceParams& p);
 bool trace_fan_supported(uint32_t nf);
