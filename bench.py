@@ -492,9 +492,19 @@ def main():
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     nf = len(W.freqs)
     contribs = int(st.contributions)
-    acc = {"model": "SURVEY.md 8d: C*R*(160+32F) FP32 flops + C*R*F sincos per path (R = 1)",
+    acc_s = (d["acc_ms"] if nf > 1 else path_ms) / 1e3
+    acc = {"model": "SURVEY.md 8d: C*R*(160+32F) FP32 flops + C*R*F sincos per path (R = 1), the direct "
+                    "per-frequency evaluation; on a uniform grid the library runs a type-1 NUFFT instead "
+                    "(csrc/spread.cu: ~40 warp instructions per record, independent of F), so these are "
+                    "direct-equivalent rates",
            "contributions_per_path": contribs / max(paths, 1),
-           "kernel": "accumulate_kernel" if nf > 1 else "path_kernel (register sums)",
+           "kernel": ("bucket_count + bucket_scatter + spread_kernel + nufft_finish (csrc/spread.cu)"
+                      if nf > 1 else "path_kernel (register sums)"),
+           "records_per_s": contribs / acc_s,
+           "hbm_bytes_per_record": 168,
+           "hbm_bytes_note": "96 B record (spread) + 2 x 32 B sector (the two bucket passes read the incidence "
+                             "word) + 4 B index written + 4 B read",
+           "hbm_GBps": contribs * 168 / acc_s / 1e9,
            "kernel_ms_per_step": d["acc_ms"] if nf > 1 else path_ms,
            "fp32_tflops": contribs * (160 + 32 * nf) / ((d["acc_ms"] if nf > 1 else path_ms) / 1e3) / 1e12,
            "fp32_peak_tflops": sm_count * 128 * 2 * f_mhz * 1e6 / 1e12,
@@ -562,7 +572,7 @@ def main():
             "sweep_wall_ms": d["ms"],
             "step_ms": [round(x, 3) for x in d["step_ms"]],
             "kernels_ms_per_step": {"path_kernel": path_ms, "path_launches": d["path_launches"],
-                                    "accumulate_kernel": d["acc_ms"], "accumulate_launches": d["acc_launches"]},
+                                    "accumulation": d["acc_ms"], "accumulate_launches": d["acc_launches"]},
             "rcs_vs_cpu_ref": rcs,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

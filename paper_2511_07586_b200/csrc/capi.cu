@@ -348,6 +348,7 @@ struct mcsbr_scene {
     DevBuf<double> nufft_hat;   // spread.cu: 1 / Psi(m)
     uint32_t nufft_hat_nf = 0;  // the nf nufft_hat holds
     DevBuf<uint32_t> nufft_idx;     // spread.cu: record indices by incidence
+    DevBuf<uint32_t> nufft_inc;     // spread.cu: each record's incidence (written by the path kernel)
     DevBuf<uint32_t> nufft_bucket;  // spread.cu: per-incidence counts / cursors
     DevBuf<uint32_t> cover;  // launch-ray coverage bitmaps of the current job
     DevBuf<float4> leaf32;                 // statistical-mode fp32 leaf triangle records (built on first use)
@@ -860,6 +861,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         CK(s->nufft_bucket.reserve(2ull * (max_inc + 1)), "dev_malloc(nufft buckets)");
         nq.coef = s->nufft_hat.p + nf;
         nq.idx = env_u32("MCSBR_NUFFT_SORT", 1) ? s->nufft_idx.p : nullptr;
+        if (nq.idx) CK(s->nufft_inc.reserve(rec_cap), "dev_malloc(record incidences)");
         nq.bucket = s->nufft_bucket.p;
         nq.grid = s->nufft_grid.p;
         nq.inv_hat = s->nufft_hat.p;
@@ -919,6 +921,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     p.recs = defer ? s->recs.p : nullptr;
     p.rec_count = s->tile.p + 1;
     p.rec_cap = rec_cap;
+    p.rec_inc = nufft && nq.idx ? s->nufft_inc.p : nullptr;
     // scheduling knobs (A/B experiments only; the defaults are the product)
     // Chunk cap: large scenes keep every SM's warps inside a narrow window of
     // the aperture (their BVH working set outgrows L1/L2: c4 -35% going from
@@ -1442,6 +1445,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     s->nufft_grid.release(true);
     s->nufft_hat.release(true);
     s->nufft_idx.release(true);
+    s->nufft_inc.release(true);
     s->nufft_bucket.release(true);
     s->cover.release(true);
     s->leaf32.release(true);

@@ -115,6 +115,7 @@ struct TraceParams {
     double* recs;                      // [rec_cap][12]: amp[4], s (re, im), incidence
     unsigned long long* rec_count;
     uint64_t rec_cap;
+    uint32_t* rec_inc;                 // [rec_cap] each record's incidence again, packed (spread.cu buckets), or nullptr
     unsigned long long* counters;
     unsigned long long* tile_counter;  // global cursor over the flattened entry space
     uint64_t total_entries;            // entries of all incidences (this shard)

@@ -267,11 +267,15 @@ __global__ void __launch_bounds__(256) bucket_count_kernel(TraceParams P, NufftP
     for (uint32_t i = threadIdx.x; i < n_inc; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint64_t n = min(static_cast<uint64_t>(*P.rec_count), P.rec_cap);
-    const double2* recs = reinterpret_cast<const double2*>(P.recs);
-    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t a = static_cast<uint32_t>(__double_as_longlong(recs[r * (kRecWords / 2) + 5].x));
-        atomicAdd(&hist[a], 1u);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); r0 < n;
+         r0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {  // warp-uniform trip count
+        const uint64_t r = r0 + lane;
+        const uint32_t a = r < n ? P.rec_inc[r] : 0xffffffffu;
+        // warp-aggregated: consecutive records are mostly one incidence
+        const unsigned same = __match_any_sync(0xffffffffu, a);
+        if (a != 0xffffffffu && lane == static_cast<uint32_t>(__ffs(same) - 1))
+            atomicAdd(&hist[a], static_cast<uint32_t>(__popc(same)));
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n_inc; i += blockDim.x)
@@ -308,7 +312,6 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(TraceParams P, Nuff
     uint32_t* base = hist + n_inc;
     constexpr uint32_t kTile = 4096;
     const uint64_t n = min(static_cast<uint64_t>(*P.rec_count), P.rec_cap);
-    const double2* recs = reinterpret_cast<const double2*>(P.recs);
     uint32_t* cursor = Q.bucket + n_inc + 1;
     for (uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kTile; t0 < n; t0 += static_cast<uint64_t>(gridDim.x) * kTile) {
         for (uint32_t i = threadIdx.x; i < n_inc; i += blockDim.x) hist[i] = 0;
@@ -317,8 +320,10 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(TraceParams P, Nuff
 #pragma unroll
         for (int k = 0; k < static_cast<int>(kTile / 256); ++k) {
             const uint64_t r = t0 + k * 256 + threadIdx.x;
-            av[k] = r < n ? static_cast<uint32_t>(__double_as_longlong(recs[r * (kRecWords / 2) + 5].x)) : 0xffffffffu;
-            if (av[k] != 0xffffffffu) atomicAdd(&hist[av[k]], 1u);
+            av[k] = r < n ? P.rec_inc[r] : 0xffffffffu;
+            const unsigned same = __match_any_sync(0xffffffffu, av[k]);
+            if (av[k] != 0xffffffffu && (threadIdx.x & 31) == __ffs(same) - 1)
+                atomicAdd(&hist[av[k]], static_cast<uint32_t>(__popc(same)));
         }
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n_inc; i += blockDim.x) {
@@ -326,10 +331,16 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(TraceParams P, Nuff
             hist[i] = 0;
         }
         __syncthreads();
+        const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int k = 0; k < static_cast<int>(kTile / 256); ++k) {
+            const unsigned same = __match_any_sync(0xffffffffu, av[k]);
+            const int leader = __ffs(same) - 1;
+            uint32_t off = 0;
+            if (av[k] != 0xffffffffu && lane == leader) off = atomicAdd(&hist[av[k]], static_cast<uint32_t>(__popc(same)));
+            off = __shfl_sync(0xffffffffu, off, leader);
             if (av[k] == 0xffffffffu) continue;
-            const uint32_t pos = base[av[k]] + atomicAdd(&hist[av[k]], 1u);
+            const uint32_t pos = base[av[k]] + off + __popc(same & ((1u << lane) - 1u));
             Q.idx[pos] = static_cast<uint32_t>(t0 + k * 256 + threadIdx.x);
         }
         __syncthreads();
@@ -433,7 +444,7 @@ cudaError_t launch_spread(const TraceParams& p, const NufftPlan& q, uint32_t n_i
     cudaError_t e = cudaMemsetAsync(q.grid, 0, sizeof(double) * 8 * q.ng * n_inc, stream);
     if (e != cudaSuccess) return e;
     NufftPlan qs = q;
-    if (q.idx && n_inc > 1 && n_inc <= kNufftSortMaxInc) {
+    if (q.idx && p.rec_inc && n_inc > 1 && n_inc <= kNufftSortMaxInc) {
         if ((e = cudaMemsetAsync(q.bucket, 0, sizeof(uint32_t) * 2 * (n_inc + 1), stream)) != cudaSuccess) return e;
         bucket_count_kernel<<<device_sms * 4, 256, sizeof(uint32_t) * n_inc, stream>>>(p, q, n_inc);
         bucket_prefix_kernel<<<1, 1024, 0, stream>>>(q, n_inc);

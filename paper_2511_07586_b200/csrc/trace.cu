@@ -683,6 +683,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                         for (int ch = 0; ch < 4; ++ch) r[ch] = make_double2(amp[ch].re, amp[ch].im);
                         r[4] = make_double2(re_of(s_path), im_of(s_path));
                         r[5] = make_double2(__longlong_as_double(static_cast<long long>(a)), 0.0);
+                        if (P.rec_inc) P.rec_inc[slot] = a;
                     }
                     // buffer full (the host sizes it so this is rare): the warp
                     // adds each overflowing contribution straight into the sums,

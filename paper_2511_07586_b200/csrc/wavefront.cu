@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(128, MCSBR_WF_SHADE_BLOCKS) wf_shade(TracePara
                 for (int ch = 0; ch < 4; ++ch) r[ch] = make_double2(amp[ch].re, amp[ch].im);
                 r[4] = make_double2(re_of(s_path), im_of(s_path));
                 r[5] = make_double2(__longlong_as_double(static_cast<long long>(rec_inc)), 0.0);
+                if (P.rec_inc) P.rec_inc[slot] = rec_inc;
             }
             // record buffer full: add the contribution straight into the sums
             unsigned om = __ballot_sync(kFull, visible && !stored);
