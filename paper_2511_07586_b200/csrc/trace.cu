@@ -679,11 +679,20 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                     const bool stored = visible && slot < P.rec_cap;
                     if (stored) {
                         double2* r = reinterpret_cast<double2*>(P.recs) + slot * kRecD2;
+#ifdef MCSBR_REC_PLAIN
+#define MCSBR_REC_ST(p, v) (*(p) = (v))
+#else
+                        // streaming stores (evict-first): the records are read once,
+                        // by the accumulation, and should not displace the BVH and
+                        // the local-memory lines from L2
+#define MCSBR_REC_ST(p, v) __stcs((p), (v))
+#endif
 #pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) r[ch] = make_double2(amp[ch].re, amp[ch].im);
-                        r[4] = make_double2(re_of(s_path), im_of(s_path));
-                        r[5] = make_double2(__longlong_as_double(static_cast<long long>(a)), 0.0);
-                        if (P.rec_inc) P.rec_inc[slot] = a;
+                        for (int ch = 0; ch < 4; ++ch) MCSBR_REC_ST(r + ch, make_double2(amp[ch].re, amp[ch].im));
+                        MCSBR_REC_ST(r + 4, make_double2(re_of(s_path), im_of(s_path)));
+                        MCSBR_REC_ST(r + 5, make_double2(__longlong_as_double(static_cast<long long>(a)), 0.0));
+                        if (P.rec_inc) MCSBR_REC_ST(P.rec_inc + slot, a);
+#undef MCSBR_REC_ST
                     }
                     // buffer full (the host sizes it so this is rare): the warp
                     // adds each overflowing contribution straight into the sums,
