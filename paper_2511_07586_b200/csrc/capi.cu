@@ -669,7 +669,9 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     uint64_t group_cap = ~uint64_t{0};
     if (nf > 1) {
         learn_rec_ratio(const_cast<mcsbr_scene*>(s));
-        group_cap = std::max<uint64_t>(static_cast<uint64_t>(static_cast<double>(kRecCapMax) / s->rec_ratio),
+        // (a multi-frequency fan appends up to one record per receiver of its chunk)
+        const double fan_mult = n_rx > 1 ? static_cast<double>(std::min<uint32_t>(n_rx, 32)) : 1.0;
+        group_cap = std::max<uint64_t>(static_cast<uint64_t>(static_cast<double>(kRecCapMax) / (s->rec_ratio * fan_mult)),
                                        uint64_t{1} << 20);
         group_cap = env_u32("MCSBR_GROUP_ENTRIES", static_cast<uint32_t>(std::min<uint64_t>(group_cap, 0xffffffffu)));
     }
@@ -818,9 +820,31 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // contribution; sized for one per launched path of the largest group
     // (measured c4/c5: ~0.1 per path), overflow falls back to direct atomics
     const bool defer = nf > 1 || exact;
+    // Bistatic fans (several receivers per incidence): trace once per chunk
+    // of 32 receivers, lane l evaluating receiver l's occlusion and
+    // projection.  F = 1 sums in the lanes' registers; F > 1 appends one
+    // record per visible (contribution, receiver), in row 32 a + l of the
+    // accumulation (fan_rows).  The exact reduction traces receivers one by
+    // one.
+    // F > 1 fans need the NUFFT's row buckets: its spread (and the direct
+    // kernel) flush their sums whenever consecutive records change row, and
+    // a fan's consecutive records are different receivers
+    const char* acc_env = std::getenv("MCSBR_ACC");
+    const bool acc_direct = acc_env && std::strcmp(acc_env, "direct") == 0;
+    uint32_t max_group_inc = 1;
+    for (const Job::Group& gr : job.groups) max_group_inc = std::max(max_group_inc, gr.a1 - gr.a0);
+    const bool rows_bucketed = !exact && job.uniform_f && nufft_supported(nf) && !acc_direct &&
+                               env_u32("MCSBR_NUFFT_SORT", 1) != 0 && max_group_inc * 32u <= kNufftSortMaxInc;
+    const bool fan = job.n_rx > 1 && trace_fan_supported(nf) && !exact && !(extra && extra->det) &&
+                     (nf == 1 || rows_bucketed) &&
+                     env_u32("MCSBR_FAN", 1) != 0;  // (A/B: MCSBR_FAN=0 traces per receiver)
+    const uint32_t fan_rows = fan && nf > 1 ? 32u : 0u;
+    const uint32_t rows_per_inc = fan_rows ? fan_rows : 1u;  // accumulation rows per incidence
     uint64_t rec_cap = 0;
     if (defer) {
-        rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1) + 4096;
+        rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1 *
+                                        (fan_rows ? std::min<uint32_t>(job.n_rx, fan_rows) : 1u)) +
+                  4096;
         rec_cap = std::min<uint64_t>(rec_cap, kRecCapMax);
         rec_cap = env_u32("MCSBR_REC_CAP", static_cast<uint32_t>(rec_cap));
         CK(s->recs.reserve(rec_cap * 12), "dev_malloc(contribution records)");
@@ -832,8 +856,6 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // uniform frequency grids: accumulation as a non-uniform DFT (spread.cu);
     // MCSBR_ACC=direct keeps the per-frequency phasor kernel (A/B)
     NufftPlan nq{};
-    const char* acc_env = std::getenv("MCSBR_ACC");
-    const bool acc_direct = acc_env && std::strcmp(acc_env, "direct") == 0;
     const bool nufft = defer && !exact && job.uniform_f && nufft_supported(nf) && !acc_direct;
     if (nufft) {
         nq.ng = 2 * nf;
@@ -846,7 +868,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         const char* ep = std::getenv("MCSBR_NUFFT_ETA_POLY");  // tests: force the exact continuation
         nq.eta_poly = std::min(nq.eta_max, ep ? std::strtod(ep, nullptr) : 0.1);
         uint32_t max_inc = 1;
-        for (const Job::Group& gr : job.groups) max_inc = std::max(max_inc, gr.a1 - gr.a0);
+        for (const Job::Group& gr : job.groups) max_inc = std::max(max_inc, (gr.a1 - gr.a0) * rows_per_inc);
         CK(s->nufft_grid.reserve(nufft_grid_values(nf) * max_inc), "dev_malloc(nufft grids)");
         if (s->nufft_hat_nf != nf) {  // pageable source: the call returns once it is staged
             std::vector<double> hat, coef;
@@ -870,7 +892,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     incs.resize(n_units + job.n_inc);
     const bool det_job = extra && extra->det;
     // only the deferred-accumulation kernels cull (trace.cu kCull)
-    const bool cull = !det_job && (nf > 1 || exact) && env_u32("MCSBR_COVER", 1) != 0;
+    const bool cull = !det_job && (nf > 1 || exact) && !fan && env_u32("MCSBR_COVER", 1) != 0;
     uint64_t cover_words = 0;
     uint32_t n_cover = 0;  // incidences with a bitmap (the coverage kernel's blocks)
     for (uint32_t a = 0; a < job.n_inc; ++a) {
@@ -953,13 +975,10 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         CK(cudaEventCreate(&s->ev1), "cudaEventCreate");
     }
     if (kernel_ms) CK(cudaEventRecord(s->ev0, stream), "cudaEventRecord");
-    // Bistatic fans (several receivers per incidence, one frequency): trace
-    // once per chunk of 32 receivers (fan mode).  Otherwise one launch per
-    // receiver index (multi-frequency bistatic sweeps re-trace per receiver,
-    // as the reference does).
-    const bool fan = job.n_rx > 1 && trace_fan_supported(nf) && !exact;
+    // fans: one launch per chunk of 32 receivers; otherwise one per receiver
     const uint32_t step = fan ? 32u : 1u;
     p.fan = fan ? 1 : 0;
+    p.fan_rows = fan_rows;
     if (defer) CK(cudaMemsetAsync(s->tile.p + 2, 0, sizeof(unsigned long long), stream), "reset peak");
     if (cover_words) {
         CK(launch_cover(s->inc.p + n_units, n_cover, s->d_tri32, s->nt, s->center, s->radius,
@@ -1015,7 +1034,8 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
                 CK(kt_mark(1, stream, s->device, false), "cudaEventRecord");
                 const uint64_t expected = static_cast<uint64_t>(static_cast<double>(gr.entries) * s->rec_ratio / 1.25);
                 if (nufft)
-                    CK(launch_spread(p, nq, gr.a1 - gr.a0, s->sms, stream, &g_launches, expected), "spread launch");
+                    CK(launch_spread(p, nq, (gr.a1 - gr.a0) * rows_per_inc, s->sms, stream, &g_launches, expected),
+                       "spread launch");
                 else
                     CK(launch_accumulate(p, s->sms, stream, &g_launches, expected), "accumulate launch");
                 CK(kt_mark(1, stream, s->device, true), "cudaEventRecord");
@@ -1026,11 +1046,11 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         CK(launch_exact_limbs(s->xsums.p, n_values, d_limbs, stream), "exact limbs launch");
         ++g_launches;
     }
-    if (defer && s->peak_host) {  // learn the record ratio for the next job
+    if (defer && s->peak_host) {  // learn the record ratio (per entry and receiver row) for the next job
         CK(cudaMemcpyAsync(s->peak_host, s->tile.p + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            stream), "peak record count");
         CK(cudaEventRecord(s->peak_ev, stream), "cudaEventRecord");
-        s->peak_entries = job.max_group_entries;
+        s->peak_entries = job.max_group_entries * (fan_rows ? std::min<uint32_t>(job.n_rx, fan_rows) : 1u);
         s->peak_pending = true;
     }
     if (kernel_ms) {

@@ -103,7 +103,9 @@ struct TraceParams {
     uint32_t inc_base;      // job index of the launch's first incidence (RNG keys, path log)
     uint32_t n_rx;          // receivers per incidence
     uint32_t rx_index;      // receiver traced by this launch (fan: the first of up to 32)
-    int fan;                // bistatic fan mode (nf == 1)
+    int fan;                // bistatic fan mode (up to 32 receivers per launch)
+    uint32_t fan_rows;      // fan with nf > 1 (deferred records): 32, and a record's row is
+                            // 32 * incidence + receiver lane (sums_row); else 0
     const RxDev* rx;        // [n_inc * n_rx]
     const double* k0;       // [nf] wavenumbers 2*pi*f/c
     uint32_t nf;
@@ -159,6 +161,17 @@ struct TraceParams {
     unsigned long long* det_blocks;          // [n_blocks][2]: sum peak depth, sum pushes
     uint64_t det_block_size;                 // cells per accounting block
 };
+
+// Row of the [incidence][receiver] sums that a contribution record's row
+// index `a` adds into: an incidence of this launch (receiver rx_index), or,
+// in a multi-frequency bistatic fan (fan_rows = 32), receiver rx_index + a % 32
+// of incidence a / 32.
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__ size_t sums_row(const TraceParams& P, uint32_t a) {
+    return P.fan_rows ? static_cast<size_t>(a >> 5) * P.n_rx + P.rx_index + (a & 31u)
+                      : static_cast<size_t>(a) * P.n_rx + P.rx_index;
+}
+#endif
 constexpr int kDetFields = 24;  // origin 3, dir 3, e0 6, e1 6, phi 2, medium 2, bounce 1 (+1 spare)
 // branch stacks are sized for 4 resident 128-thread blocks per SM (the path
 // kernel's launch bound); launch_trace caps a det grid at the stack capacity

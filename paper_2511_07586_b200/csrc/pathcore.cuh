@@ -878,6 +878,23 @@ __device__ __forceinline__ Cx freq_phasor(const TraceParams& P, uint32_t f, NT s
 
 constexpr int kRecD2 = 6;  // contribution record: 6 double2 = 96 B (amp[4], s, incidence)
 
+// Append contribution record `slot`: the four projected amplitudes, the net
+// optical path and its row (an incidence of the launch, or a fan row, see
+// sums_row), plus the row again in the packed array the NUFFT buckets read.
+// Streaming stores (evict-first): the records are read once, by the
+// accumulation, and should not displace the BVH and the local-memory lines
+// from L2 (c5 -0.8% against plain stores).
+template <typename NT>
+__device__ __forceinline__ void write_record(const TraceParams& P, uint64_t slot, const Cx (&amp)[4], NT s,
+                                             uint32_t row) {
+    double2* r = reinterpret_cast<double2*>(P.recs) + slot * kRecD2;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) __stcs(r + ch, make_double2(amp[ch].re, amp[ch].im));
+    __stcs(r + 4, make_double2(re_of(s), im_of(s)));
+    __stcs(r + 5, make_double2(__longlong_as_double(static_cast<long long>(row)), 0.0));
+    if (P.rec_inc) __stcs(P.rec_inc + slot, row);
+}
+
 // Record-buffer overflow: one term added straight into the sums -- an fp64
 // atomic, or under MCSBR_REDUCE_EXACT the term rounded once to 192-bit fixed
 // point (fixedpoint.cuh) and added with carries into P.xsums (the same value
@@ -892,5 +909,22 @@ __device__ __forceinline__ void add_value(const TraceParams& P, double* out, uin
     if (!mcsbr_fx::fx_from_double(v, w))
         atomicOr(P.counters + kCntFault, static_cast<unsigned long long>(kFaultFixedRange));
     mcsbr_fx::fx_atomic_add(P.xsums + ((out - P.sums) + k) * 3, w);
+}
+
+// Fan record that did not fit the buffer (the host sizes it so this is
+// rare): the lane adds it straight into its receiver's sums, every
+// frequency.
+template <typename NT>
+__device__ __forceinline__ void fan_record_overflow(const TraceParams& P, uint32_t row, const Cx (&am)[4], NT sp) {
+    double* out = P.sums + sums_row(P, row) * P.nf * 8;
+    for (uint32_t f = 0; f < P.nf; ++f) {
+        const Cx z = freq_phasor(P, f, sp);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            const Cx v = am[ch] * z;
+            add_value(P, out, f * 8 + 2 * ch, v.re);
+            add_value(P, out, f * 8 + 2 * ch + 1, v.im);
+        }
+    }
 }
 

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(64) spread_kernel(TraceParams P, NufftPlan Q) 
                 } else {
                     // strongly attenuated path: direct phasors, lanes over
                     // frequencies, straight into the sums (rare)
-                    double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
+                    double* out = P.sums + sums_row(P, a) * P.nf * 8;
                     const double hstep = 2.0 * M_PI / dng;
                     for (uint32_t f = lane; f < P.nf; f += 32) {
                         const double m = static_cast<double>(static_cast<int>(f) - static_cast<int>(Q.fc)) * hstep;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256) nufft_finish_kernel(TraceParams P, NufftP
     for (uint32_t i = threadIdx.x; i < 8 * ng; i += blockDim.x) G[i] = src[i];
     for (uint32_t i = threadIdx.x; i < ng; i += blockDim.x) sincospi(2.0 * i / ng, &sn[i], &cs[i]);
     __syncthreads();
-    double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
+    double* out = P.sums + sums_row(P, a) * P.nf * 8;
     for (uint32_t o = threadIdx.x; o < P.nf * 4; o += blockDim.x) {
         const uint32_t f = o >> 2, k = o & 3;
         const int m = static_cast<int>(f) - static_cast<int>(Q.fc);

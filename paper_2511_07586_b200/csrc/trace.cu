@@ -57,13 +57,16 @@ namespace {
 //              the path kernel's shared memory -- and so its L1 -- free of
 //              per-warp [F][4] arrays).
 //   kModeReg   one receiver, F = 1: per-lane register sums, warp-reduced per tile
+//   kModeFanRec the same fan with F > 1: lane l appends one record per visible
+//              (contribution, receiver l) in row 32 a + l (sums_row), which
+//              the accumulation kernels (NUFFT or direct) then sum
 //   kModeFan   a bistatic fan of up to 32 receivers per launch (P.rx_index is
 //              the first), F = 1: lane l owns receiver rx_index + l; every
 //              contribution is broadcast across the warp and each lane runs
 //              its receiver's occlusion test and projection (a coherent
 //              32-ray bundle from one exit point), so paths are traced once
 //              per 32 receivers instead of once per receiver.
-enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2 };
+enum { kModeDefer = 0, kModeReg = 1, kModeFan = 2, kModeFanRec = 3 };
 
 #ifndef MCSBR_MIN_BLOCKS
 #define MCSBR_MIN_BLOCKS 4  // 128 registers: 16 warps/SM (measured best of 1/2/3/4/6)
@@ -95,6 +98,8 @@ struct MinBlocks {
 template <int kMode, bool kDiel, bool kLossy, bool kDet, bool kFast>
 __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value)) path_kernel(TraceParams P) {
     constexpr bool kRegAcc = kMode != kModeDefer;
+    constexpr bool kFanM = kMode == kModeFan || kMode == kModeFanRec;  // any bistatic fan
+    constexpr bool kFanRec = kMode == kModeFanRec;  // fan with F > 1: deferred records (fan_rows)
     // launch-ray culling by the coverage bitmaps (cover.cu): the deferred-
     // accumulation Monte Carlo kernels (large ISAR scenes); run_job builds
     // bitmaps only for those
@@ -191,8 +196,8 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
     }
     // add the warp's accumulators into incidence cur_a's sums and clear them
     auto flush = [&]() {
-        if (kRegAcc && cur_a != 0xffffffffu)
-            flush_sums<kMode == kModeFan, kFAcc>(P.sums, P.n_rx, P.rx_index, sl.p, cur_a, lane);
+        if (kRegAcc && !kFanRec && cur_a != 0xffffffffu)
+            flush_sums<kFanM, kFAcc>(P.sums, P.n_rx, P.rx_index, sl.p, cur_a, lane);
     };
 
     for (;;) {
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
             cur_a = a;
         }
         // fan mode: lane l evaluates receiver rx_index + l (if it exists)
-        const uint32_t my_rx = P.rx_index + (kMode == kModeFan ? static_cast<uint32_t>(lane) : 0u);
+        const uint32_t my_rx = P.rx_index + (kFanM ? static_cast<uint32_t>(lane) : 0u);
         const bool has_rx = my_rx < P.n_rx;
         const RxDev& R = P.rx[static_cast<size_t>(a) * P.n_rx + (has_rx ? my_rx : P.rx_index)];
 
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                                 m = m * scale;
                             };
                             EF j0, m0, j1, m1;
-                            if constexpr (kMode == kModeFan) {
+                            if constexpr (kFanM) {
                                 currents(s.e0, 0, j0, m0);
                                 currents(s.e1, 1, j1, m1);
                                 fj0 = j0;
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                                 s_path = s.phi - dot(ld3(R.k_s), point);
                             }
                             if (scratch) {
-                                if constexpr (kMode == kModeFan) {
+                                if constexpr (kFanM) {
                                     store_cv(&scratch->a_j[0][0][0], j0);
                                     store_cv(&scratch->a_m[0][0][0], m0);
                                 }
@@ -605,7 +610,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                     save_em<L>(sl, s);
                 }
                 // ---- chi visibility (farfield.cpp:63-68): queue the occlusion query ----
-                if (candidate && kMode == kModeFan) {
+                if (candidate && kFanM) {
                     fan = true;  // evaluated below by the whole warp
                 } else if (candidate) {
                     if (P.occlusion) {
@@ -632,7 +637,7 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                 }
             }
             // ---- bistatic fan: every contribution against this launch's receivers ----
-            if (kMode == kModeFan) {
+            if (kFanM) {
                 unsigned fm = __ballot_sync(kFull, fan);
                 const V3 ks = ld3(R.k_s);
                 while (fm) {
@@ -658,7 +663,23 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                         }
                         if (vis) {
                             ++n_contrib;
-                            acc_add<kFAcc>(sl, am, phasor(P.k0[0], sp));
+                            if constexpr (kFanRec) {
+                                // multi-frequency fan: one deferred record per
+                                // visible (contribution, receiver), row 32 a + lane
+                                // (sums_row); one atomic per group of lanes here
+                                const unsigned m = __activemask();
+                                const int leader = __ffs(m) - 1;
+                                unsigned long long base = 0;
+                                if (lane == leader)
+                                    base = atomicAdd(P.rec_count, static_cast<unsigned long long>(__popc(m)));
+                                base = __shfl_sync(m, base, leader);
+                                const uint64_t slot = base + __popc(m & ((1u << lane) - 1u));
+                                const uint32_t row = a * 32u + static_cast<uint32_t>(lane);
+                                if (slot < P.rec_cap) write_record(P, slot, am, sp, row);
+                                else fan_record_overflow(P, row, am, sp);
+                            } else {
+                                acc_add<kFAcc>(sl, am, phasor(P.k0[0], sp));
+                            }
                         }
                     }
                 }
@@ -677,28 +698,12 @@ __global__ void __launch_bounds__(128, (MinBlocks<kMode, kDiel, kLossy>::value))
                     base = __shfl_sync(kFull, base, 0);
                     const uint64_t slot = base + __popc(vm & ((1u << lane) - 1u));
                     const bool stored = visible && slot < P.rec_cap;
-                    if (stored) {
-                        double2* r = reinterpret_cast<double2*>(P.recs) + slot * kRecD2;
-#ifdef MCSBR_REC_PLAIN
-#define MCSBR_REC_ST(p, v) (*(p) = (v))
-#else
-                        // streaming stores (evict-first): the records are read once,
-                        // by the accumulation, and should not displace the BVH and
-                        // the local-memory lines from L2
-#define MCSBR_REC_ST(p, v) __stcs((p), (v))
-#endif
-#pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) MCSBR_REC_ST(r + ch, make_double2(amp[ch].re, amp[ch].im));
-                        MCSBR_REC_ST(r + 4, make_double2(re_of(s_path), im_of(s_path)));
-                        MCSBR_REC_ST(r + 5, make_double2(__longlong_as_double(static_cast<long long>(a)), 0.0));
-                        if (P.rec_inc) MCSBR_REC_ST(P.rec_inc + slot, a);
-#undef MCSBR_REC_ST
-                    }
+                    if (stored) write_record(P, slot, amp, s_path, a);
                     // buffer full (the host sizes it so this is rare): the warp
                     // adds each overflowing contribution straight into the sums,
                     // lanes over frequencies
                     unsigned om = __ballot_sync(kFull, visible && !stored);
-                    double* out = P.sums + (static_cast<size_t>(a) * P.n_rx + P.rx_index) * P.nf * 8;
+                    double* out = P.sums + sums_row(P, a) * P.nf * 8;
                     while (om) {
                         const int src = __ffs(om) - 1;
                         om &= om - 1;
@@ -836,7 +841,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(TraceParams P, uint32_t
             for (int k = 0; k < 8; ++k) acc[m][k] = 0.0;
         auto flush = [&]() {
             if (cur == 0xffffffffu) return;
-            double* out = P.sums + (static_cast<size_t>(cur) * P.n_rx + P.rx_index) * P.nf * 8;
+            double* out = P.sums + sums_row(P, cur) * P.nf * 8;
 #pragma unroll
             for (int m = 0; m < FPL; ++m) {
                 const uint32_t f = f0 + 32u * m;
@@ -953,7 +958,7 @@ __global__ void __launch_bounds__(128) accumulate_exact_kernel(TraceParams P, ui
         for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0;
         auto flush = [&]() {
             if (cur == 0xffffffffu || !has_f) return;
-            unsigned long long* g = P.xsums + ((static_cast<size_t>(cur) * P.n_rx + P.rx_index) * P.nf + f) * 8 * 3;
+            unsigned long long* g = P.xsums + (sums_row(P, cur) * P.nf + f) * 8 * 3;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 mcsbr_fx::fx_atomic_add(g + 3 * k, acc[k]);
@@ -1026,7 +1031,7 @@ __global__ void intersect_kernel(SceneView S, const double* __restrict__ o, cons
 
 bool trace_uses_register_accumulator(const TraceParams& p) { return p.nf == 1 && !p.xsums; }
 
-bool trace_fan_supported(uint32_t nf) { return nf == 1; }
+bool trace_fan_supported(uint32_t) { return true; }  // F = 1 register sums, F > 1 fan records
 
 template <int kMode, bool kDiel, bool kLossy, bool kDet, bool kFast>
 static cudaError_t launch_mode(const TraceParams& p, int device_sms, int threads, size_t smem,
@@ -1056,6 +1061,8 @@ static cudaError_t launch_kind(int mode, const TraceParams& p, int sms, int thre
     if (p.det)  // one receiver per launch (the deterministic solver has no fan mode)
         return mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, true, false>(p, sms, threads, smem, stream)
                                 : launch_mode<kModeDefer, kDiel, kLossy, true, false>(p, sms, threads, smem, stream);
+    if (mode == kModeFanRec)  // multi-frequency fans: fp64 triangle tests in every mode
+        return launch_mode<kModeFanRec, kDiel, kLossy, false, false>(p, sms, threads, smem, stream);
     if (p.fast_tri)  // statistical-mode fp32 triangle tests
         return mode == kModeFan   ? launch_mode<kModeFan, kDiel, kLossy, false, true>(p, sms, threads, smem, stream)
                : mode == kModeReg ? launch_mode<kModeReg, kDiel, kLossy, false, true>(p, sms, threads, smem, stream)
@@ -1126,7 +1133,8 @@ cudaError_t launch_accumulate(const TraceParams& p, int device_sms, cudaStream_t
 
 cudaError_t launch_trace(const TraceParams& p, int device_sms, cudaStream_t stream, uint64_t* launches) {
     const int threads = 128;
-    const int mode = (p.fan && !p.det) ? kModeFan : (trace_uses_register_accumulator(p) ? kModeReg : kModeDefer);
+    const int mode = (p.fan && !p.det) ? (p.fan_rows ? kModeFanRec : kModeFan)
+                                       : (trace_uses_register_accumulator(p) ? kModeReg : kModeDefer);
     size_t smem = 0;
     if (const char* v = std::getenv("MCSBR_EXTRA_SMEM")) smem += std::strtoul(v, nullptr, 10);  // A/B only
     // three physics instantiations: all-PEC (dielectric code compiled out),

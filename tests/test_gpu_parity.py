@@ -269,6 +269,43 @@ def test_bistatic_fan_equals_per_receiver_estimates():
     assert st.contributions == contribs
 
 
+
+@pytest.mark.parametrize("kind", ["uniform_nufft", "nonuniform_direct", "record_overflow", "lossy"])
+def test_bistatic_fan_multifrequency(kind, monkeypatch):
+    """Multi-frequency bistatic fans (F > 1: one record per visible
+    (contribution, receiver), row 32 a + lane) == one estimate per receiver,
+    and == the oracle on sampled receivers.  Uniform grids of >= 32
+    frequencies accumulate the rows by the bucketed NUFFT; other grids trace
+    receiver by receiver (the direct kernel would flush at every record of
+    a fan); a tiny record buffer sends the overflow lanes' adds straight
+    into their receivers' sums.  40 receivers: a full and a partial 32-lane
+    chunk."""
+    obj, mm = M.coated_sphere(subdivisions=2, lossless=kind != "lossy")
+    sd = M.load_scene(obj, mm)
+    s = M.Scene(sd)
+    cfg = M.McConfig(strata_per_wavelength=6, samples_per_stratum=1, seed=3, max_bounce=16,
+                     roulette=M.RouletteConfig(enabled=True, min_bounce=3))
+    freqs = np.array([2.7e9, 3.0e9, 3.4e9, 3.45e9]) if kind == "nonuniform_direct" else np.linspace(2.5e9, 3.5e9, 32)
+    if kind == "record_overflow":
+        monkeypatch.setenv("MCSBR_REC_CAP", "3000")
+    incs = [M.monostatic_excitation(90.0, 0.0), M.monostatic_excitation(60.0, 30.0)]
+    rx_thetas = np.linspace(0.0, 180.0, 40)
+    rxs = [[M.bistatic_excitation(th_i, ph_i, float(th), 0.0) for th in rx_thetas]
+           for th_i, ph_i in ((90.0, 0.0), (60.0, 30.0))]
+    vals, st = M.estimate_batch(s, [(e, 0.0) for e in incs], rxs, freqs, cfg)
+    assert vals.shape == (2, 40, 4, len(freqs))
+    contribs = 0
+    for i in range(2):
+        for r, exc in enumerate(rxs[i]):
+            single = M.estimate(s, exc, freqs, cfg)
+            contribs += single.stats.contributions
+            scale = max(np.max(np.abs(single.sweep.values)), 1e-300)
+            assert np.max(np.abs(vals[i, r] - single.sweep.values)) <= 1e-9 * scale, (i, r)
+            if kind != "lossy" and r % 19 == 0:
+                ref = oracle_estimate(sd, exc, freqs, cfg, contributions=False)
+                assert np.max(np.abs(vals[i, r] - ref["values"])) <= 1e-9 * scale
+    assert st.contributions == contribs
+
 def test_sweep_sharded_single_rank_equals_batch():
     """distributed.sweep_sharded (device buffers + finalize) == estimate_batch."""
     from paper_2511_07586_b200 import distributed as D
