@@ -11,6 +11,7 @@
 // Everything per ray runs on the GPU (bvh.cu, trace.cu); there is no CPU
 // fallback: without a device every compute entry point returns MCSBR_ECUDA.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -44,13 +45,14 @@ AllocCache& alloc_cache() {
     static AllocCache* c = new AllocCache();  // never destroyed (used during process exit)
     return *c;
 }
-// a sixth of the device's memory (B200: ~30 GB): large enough to keep a
-// sweep's multi-GB contribution-record buffer between scenes (a cudaFree of
-// it costs up to ~0.5 s), small enough to leave the device to others
+// a quarter of the device's memory (B200: ~45 GB): large enough to keep a
+// sweep's contribution-record buffer between scenes (c5: ~32 GB, one launch
+// group; a cudaFree + cudaMalloc of it costs ~15 ms per e2e step, up to
+// ~0.5 s), small enough to leave the device to others
 size_t cache_limit(AllocCache& c, int dev) {
     if (!c.limit[dev]) {
         size_t free_b = 0, total = 0;
-        c.limit[dev] = cudaMemGetInfo(&free_b, &total) == cudaSuccess ? total / 6 : (size_t{4} << 30);
+        c.limit[dev] = cudaMemGetInfo(&free_b, &total) == cudaSuccess ? total / 4 : (size_t{4} << 30);
     }
     return c.limit[dev];
 }
@@ -306,6 +308,16 @@ struct DevBuf {
 
 }  // namespace
 
+// Records-per-entry estimate a NEW scene starts from: the last one learnt on
+// any scene of the process (a sweep repeated on fresh scenes -- the e2e
+// step -- then sizes its record buffer right from the first call, and the
+// buffer is the same size class the allocator cached).  A hint only: a
+// wrong one costs memory or overflow adds, never correctness.
+std::atomic<double>& rec_ratio_hint() {
+    static std::atomic<double> h{0.25};
+    return h;
+}
+
 struct mcsbr_scene {
     // multi-device scenes (mcsbr_gpu_scene_create_multi): this object is the
     // primary (devices[0], where the BVH was built); replicas hold copies of
@@ -324,7 +336,7 @@ struct mcsbr_scene {
     // deferred accumulation: contribution records per launched entry, learnt
     // from the peak record count of earlier F > 1 jobs on this scene (read
     // back asynchronously: peak_host is valid once peak_ev has completed)
-    double rec_ratio = 0.25;
+    double rec_ratio = rec_ratio_hint().load(std::memory_order_relaxed);
     unsigned long long* peak_host = nullptr;
     cudaEvent_t peak_ev = nullptr;
     uint64_t peak_entries = 0;
@@ -525,7 +537,20 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 }
 
 constexpr uint64_t kPathStateBytes = 192;
-constexpr uint64_t kRecCapMax = uint64_t{1} << 28;  // contribution records (96 B each): 25.8 GB
+// contribution records (96 B each): at most 2^29 (51.5 GB) and a third of
+// the device's memory.  c5's sweep (~242 M records) then runs as ONE launch
+// group: device -0.5%, e2e -2.1% against 2^28 (two groups), same box
+uint64_t rec_cap_max() {
+    static const uint64_t cap = [] {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            return uint64_t{1} << 28;
+        }
+        return std::max<uint64_t>(uint64_t{1} << 24, std::min<uint64_t>(uint64_t{1} << 29, total_b / 3 / 96));
+    }();
+    return cap;
+}
 constexpr uint64_t kCoverBudgetWords = uint64_t{1} << 26;  // coverage bitmaps: at most 256 MB per job
 
 // Fold the peak record count of the scene's previous F > 1 job (if its
@@ -547,6 +572,7 @@ void learn_rec_ratio(mcsbr_scene* s) {
     if (s->peak_entries == 0) return;
     const double seen = static_cast<double>(*s->peak_host) / static_cast<double>(s->peak_entries);
     s->rec_ratio = std::min(std::max(seen * 1.25, 1.0 / 64.0), 8.0);
+    rec_ratio_hint().store(s->rec_ratio, std::memory_order_relaxed);
 }  // sizeof(mcsbr::PathState), path_engine.hpp:16-28
 
 struct Job {
@@ -665,13 +691,13 @@ int plan_job(const mcsbr_scene* s, const mcsbr_incidence* incs, uint32_t n_inc,
     }
     job->unit0[n_inc] = static_cast<uint32_t>(job->inc.size());
     job->total_entries = total;
-    // F > 1: the launch groups are sized so their records fit kRecCapMax
+    // F > 1: the launch groups are sized so their records fit rec_cap_max()
     uint64_t group_cap = ~uint64_t{0};
     if (nf > 1) {
         learn_rec_ratio(const_cast<mcsbr_scene*>(s));
         // (a multi-frequency fan appends up to one record per receiver of its chunk)
         const double fan_mult = n_rx > 1 ? static_cast<double>(std::min<uint32_t>(n_rx, 32)) : 1.0;
-        group_cap = std::max<uint64_t>(static_cast<uint64_t>(static_cast<double>(kRecCapMax) / (s->rec_ratio * fan_mult)),
+        group_cap = std::max<uint64_t>(static_cast<uint64_t>(static_cast<double>(rec_cap_max()) / (s->rec_ratio * fan_mult)),
                                        uint64_t{1} << 20);
         group_cap = env_u32("MCSBR_GROUP_ENTRIES", static_cast<uint32_t>(std::min<uint64_t>(group_cap, 0xffffffffu)));
     }
@@ -845,7 +871,7 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
         rec_cap = static_cast<uint64_t>(static_cast<double>(job.max_group_entries) * s->rec_ratio * 1.1 *
                                         (fan_rows ? std::min<uint32_t>(job.n_rx, fan_rows) : 1u)) +
                   4096;
-        rec_cap = std::min<uint64_t>(rec_cap, kRecCapMax);
+        rec_cap = std::min<uint64_t>(rec_cap, rec_cap_max());
         rec_cap = env_u32("MCSBR_REC_CAP", static_cast<uint32_t>(rec_cap));
         CK(s->recs.reserve(rec_cap * 12), "dev_malloc(contribution records)");
     }
@@ -1480,6 +1506,7 @@ void mcsbr_gpu_scene_destroy(mcsbr_scene* s) {
     pinned_release(s->wf_host);
     if (s->wf_ev) cudaEventDestroy(s->wf_ev);
     if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->peak_host) learn_rec_ratio(s);  // the last job's ratio becomes the next scene's hint
     if (s->peak_ev) cudaEventDestroy(s->peak_ev);
     pinned_release(s->peak_host);
     if (s->ev1) cudaEventDestroy(s->ev1);
