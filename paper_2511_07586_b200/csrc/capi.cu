@@ -12,6 +12,7 @@
 // fallback: without a device every compute entry point returns MCSBR_ECUDA.
 #include <algorithm>
 #include <atomic>
+#include <iterator>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -123,6 +124,18 @@ void dev_free(void* p, bool synced) {
     }
     const int dev = it->second.first;
     const size_t n = it->second.second;
+    if (dev >= 0 && dev < 64 && n <= cache_limit(c, dev)) {
+        // keep the block just freed (the one the next, similar call asks for)
+        // and hand older cached blocks back to the driver, largest first
+        auto& fb = c.free_blocks[dev];
+        while (c.cached[dev] + n > cache_limit(c, dev) && !fb.empty()) {
+            auto big = std::prev(fb.end());
+            cudaFree(big->second);
+            c.size_of.erase(big->second);
+            c.cached[dev] -= big->first;
+            fb.erase(big);
+        }
+    }
     if (dev < 0 || dev >= 64 || c.cached[dev] + n > cache_limit(c, dev)) {
         if (getenv("MCSBR_ALLOC_DEBUG") && n >= (size_t{16} << 20))
             fprintf(stderr, "[alloc] cudaFree %zu MB (cached %zu MB)\n", n >> 20, c.cached[dev] >> 20);
