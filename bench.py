@@ -473,7 +473,7 @@ def main():
         except Exception:
             pass
     # the cache-level picture of the same kernel from the committed ncu
-    # capture (one launch of the bench sweep): L1 / L2 bytes per launch, the
+    # capture (a 16-azimuth launch of the bench kernel): L1 / L2 bytes per launch, the
     # bandwidth they imply over that launch, and their share of the unit's
     # peak throughput as ncu reports it; issue-slot activity
     cache_roofs = None
