@@ -59,11 +59,30 @@ using namespace mcsbr_dev;
 constexpr int kRecWords = 12;  // contribution record: amp[4], s (re, im), incidence (pathcore.cuh kRecD2)
 constexpr int kSt = 6;         // staged record: c[4], (t, eta), incidence
 constexpr int kPolyN = kNufftPolyN;
+#ifndef MCSBR_SPREAD_POLY
+#define MCSBR_SPREAD_POLY estrin  // A/B: -DMCSBR_SPREAD_POLY=horner
+#endif
 
 __device__ __forceinline__ Cx csqrt_pos(Cx q) {  // principal root, Re q > 0 (no cancellation)
     const double r = sqrt(__fma_rn(q.re, q.re, q.im * q.im));
     const double sr = sqrt(0.5 * (r + q.re));
     return {sr, q.im / (2.0 * sr)};
+}
+
+// The same polynomial by Estrin's scheme: 16 operations in a dependency
+// chain 4 deep instead of Horner's 13 (the spread kernel's top stall is
+// the fixed-latency 'wait' on DFMA chains); the value differs from Horner's
+// by rounding only (~1e-16 relative, the kernel fit itself is 2e-13)
+__device__ __forceinline__ double estrin(const double (&cf)[kPolyN], double x) {
+    static_assert(kPolyN == 14, "estrin() is written for degree 13");
+    const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
+    const double p0 = __fma_rn(cf[1], x, cf[0]), p1 = __fma_rn(cf[3], x, cf[2]);
+    const double p2 = __fma_rn(cf[5], x, cf[4]), p3 = __fma_rn(cf[7], x, cf[6]);
+    const double p4 = __fma_rn(cf[9], x, cf[8]), p5 = __fma_rn(cf[11], x, cf[10]);
+    const double p6 = __fma_rn(cf[13], x, cf[12]);
+    const double q0 = __fma_rn(p1, x2, p0), q1 = __fma_rn(p3, x2, p2), q2 = __fma_rn(p5, x2, p4);
+    const double r0 = __fma_rn(q1, x4, q0), r1 = __fma_rn(p6, x4, q2);
+    return __fma_rn(r1, x8, r0);
 }
 
 __device__ __forceinline__ double horner(const double (&cf)[kPolyN], double x) {
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(64) spread_kernel(TraceParams P, NufftPlan Q) 
                         g1 = g1 < 0 ? g1 + static_cast<int>(ng) : (g1 >= static_cast<int>(ng) ? g1 - static_cast<int>(ng) : g1);
                         const double2 d0 = t1[2 * hh], d1 = t1[2 * hh + 1];
                         if (te.y == 0.0 && te1.y == 0.0) {
-                            const double w = horner(cf, x);
+                            const double w = MCSBR_SPREAD_POLY(cf, x);
                             const double wo = __shfl_xor_sync(0xffffffffu, w, 16);
                             add_real(Gh, ng, g, hh ? wo : w, c0, c1);
                             __syncwarp();
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(64) spread_kernel(TraceParams P, NufftPlan Q) 
                 // in x = 2 delta - 1 (+ j 2 Im delta for a complex offset)
                 const double x = __fma_rn(2.0, g0 - te.x, 15.0);
                 if (te.y == 0.0) {
-                    add_real(Gh, ng, g, horner(cf, x), c0, c1);
+                    add_real(Gh, ng, g, MCSBR_SPREAD_POLY(cf, x), c0, c1);
                 } else if (fabs(te.y) <= Q.eta_poly) {
                     add_cx(Gh, ng, g, horner_c(cf, x, -2.0 * te.y), c0, c1);
                 } else if (fabs(te.y) <= Q.eta_max) {
