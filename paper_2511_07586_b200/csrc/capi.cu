@@ -417,7 +417,7 @@ namespace {
 
 // scenes up to this many triangles get the long scheduling chunks (run_job)
 constexpr uint32_t kSmallSceneTris = 131072;
-constexpr uint32_t kLargeSceneTris = 524288;  // above: 512-entry chunk cap (c5), below 256 (c4)
+constexpr uint32_t kLargeSceneTris = 524288;  // above: 1024-entry chunk cap (c5), below 256 (c4)
 
 // launch_rect's axes (geometry.cpp:246-253): seed axis x, or y if |k.x| > 0.9
 void plan_axes(const double k_inc[3], V* k, V* u, V* v) {
@@ -992,8 +992,10 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     // (A/B knobs sanitised: chunk sizes non-zero multiples of 32, min <= max)
     // Measured (r02, same box): c5 (1 M triangles) 256 -> 512: path kernel
     // -2.2% (lossy) / -2.3% (lossless twin), accumulation unchanged; 1024:
-    // +0.7%; c4 (200 k) 256 -> 512: +8%.
-    const uint32_t cap_default = s->nt <= kSmallSceneTris ? 2048u : (s->nt <= kLargeSceneTris ? 256u : 512u);
+    // +0.7% while the sweep ran as two launch groups, -0.5% since it runs as
+    // one (446.9 vs 448.8 ms, 2048: 448.7; tools/ab_c5_knobs.sh); c4 (200 k)
+    // 256 -> 512: +8%.
+    const uint32_t cap_default = s->nt <= kSmallSceneTris ? 2048u : (s->nt <= kLargeSceneTris ? 256u : 1024u);
     p.chunk_max = std::max(32u, env_u32("MCSBR_CHUNK_MAX", cap_default) / 32u * 32u);
     p.chunk_min = std::min(p.chunk_max, std::max(32u, env_u32("MCSBR_CHUNK_MIN", 32) / 32u * 32u));
     p.gss_div = env_u32("MCSBR_GSS", 16);
