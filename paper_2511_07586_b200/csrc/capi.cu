@@ -998,13 +998,16 @@ int run_job(mcsbr_scene* s, const Job& job, uint32_t nf, const mcsbr_mc_config* 
     const uint32_t cap_default = s->nt <= kSmallSceneTris ? 2048u : (s->nt <= kLargeSceneTris ? 256u : 1024u);
     p.chunk_max = std::max(32u, env_u32("MCSBR_CHUNK_MAX", cap_default) / 32u * 32u);
     p.chunk_min = std::min(p.chunk_max, std::max(32u, env_u32("MCSBR_CHUNK_MIN", 32) / 32u * 32u));
-    p.gss_div = env_u32("MCSBR_GSS", 16);
+    // guided-scheduling divisor: chunk = remaining / (gss_div * warps).  Above
+    // 512 k triangles 32 with 16-row bands (below): c5 as one launch group
+    // 447.3 / 446.4 -> 442.8 / 444.1 ms (two alternations, same box)
+    p.gss_div = env_u32("MCSBR_GSS", s->nt > kLargeSceneTris ? 32u : 16u);
     // band height of the launch-entry dispatch order (0 = linear; a power of two)
     {
         // 8-row bands above 512 k triangles: c5 path kernel -1.6% (its
         // accumulation +3.8%: the records come out less ordered), 4 below
-        // (c4 +41% at 8)
-        const uint32_t bh = env_u32("MCSBR_BAND", s->nt > kLargeSceneTris ? 8u : 4u);
+        // (c4 +41% at 8); 16 rows (with gss 32) once c5 ran as one group
+        const uint32_t bh = env_u32("MCSBR_BAND", s->nt > kLargeSceneTris ? 16u : 4u);
         p.band_order = static_cast<int32_t>(bh & (bh - 1) ? 4 : bh);
     }
     p.uniform_f = job.uniform_f;
